@@ -351,6 +351,18 @@ oppo_status oppo_read_rollout(oppo_engine* e, int64_t id, int32_t* tokens, float
 oppo_status oppo_run_seed(oppo_engine* e, const oppo_run_config* cfg, uint64_t seed,
                           oppo_step_record* records, int32_t* n_records, int64_t* sel_ids);
 
+/* Prompt tokens of an admitted sequence (synthetic stream or caller-provided). */
+oppo_status oppo_read_prompt(oppo_engine* e, int64_t id, int32_t* out, int32_t cap, int32_t* len);
+
+/* Copies one weight tensor as fp32 (oracle parity).  model: 0 actor, 1 reward,
+ * 2 critic, 3 ref.  name: embed lm_head final_norm head wqkv bqkv wo wgu
+ * wdown ln1 ln2 (layer-indexed for the last seven). */
+oppo_status oppo_get_tensor(oppo_engine* e, int32_t model, const char* name, int32_t layer,
+                            float* out, int64_t cap, int64_t* n_out);
+
+/* Sets the thread-local message read by oppo_last_error_global(). */
+void oppo_set_global_error(const char* msg);
+
 /* --------------------------------------------- kernel-level entry points
  * Device pointers; used by the parity tests to drive one kernel at a time. */
 

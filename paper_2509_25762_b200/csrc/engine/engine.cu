@@ -1,0 +1,1449 @@
+// engine.cu — the GPU step executor behind oppo_run_step / oppo_ppo_update.
+//
+// One engine per GPU holds four Qwen2-style models (actor, reward, critic,
+// reference), a paged KV cache per model sharing one page table, per-slot
+// rollout buffers, and two streams:
+//   sa (high priority): actor — prompt prefill at admission, then one lockstep
+//       decode iteration per tick of the logical clock;
+//   ss (low priority): scorers — chunk "waves" of reward / critic / reference
+//       incremental prefill, each gated by an event recorded after the decode
+//       iteration that completed the chunk (streamed mode), or one wave after
+//       generation (sequential mode = overlap off).
+// The cut (stop_after-th finisher), chunk boundaries and carried progress come
+// from plan_step() (host), i.e. the reference's run_step under the lockstep
+// latency model; the GPU realises exactly that work.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "engine.cuh"
+#include "host/driver.hpp"
+#include "kernels/ppo.cuh"
+
+namespace oppo {
+
+namespace {
+
+constexpr float kRmsEps = 1e-6f;
+constexpr float kRopeTheta = 1e6f;
+
+template <class T> constexpr int dtype_of();
+template <> constexpr int dtype_of<float>() { return OPPO_DTYPE_F32; }
+template <> constexpr int dtype_of<__nv_bfloat16>() { return OPPO_DTYPE_BF16; }
+
+void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    OPPO_CUDA_CHECK(cudaMalloc(&p, bytes));
+    return p;
+}
+
+inline int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// ------------------------------------------------------------ arena upload
+struct Arena {  // one pinned host staging buffer -> one device buffer per step
+    std::vector<uint8_t> host;
+    void* dev = nullptr;
+    size_t cap = 0;
+    uint8_t* pinned = nullptr;
+    size_t pinned_cap = 0;
+    size_t push(const void* p, size_t bytes) {
+        const size_t off = (host.size() + 255) & ~size_t(255);
+        host.resize(off + bytes);
+        if (bytes) std::memcpy(host.data() + off, p, bytes);
+        return off;
+    }
+    template <class V> size_t push_vec(const std::vector<V>& v) {
+        return push(v.data(), v.size() * sizeof(V));
+    }
+    template <class V> V* at(size_t off) { return reinterpret_cast<V*>(static_cast<uint8_t*>(dev) + off); }
+    void upload(cudaStream_t st) {
+        if (host.size() > cap) {
+            if (dev) cudaFree(dev);
+            cap = host.size() * 2;
+            dev = dalloc(cap);
+        }
+        if (host.size() > pinned_cap) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned_cap = host.size() * 2;
+            OPPO_CUDA_CHECK(cudaMallocHost(&pinned, pinned_cap));
+        }
+        std::memcpy(pinned, host.data(), host.size());
+        if (!host.empty())
+            OPPO_CUDA_CHECK(cudaMemcpyAsync(dev, pinned, host.size(), cudaMemcpyHostToDevice, st));
+    }
+    void release() {
+        if (dev) cudaFree(dev);
+        if (pinned) cudaFreeHost(pinned);
+        dev = nullptr;
+        pinned = nullptr;
+        cap = pinned_cap = 0;
+    }
+};
+
+struct EngineExtra {
+    Arena step_arena, admit_arena, upd_arena;
+};
+std::unordered_map<const Engine*, EngineExtra> g_extra;
+
+// --------------------------------------------------------------- weights
+template <class T>
+void init_tensor(T* p, int64_t n, uint64_t seed, uint64_t id, float std_, cudaStream_t st) {
+    if (n <= 0) return;
+    init_normal<T><<<cdiv(n, 256), 256, 0, st>>>(p, n, seed, id, std_);
+}
+template <class T>
+void fill_tensor(T* p, int64_t n, float v, cudaStream_t st) {
+    if (n <= 0) return;
+    fill_value<T><<<cdiv(n, 256), 256, 0, st>>>(p, n, v);
+}
+
+template <class T>
+void build_model(Engine& e, Model& m, int id, cudaStream_t st) {
+    const auto& d = m.dims;
+    const uint64_t seed = e.cfg.weight_seed;
+    auto tid = [&](int layer, int t) {
+        return (static_cast<uint64_t>(id) << 40) | (static_cast<uint64_t>(layer + 1) << 8) | t;
+    };
+    const int64_t V = d.vocab, D = d.d_model;
+    m.embed = dalloc(V * D * sizeof(T));
+    init_tensor(static_cast<T*>(m.embed), V * D, seed, tid(-1, 0), 0.02f, st);
+    if (d.tied) {
+        m.lm_head = m.embed;
+    } else {
+        m.lm_head = dalloc(V * D * sizeof(T));
+        init_tensor(static_cast<T*>(m.lm_head), V * D, seed, tid(-1, 1), 0.02f, st);
+    }
+    const int64_t qkv = m.qkv_width(), qw = m.q_width(), F = d.d_ff;
+    m.layers.resize(d.n_layers);
+    for (int l = 0; l < d.n_layers; ++l) {
+        auto& L = m.layers[l];
+        L.wqkv = dalloc(qkv * D * sizeof(T));
+        L.bqkv = static_cast<float*>(dalloc(qkv * sizeof(float)));
+        L.wo = dalloc(D * qw * sizeof(T));
+        L.wgu = dalloc(2 * F * D * sizeof(T));
+        L.wdown = dalloc(D * F * sizeof(T));
+        L.ln1 = static_cast<float*>(dalloc(D * sizeof(float)));
+        L.ln2 = static_cast<float*>(dalloc(D * sizeof(float)));
+        init_tensor(static_cast<T*>(L.wqkv), qkv * D, seed, tid(l, 1), 0.02f, st);
+        init_tensor(L.bqkv, qkv, seed, tid(l, 2), 0.02f, st);
+        init_tensor(static_cast<T*>(L.wo), D * qw, seed, tid(l, 3), 0.02f, st);
+        init_tensor(static_cast<T*>(L.wgu), 2 * F * D, seed, tid(l, 4), 0.02f, st);
+        init_tensor(static_cast<T*>(L.wdown), D * F, seed, tid(l, 5), 0.02f, st);
+        fill_tensor(L.ln1, D, 1.0f, st);
+        fill_tensor(L.ln2, D, 1.0f, st);
+    }
+    m.final_norm = static_cast<float*>(dalloc(D * sizeof(float)));
+    fill_tensor(m.final_norm, D, 1.0f, st);
+    if (id == REWARD || id == CRITIC) {
+        m.head = static_cast<float*>(dalloc(D * sizeof(float)));
+        init_tensor(m.head, D, seed, tid(-1, 7), id == REWARD ? 0.5f : 0.02f, st);
+    }
+    // KV pools
+    m.layer_stride = static_cast<int64_t>(e.n_pages) * d.n_kv_heads * e.page_size * d.head_dim;
+    const size_t kvb = static_cast<size_t>(m.layer_stride) * d.n_layers * sizeof(T);
+    m.k_pool = dalloc(kvb);
+    m.v_pool = dalloc(kvb);
+    OPPO_CUDA_CHECK(cudaMemsetAsync(m.k_pool, 0, kvb, st));
+    OPPO_CUDA_CHECK(cudaMemsetAsync(m.v_pool, 0, kvb, st));
+    m.used = true;
+}
+
+void check_dims(const oppo_model_dims& d, const char* who) {
+    auto bad = [&](const std::string& m) { config_error(std::string(who) + ": " + m); };
+    if (d.n_layers < 1 || d.d_model < 64 || d.d_model % 64) bad("d_model must be a multiple of 64");
+    if (d.n_heads < 1 || d.n_kv_heads < 1 || d.n_heads % d.n_kv_heads)
+        bad("n_heads must be a multiple of n_kv_heads");
+    if (d.head_dim != 32 && d.head_dim != 64 && d.head_dim != 128) bad("head_dim must be 32/64/128");
+    if (d.d_ff < 64 || d.d_ff % 64) bad("d_ff must be a multiple of 64");
+    if (d.vocab < 2) bad("vocab must be >= 2");
+    if ((d.n_heads * d.head_dim) % 64) bad("n_heads*head_dim must be a multiple of 64");
+}
+
+template <class T>
+void alloc_work(Engine& e, Work& w, int rows, bool lm_rows) {
+    int dmax = 0, qkvmax = 0, qmax = 0, fmax_ = 0, vmax = 0, hmax = 0, hdmax = 0;
+    for (auto& m : e.models) {
+        if (!m.used) continue;
+        dmax = std::max(dmax, m.dims.d_model);
+        qkvmax = std::max(qkvmax, m.qkv_width());
+        qmax = std::max(qmax, m.q_width());
+        fmax_ = std::max(fmax_, m.dims.d_ff);
+        vmax = std::max(vmax, m.dims.vocab);
+        hmax = std::max(hmax, m.dims.n_heads);
+        hdmax = std::max(hdmax, m.dims.head_dim);
+    }
+    w.max_rows = rows;
+    const size_t R = rows;
+    w.meta.slot = static_cast<int32_t*>(dalloc(R * 4));
+    w.meta.pos = static_cast<int32_t*>(dalloc(R * 4));
+    w.meta.tok = static_cast<int32_t*>(dalloc(R * 4));
+    w.meta.t = static_cast<int32_t*>(dalloc(R * 4));
+    w.meta.key = static_cast<uint64_t*>(dalloc(R * 8));
+    w.x = static_cast<float*>(dalloc(R * dmax * 4));
+    w.h = dalloc(R * dmax * sizeof(T));
+    w.qkv = dalloc(R * qkvmax * sizeof(T));
+    w.q = dalloc(R * qmax * sizeof(T));
+    w.attn = dalloc(R * qmax * sizeof(T));
+    w.ff = dalloc(R * fmax_ * sizeof(T));
+    w.head_out = static_cast<float*>(dalloc(R * 4));
+    const int lm_R = lm_rows ? rows : rows;
+    w.partials = static_cast<float4*>(dalloc(static_cast<size_t>(lm_R) * cdiv(vmax, 128) * 16));
+    w.tgt_logit = static_cast<float*>(dalloc(R * 4));
+    w.lse = static_cast<float*>(dalloc(R * 4));
+    w.lm_in = dalloc(R * dmax * sizeof(T));
+    w.lm_tgt = static_cast<int32_t*>(dalloc(R * 4));
+    w.lm_slot = static_cast<int32_t*>(dalloc(R * 4));
+    w.lm_t = static_cast<int32_t*>(dalloc(R * 4));
+    w.gemm_ws_floats = static_cast<size_t>(16) << 20;  // 64 MB
+    w.gemm_ws = static_cast<float*>(dalloc(w.gemm_ws_floats * 4));
+    w.gemm_cnt_n = 1 << 16;
+    w.gemm_cnt = static_cast<int*>(dalloc(w.gemm_cnt_n * 4));
+    OPPO_CUDA_CHECK(cudaMemset(w.gemm_cnt, 0, w.gemm_cnt_n * 4));
+    w.attn_ws_rows = std::max<size_t>(R * hmax * 8, static_cast<size_t>(e.num_sms) * 64);
+    w.attn_ws_o = static_cast<float*>(dalloc(w.attn_ws_rows * hdmax * 4));
+    w.attn_ws_ml = static_cast<float*>(dalloc(w.attn_ws_rows * 2 * 4));
+}
+
+// --------------------------------------------------------------- forward
+template <class T>
+void launch_attn_decode(int hd, int G, dim3 grid, cudaStream_t st, const T* q, T* out,
+                        const KvView& kv, int layer, const int32_t* slot, const int32_t* pos,
+                        int rows, int split_len, float* wo, float* wml) {
+#define OPPO_ATTN(HD_, G_)                                                                   \
+    if (hd == HD_ && G == G_) {                                                              \
+        attn_decode<T, HD_, G_><<<grid, 128, 0, st>>>(q, out, kv, layer, slot, pos, rows,     \
+                                                     split_len, wo, wml);                    \
+        return;                                                                              \
+    }
+    OPPO_ATTN(32, 1)
+    OPPO_ATTN(32, 2)
+    OPPO_ATTN(64, 1)
+    OPPO_ATTN(64, 2)
+    OPPO_ATTN(64, 7)
+    OPPO_ATTN(128, 1)
+    OPPO_ATTN(128, 6)
+    OPPO_ATTN(128, 7)
+#undef OPPO_ATTN
+    config_error("unsupported (head_dim, q heads per kv head) = (" + std::to_string(hd) + ", " +
+                 std::to_string(G) + ")");
+}
+
+template <class T>
+void launch_attn_prefill(int hd, dim3 grid, cudaStream_t st, const T* q, T* out, const KvView& kv,
+                         int layer, const QBlock* blocks, int n_heads) {
+    if (hd == 32) attn_prefill<T, 32><<<grid, 128, 0, st>>>(q, out, kv, layer, blocks, n_heads);
+    else if (hd == 64) attn_prefill<T, 64><<<grid, 128, 0, st>>>(q, out, kv, layer, blocks, n_heads);
+    else attn_prefill<T, 128><<<grid, 128, 0, st>>>(q, out, kv, layer, blocks, n_heads);
+}
+
+template <class T>
+struct Final {
+    bool write_h = true;
+    const float* head = nullptr;
+    T* cache = nullptr;  // per-slot hidden cache [S, tok_stride, d]
+    int t_lo = 1, t_hi = 0;
+};
+
+template <class T>
+void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, int max_ctx,
+             const QBlock* qblocks, int n_qblocks, const Final<T>& fin) {
+    const auto& d = m.dims;
+    const int D = d.d_model, H = d.n_heads, KV = d.n_kv_heads, hd = d.head_dim;
+    const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
+    embed_rows<T><<<R, 128, 0, st>>>(static_cast<const T*>(m.embed), w.meta.tok, w.x, R, D);
+    const int nrm_blocks = cdiv(R, 4);
+    int splits = 1, split_len = std::max(1, max_ctx);
+    if (decode) {
+        const int base = R * KV;
+        const int want = cdiv(2 * e.num_sms, base);
+        splits = std::max(1, std::min({want, cdiv(max_ctx, 128), 32}));
+        while (splits > 1 && static_cast<size_t>(R) * H * splits > w.attn_ws_rows) --splits;
+        split_len = cdiv(max_ctx, splits);
+    }
+    for (int l = 0; l < d.n_layers; ++l) {
+        const auto& L = m.layers[l];
+        rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(w.x, L.ln1, static_cast<T*>(w.h), R, D, kRmsEps,
+                                                    nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
+        EpiParams ep{};
+        ep.mode = EPI_STORE;
+        ep.y = w.qkv;
+        ep.ldy = m.qkv_width();
+        ep.bias = L.bqkv;
+        ep.scale = 1.f;
+        gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
+        rope_append<T><<<R, 128, 0, st>>>(static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l,
+                                          w.meta.slot, w.meta.pos, R, H, kRopeTheta);
+        if (decode) {
+            launch_attn_decode<T>(hd, H / KV, dim3(R, KV, splits), st, static_cast<const T*>(w.q),
+                                  static_cast<T*>(w.attn), kv, l, w.meta.slot, w.meta.pos, R,
+                                  split_len, w.attn_ws_o, w.attn_ws_ml);
+            if (splits > 1)
+                attn_split_combine<T><<<dim3(R, H), 64, 0, st>>>(w.attn_ws_o, w.attn_ws_ml,
+                                                                static_cast<T*>(w.attn), R, H, hd,
+                                                                splits);
+        } else {
+            launch_attn_prefill<T>(hd, dim3(n_qblocks, H), st, static_cast<const T*>(w.q),
+                                   static_cast<T*>(w.attn), kv, l, qblocks, H);
+        }
+        ep = EpiParams{};
+        ep.mode = EPI_ADD_F32;
+        ep.y = w.x;
+        ep.ldy = D;
+        ep.scale = 1.f;
+        gemm_run(e, w, st, w.attn, R, m.q_width(), m.q_width(), L.wo, D, m.q_width(), ep);
+        rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(w.x, L.ln2, static_cast<T*>(w.h), R, D, kRmsEps,
+                                                    nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
+        ep = EpiParams{};
+        ep.mode = EPI_SWIGLU;
+        ep.y = w.ff;
+        ep.ldy = d.d_ff;
+        ep.scale = 1.f;
+        gemm_run(e, w, st, w.h, R, D, D, L.wgu, 2 * d.d_ff, D, ep);
+        ep = EpiParams{};
+        ep.mode = EPI_ADD_F32;
+        ep.y = w.x;
+        ep.ldy = D;
+        ep.scale = 1.f;
+        gemm_run(e, w, st, w.ff, R, d.d_ff, d.d_ff, L.wdown, D, d.d_ff, ep);
+        e.launches += 6 + (splits > 1);
+    }
+    rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(
+        w.x, m.final_norm, fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, fin.head,
+        w.head_out, fin.cache, w.meta.slot, w.meta.t, e.tok_stride, fin.t_lo, fin.t_hi);
+    e.launches += 2;
+    OPPO_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace
+
+// =================================================================== create
+Engine* engine_new(const oppo_engine_cfg& cfg) {
+    auto* e = new Engine();
+    e->cfg = cfg;
+    try {
+        e->dtype = cfg.dtype;
+        if (cfg.dtype != OPPO_DTYPE_F32 && cfg.dtype != OPPO_DTYPE_BF16)
+            config_error("dtype must be f32 or bf16");
+        e->esz = cfg.dtype == OPPO_DTYPE_F32 ? 4 : 2;
+        const oppo_model_dims* dims[N_MODELS] = {&cfg.actor, &cfg.reward, &cfg.critic, &cfg.ref};
+        const char* names[N_MODELS] = {"actor", "reward", "critic", "ref"};
+        for (int i = 0; i < N_MODELS; ++i) {
+            check_dims(*dims[i], names[i]);
+            e->models[i].dims = *dims[i];
+        }
+        const int V = cfg.actor.vocab;
+        if (cfg.ref.vocab != V) config_error("actor and ref must share one vocabulary");
+        if (cfg.reward.vocab != V || cfg.critic.vocab != V)
+            config_error("all models must share one vocabulary (SURVEY 2.4)");
+        if (cfg.max_slots < 1) config_error("max_slots must be >= 1");
+        if (cfg.max_prompt_len < 1 || cfg.max_response_len < 1)
+            config_error("max prompt/response lengths must be >= 1");
+        OPPO_CUDA_CHECK(cudaSetDevice(cfg.device));
+        OPPO_CUDA_CHECK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, cfg.device));
+        int lo = 0, hi = 0;
+        OPPO_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
+        OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
+        for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done})
+            OPPO_CUDA_CHECK(cudaEventCreate(ev));
+
+        e->S = cfg.max_slots;
+        e->Pmax = cfg.max_prompt_len;
+        e->Lmax = cfg.max_response_len;
+        e->page_size = cfg.page_size > 0 ? cfg.page_size : 64;
+        e->max_pages = cdiv(e->Pmax + e->Lmax + 1, e->page_size);
+        e->n_pages = cfg.kv_pages > 0 ? cfg.kv_pages : e->S * e->max_pages;
+        e->tok_stride = e->Lmax + 2;
+        for (int s = e->S - 1; s >= 0; --s) e->free_slots.push_back(s);
+        for (int p = e->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
+        e->slots.resize(e->S);
+
+        const size_t S = e->S, TS = e->tok_stride;
+        e->d_page_table = static_cast<int32_t*>(dalloc(S * e->max_pages * 4));
+        OPPO_CUDA_CHECK(cudaMemset(e->d_page_table, 0, S * e->max_pages * 4));
+        e->d_prompt = static_cast<int32_t*>(dalloc(S * e->Pmax * 4));
+        e->d_tok = static_cast<int32_t*>(dalloc(S * TS * 4));
+        OPPO_CUDA_CHECK(cudaMemset(e->d_tok, 0, S * TS * 4));
+        e->d_old_lp = static_cast<float*>(dalloc(S * TS * 4));
+        e->d_ref_lp = static_cast<float*>(dalloc(S * TS * 4));
+        e->d_values = static_cast<float*>(dalloc(S * TS * 4));
+        OPPO_CUDA_CHECK(cudaMemset(e->d_values, 0, S * TS * 4));
+        OPPO_CUDA_CHECK(cudaMemset(e->d_ref_lp, 0, S * TS * 4));
+        e->d_reward = static_cast<float*>(dalloc(S * 4));
+        e->d_target_len = static_cast<int32_t*>(dalloc(S * 4));
+        e->d_hf_actor = dalloc(S * TS * cfg.actor.d_model * e->esz);
+        e->d_hf_critic = dalloc(S * TS * cfg.critic.d_model * e->esz);
+        e->d_ref_pending = dalloc(S * cfg.ref.d_model * e->esz);
+
+        cudaStream_t st = e->sa;
+        for (int i = 0; i < N_MODELS; ++i) {
+            if (e->dtype == OPPO_DTYPE_F32) build_model<float>(*e, e->models[i], i, st);
+            else build_model<__nv_bfloat16>(*e, e->models[i], i, st);
+        }
+        if (cfg.train_heads) {
+            auto& a = e->models[ACTOR];
+            const size_t n = static_cast<size_t>(a.dims.vocab) * a.dims.d_model;
+            a.lm_master = static_cast<float*>(dalloc(n * 4));
+            if (e->dtype == OPPO_DTYPE_F32)
+                convert<float, float><<<cdiv(n, 256), 256, 0, st>>>(static_cast<float*>(a.lm_head), a.lm_master, n);
+            else
+                convert<__nv_bfloat16, float><<<cdiv(n, 256), 256, 0, st>>>(
+                    static_cast<__nv_bfloat16*>(a.lm_head), a.lm_master, n);
+        }
+        e->prefill_rows = std::max(1024, std::min(8192, e->S * (e->Pmax + 64)));
+        if (e->dtype == OPPO_DTYPE_F32) {
+            alloc_work<float>(*e, e->wa, std::max(e->S, 32), false);
+            alloc_work<float>(*e, e->ws, e->prefill_rows, true);
+        } else {
+            alloc_work<__nv_bfloat16>(*e, e->wa, std::max(e->S, 32), false);
+            alloc_work<__nv_bfloat16>(*e, e->ws, e->prefill_rows, true);
+        }
+        e->nccl = cfg.nccl_comm;
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
+        g_extra[e];
+    } catch (...) {
+        engine_free(e);
+        throw;
+    }
+    return e;
+}
+
+void engine_free(Engine* e) {
+    if (!e) return;
+    cudaDeviceSynchronize();
+    auto it = g_extra.find(e);
+    if (it != g_extra.end()) {
+        it->second.step_arena.release();
+        it->second.admit_arena.release();
+        it->second.upd_arena.release();
+        g_extra.erase(it);
+    }
+    // device memory is reclaimed with the process/context; free the big pools explicitly
+    for (auto& m : e->models) {
+        if (!m.used) continue;
+        cudaFree(m.k_pool);
+        cudaFree(m.v_pool);
+        for (auto& L : m.layers) {
+            cudaFree(L.wqkv);
+            cudaFree(L.bqkv);
+            cudaFree(L.wo);
+            cudaFree(L.wgu);
+            cudaFree(L.wdown);
+            cudaFree(L.ln1);
+            cudaFree(L.ln2);
+        }
+        if (m.lm_head != m.embed) cudaFree(m.lm_head);
+        cudaFree(m.embed);
+        cudaFree(m.final_norm);
+        if (m.head) cudaFree(m.head);
+        if (m.lm_master) cudaFree(m.lm_master);
+    }
+    for (void* p : {static_cast<void*>(e->d_hf_actor), static_cast<void*>(e->d_hf_critic),
+                    static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf})
+        if (p) cudaFree(p);
+    if (e->sa) cudaStreamDestroy(e->sa);
+    if (e->ss) cudaStreamDestroy(e->ss);
+    delete e;
+}
+
+// =================================================================== admit
+namespace {
+
+void open_step(Engine& e) {
+    if (e.step_open) return;
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_begin, e.sa));
+    e.step_open = true;
+    e.launches = 0;
+}
+
+template <class T>
+void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* prompts) {
+    open_step(e);
+    std::vector<int32_t> slots, lens;
+    std::vector<int64_t> ids;
+    std::vector<int32_t> pt_rows;  // page-table rows, S x max_pages layout subset
+    std::vector<int32_t> tlen;
+    for (int i = 0; i < n; ++i) {
+        const auto& s = seqs[i];
+        if (e.slot_of.count(s.id)) input_error("sequence " + std::to_string(s.id) + " already admitted");
+        if (s.prompt_len < 1 || s.prompt_len > e.Pmax) input_error("prompt_len outside [1, max_prompt_len]");
+        if (s.target_len < 1 || s.target_len > e.Lmax)
+            input_error("target_len outside [1, max_response_len]");
+        if (e.free_slots.empty()) input_error("no free slot (raise max_slots)");
+        const int need = cdiv(s.prompt_len + s.target_len + 1, e.page_size);
+        if (static_cast<int>(e.free_pages.size()) < need) input_error("KV page pool exhausted");
+        const int slot = e.free_slots.back();
+        e.free_slots.pop_back();
+        auto& info = e.slots[slot];
+        info = SlotInfo{};
+        info.id = s.id;
+        info.prompt_len = s.prompt_len;
+        info.target_len = s.target_len;
+        for (int p = 0; p < need; ++p) {
+            info.pages.push_back(e.free_pages.back());
+            e.free_pages.pop_back();
+        }
+        e.slot_of[s.id] = slot;
+        slots.push_back(slot);
+        lens.push_back(s.prompt_len);
+        ids.push_back(s.id);
+        tlen.push_back(s.target_len);
+    }
+    if (n == 0) return;
+    auto& A = g_extra[&e].admit_arena;
+    A.host.clear();
+    // page table rows
+    std::vector<int32_t> rows(static_cast<size_t>(n) * e.max_pages, 0);
+    for (int i = 0; i < n; ++i) {
+        const auto& pg = e.slots[slots[i]].pages;
+        std::copy(pg.begin(), pg.end(), rows.begin() + static_cast<size_t>(i) * e.max_pages);
+    }
+    const size_t o_rows = A.push_vec(rows), o_slots = A.push_vec(slots), o_lens = A.push_vec(lens),
+                 o_ids = A.push_vec(ids), o_tlen = A.push_vec(tlen);
+    size_t o_prompts = 0;
+    if (prompts) {
+        size_t tot = 0;
+        for (int i = 0; i < n; ++i) tot += lens[i];
+        o_prompts = A.push(prompts, tot * 4);
+    }
+    // actor prompt prefill: positions 0..P-2 (the last prompt token feeds decode step 1)
+    std::vector<Segment> segs;
+    std::vector<QBlock> qbs;
+    int rows_total = 0;
+    for (int i = 0; i < n; ++i) {
+        const int np = lens[i] - 1;
+        if (np <= 0) continue;
+        segs.push_back({slots[i], 0, np, rows_total, lens[i], 0});
+        for (int b = 0; b < np; b += 32)
+            qbs.push_back({rows_total + b, std::min(32, np - b), slots[i], b});
+        rows_total += np;
+    }
+    const size_t o_segs = A.push_vec(segs), o_qbs = A.push_vec(qbs);
+    A.upload(e.sa);
+    cudaStream_t st = e.sa;
+    for (int i = 0; i < n; ++i)
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_page_table + static_cast<size_t>(slots[i]) * e.max_pages,
+                                        A.at<int32_t>(o_rows) + static_cast<size_t>(i) * e.max_pages,
+                                        e.max_pages * 4, cudaMemcpyDeviceToDevice, st));
+    // target lengths
+    {
+        // scatter target_len by slot
+        for (int i = 0; i < n; ++i)
+            OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_target_len + slots[i], A.at<int32_t>(o_tlen) + i, 4,
+                                            cudaMemcpyDeviceToDevice, st));
+    }
+    if (prompts) {
+        size_t off = 0;
+        for (int i = 0; i < n; ++i) {
+            OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_prompt + static_cast<size_t>(slots[i]) * e.Pmax,
+                                            A.at<int32_t>(o_prompts) + off, lens[i] * 4,
+                                            cudaMemcpyDeviceToDevice, st));
+            off += lens[i];
+        }
+    } else {
+        prompt_tokens<<<n, 128, 0, st>>>(e.d_prompt, e.Pmax, A.at<int32_t>(o_slots),
+                                         A.at<int64_t>(o_ids), A.at<int32_t>(o_lens), n,
+                                         e.cfg.sample_seed, e.models[ACTOR].dims.vocab);
+    }
+    // prefill in passes of <= wa.max_rows rows (segments are whole prompts here)
+    Work& w = e.ws;  // the scorer workspace has prefill-sized buffers; the scorer stream is idle
+    size_t si = 0;
+    while (si < segs.size()) {
+        size_t sj = si;
+        int rows_pass = 0;
+        while (sj < segs.size() && (rows_pass + segs[sj].n <= w.max_rows || sj == si)) {
+            rows_pass += segs[sj].n;
+            ++sj;
+        }
+        if (rows_pass > w.max_rows) input_error("prompt longer than the prefill workspace");
+        // rebase rows of this pass
+        std::vector<Segment> ps(segs.begin() + si, segs.begin() + sj);
+        std::vector<QBlock> pq;
+        const int base = segs[si].row0;
+        for (auto& s : ps) s.row0 -= base;
+        for (const auto& q : qbs)
+            if (q.row0 >= base && q.row0 < base + rows_pass) {
+                QBlock b = q;
+                b.row0 -= base;
+                pq.push_back(b);
+            }
+        auto& B = g_extra[&e].step_arena;  // reuse step arena's device buffer is unsafe; use pass-local upload
+        (void)B;
+        Arena pa;
+        pa.push_vec(ps);
+        const size_t oq = pa.push_vec(pq);
+        pa.upload(st);
+        segment_rows<<<static_cast<int>(ps.size()), 128, 0, st>>>(pa.at<Segment>(0), e.d_prompt, e.Pmax,
+                                                                 e.d_tok, e.tok_stride, w.meta);
+        Final<T> fin;
+        fin.write_h = false;
+        forward<T>(e, e.models[ACTOR], w, st, rows_pass, false, 0, pa.at<QBlock>(oq),
+                   static_cast<int>(pq.size()), fin);
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // pass-local arena is released below
+        pa.release();
+        si = sj;
+    }
+    (void)o_segs;
+    (void)o_qbs;
+}
+
+}  // namespace
+
+// ================================================================ run_step
+namespace {
+
+struct PassPlan {
+    size_t seg_off = 0, qb_off = 0, lm_off = 0, pend_off = 0;
+    int n_seg = 0, n_qb = 0, rows = 0, n_lm = 0, n_pend = 0;
+};
+struct WavePlan {
+    int at_iter = 0;  // 0 = before decode
+    std::vector<PassPlan> passes;
+};
+
+struct SegReq {
+    int slot, pos0, n, prompt_len;
+};
+
+// Splits a wave's segments into passes of <= cap rows and builds the
+// reference-model lm_head rows (pending resolution) for each pass.
+void build_passes(Engine& e, std::vector<SegReq>& reqs, WavePlan& wave, Arena& A) {
+    const int cap = e.ws.max_rows;
+    size_t i = 0;
+    int off_in_seg = 0;
+    while (i < reqs.size()) {
+        std::vector<Segment> segs;
+        std::vector<QBlock> qbs;
+        std::vector<LmRow> lms;
+        std::vector<int32_t> psrc, pslot;
+        int rows = 0;
+        while (i < reqs.size() && rows < cap) {
+            const SegReq& r = reqs[i];
+            const int take = std::min(r.n - off_in_seg, cap - rows);
+            const int pos0 = r.pos0 + off_in_seg;
+            segs.push_back({r.slot, pos0, take, rows, r.prompt_len, 0});
+            for (int b = 0; b < take; b += 32)
+                qbs.push_back({rows + b, std::min(32, take - b), r.slot, pos0 + b});
+            auto& info = e.slots[r.slot];
+            const int P = r.prompt_len, L = info.target_len;
+            // resolve this slot's pending reference row: its target is the token at pos0
+            if (info.ref_pending) {
+                lms.push_back({-(r.slot + 1), r.slot, pos0 - P + 1, 0});
+                info.ref_pending = false;
+            }
+            for (int k = 0; k < take; ++k) {
+                const int q = pos0 + k, t = q - P + 2;  // target response index of row q
+                if (t < 1 || t > L) continue;
+                if (k + 1 < take) {
+                    lms.push_back({rows + k, r.slot, t, 0});
+                } else {  // target not in this pass yet
+                    psrc.push_back(rows + k);
+                    pslot.push_back(r.slot);
+                    info.ref_pending = true;
+                }
+            }
+            rows += take;
+            off_in_seg += take;
+            if (off_in_seg >= r.n) {
+                ++i;
+                off_in_seg = 0;
+            }
+        }
+        PassPlan p;
+        p.seg_off = A.push_vec(segs);
+        p.n_seg = static_cast<int>(segs.size());
+        p.qb_off = A.push_vec(qbs);
+        p.n_qb = static_cast<int>(qbs.size());
+        p.lm_off = A.push_vec(lms);
+        p.n_lm = static_cast<int>(lms.size());
+        p.pend_off = A.push_vec(psrc);
+        A.push_vec(pslot);
+        p.n_pend = static_cast<int>(psrc.size());
+        p.rows = rows;
+        wave.passes.push_back(p);
+    }
+}
+
+template <class T>
+void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, int64_t& tokens) {
+    Work& w = e.ws;
+    segment_rows<<<p.n_seg, 128, 0, st>>>(A.at<Segment>(p.seg_off), e.d_prompt, e.Pmax, e.d_tok,
+                                          e.tok_stride, w.meta);
+    const QBlock* qb = A.at<QBlock>(p.qb_off);
+    tokens += p.rows;
+    // reward model: last-token scalar head
+    {
+        Final<T> fin;
+        fin.write_h = false;
+        fin.head = e.models[REWARD].head;
+        forward<T>(e, e.models[REWARD], w, st, p.rows, false, 0, qb, p.n_qb, fin);
+        reward_rows<<<cdiv(p.rows, 256), 256, 0, st>>>(w.head_out, w.meta.slot, w.meta.t, p.rows,
+                                                       e.d_target_len, e.d_reward);
+    }
+    // critic: per-token value head (state before token t) + hidden cache for the head update
+    {
+        Final<T> fin;
+        fin.write_h = false;
+        fin.head = e.models[CRITIC].head;
+        fin.cache = static_cast<T*>(e.d_hf_critic);
+        fin.t_lo = 1;
+        fin.t_hi = e.Lmax;
+        forward<T>(e, e.models[CRITIC], w, st, p.rows, false, 0, qb, p.n_qb, fin);
+        scatter_rows<<<cdiv(p.rows, 256), 256, 0, st>>>(w.head_out, w.meta.slot, w.meta.t, p.rows,
+                                                        e.d_values, e.tok_stride, 1, e.d_target_len, 0);
+    }
+    // reference: log-probs of the actor's tokens (lm_head + log-sum-exp)
+    {
+        Model& m = e.models[REF];
+        Final<T> fin;
+        fin.write_h = true;
+        forward<T>(e, m, w, st, p.rows, false, 0, qb, p.n_qb, fin);
+        const int D = m.dims.d_model;
+        if (p.n_lm > 0) {
+            gather_lm_rows<T><<<p.n_lm, 128, 0, st>>>(A.at<LmRow>(p.lm_off), p.n_lm,
+                                                      static_cast<const T*>(w.h),
+                                                      static_cast<const T*>(e.d_ref_pending), D,
+                                                      e.d_tok, e.tok_stride, static_cast<T*>(w.lm_in),
+                                                      w.lm_tgt, w.lm_slot, w.lm_t);
+            EpiParams ep{};
+            ep.mode = EPI_LOGITS;
+            ep.partials = w.partials;
+            ep.tgt_logit = w.tgt_logit;
+            ep.targets = w.lm_tgt;
+            ep.keys = nullptr;
+            gemm_run(e, w, st, w.lm_in, p.n_lm, D, D, m.lm_head, m.dims.vocab, D, ep);
+            logits_combine<<<cdiv(p.n_lm, 4), 128, 0, st>>>(
+                w.partials, cdiv(m.dims.vocab, 128), p.n_lm, nullptr, w.tgt_logit, w.lm_slot, w.lm_t,
+                nullptr, e.d_ref_lp, e.tok_stride, nullptr, nullptr);
+        }
+        if (p.n_pend > 0)
+            store_pending<T><<<p.n_pend, 128, 0, st>>>(A.at<int32_t>(p.pend_off),
+                                                       A.at<int32_t>(p.pend_off) + p.n_pend, p.n_pend,
+                                                       static_cast<const T*>(w.h),
+                                                       static_cast<T*>(e.d_ref_pending), D);
+    }
+    e.launches += 8;
+    OPPO_CUDA_CHECK(cudaGetLastError());
+}
+
+template <class T>
+void decode_iteration(Engine& e, const DecodeSeq* dseq, int M, int it, int max_ctx, cudaStream_t st) {
+    Work& w = e.wa;
+    Model& m = e.models[ACTOR];
+    decode_rows<<<cdiv(M, 128), 128, 0, st>>>(dseq, M, it, e.d_prompt, e.Pmax, e.d_tok, e.tok_stride,
+                                              e.cfg.sample_seed, w.meta);
+    Final<T> fin;
+    fin.write_h = true;
+    fin.cache = static_cast<T*>(e.d_hf_actor);
+    fin.t_lo = 1;
+    fin.t_hi = e.Lmax;
+    forward<T>(e, m, w, st, M, true, max_ctx, nullptr, 0, fin);
+    EpiParams ep{};
+    ep.mode = EPI_LOGITS;
+    ep.partials = w.partials;
+    ep.tgt_logit = w.tgt_logit;
+    ep.targets = nullptr;
+    ep.keys = w.meta.key;
+    const int D = m.dims.d_model;
+    gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
+    logits_combine<<<cdiv(M, 4), 128, 0, st>>>(w.partials, cdiv(m.dims.vocab, 128), M, w.meta.key,
+                                               nullptr, w.meta.slot, w.meta.t, e.d_tok, e.d_old_lp,
+                                               e.tok_stride, nullptr, nullptr);
+    e.launches += 3;
+}
+
+template <class T>
+void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chunk, int mode,
+                   int stop_after, std::vector<oppo_seq_outcome>& out, oppo_ledger& ledger) {
+    const StepPlan plan = plan_step(active, chunk, mode, stop_after, e.cfg.carry_granularity);
+    open_step(e);
+    const int n = static_cast<int>(active.size());
+    const int64_t t_end = plan.t_end;
+    std::vector<int> slot(n);
+    for (int i = 0; i < n; ++i) {
+        auto it = e.slot_of.find(active[i].id);
+        if (it == e.slot_of.end()) input_error("sequence " + std::to_string(active[i].id) + " not admitted");
+        slot[i] = it->second;
+        if (e.slots[slot[i]].target_len != active[i].target_len)
+            input_error("target_len changed since admission");
+    }
+    // decode order: remaining length descending, so the batch of iteration t is a prefix
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        const int ra = active[a].target_len - active[a].generated;
+        const int rb = active[b].target_len - active[b].generated;
+        return ra != rb ? ra > rb : active[a].id < active[b].id;
+    });
+    std::vector<DecodeSeq> dseq;
+    std::vector<int> rem_sorted;
+    for (int i : order) {
+        const int rem = active[i].target_len - active[i].generated;
+        if (rem <= 0) continue;
+        dseq.push_back({slot[i], active[i].prompt_len, active[i].generated, 0, active[i].id});
+        rem_sorted.push_back(rem);
+    }
+    auto& A = g_extra[&e].step_arena;
+    A.host.clear();
+    const size_t o_dseq = A.push_vec(dseq);
+
+    // ---------------------------------------------------------- wave plans
+    const bool streamed = mode == OPPO_MODE_STREAMED;
+    std::vector<int> p_cur(n);
+    for (int i = 0; i < n; ++i) p_cur[i] = active[i].prefilled_tokens;
+    std::vector<WavePlan> waves;
+    int64_t wave_tokens = 0;
+    auto make_wave = [&](int at_iter, auto&& target_p) {
+        std::vector<SegReq> reqs;
+        for (int i : order) {  // deterministic order
+            const int want = target_p(i);
+            if (want <= p_cur[i]) continue;
+            auto& info = e.slots[slot[i]];
+            const int P = active[i].prompt_len;
+            const bool first = p_cur[i] == 0 && !info.scored_prompt;
+            const int pos0 = first ? 0 : P + p_cur[i];
+            const int pos1 = P + want - 1;
+            reqs.push_back({slot[i], pos0, pos1 - pos0 + 1, P});
+            info.scored_prompt = true;
+            p_cur[i] = want;
+        }
+        if (reqs.empty()) return;
+        WavePlan wv;
+        wv.at_iter = at_iter;
+        build_passes(e, reqs, wv, A);
+        waves.push_back(std::move(wv));
+    };
+    auto whole_by = [&](int i, int64_t t) -> int {  // chunk-complete tokens after iteration t
+        const auto& s = active[i];
+        const int64_t rem = s.target_len - s.generated;
+        const int64_t rel = rem <= t ? rem : (t / chunk) * chunk;
+        return static_cast<int>(s.generated + rel);
+    };
+    if (streamed) {
+        make_wave(0, [&](int i) { return active[i].generated; });  // carried chunks, at tick 0
+        for (int64_t t = chunk; t < t_end; t += chunk)
+            make_wave(static_cast<int>(t), [&](int i) { return whole_by(i, t); });
+        make_wave(static_cast<int>(t_end), [&](int i) { return whole_by(i, t_end); });
+    } else {
+        make_wave(static_cast<int>(t_end), [&](int i) {
+            const auto& s = active[i];
+            const int64_t rem = s.target_len - s.generated;
+            return rem <= t_end ? s.target_len : s.generated;
+        });
+    }
+    // sanity: the prefilled counts must equal the logical outcome's
+    for (int i = 0; i < n; ++i) {
+        const int expect = active[i].prefilled_tokens + plan.outcomes[i].tokens_prefilled;
+        if (p_cur[i] != expect)
+            internal_error("wave plan disagrees with the logical clock (seq " +
+                           std::to_string(active[i].id) + ")");
+    }
+    A.upload(e.sa);
+    const DecodeSeq* d_dseq = A.at<DecodeSeq>(o_dseq);
+
+    // ------------------------------------------------------------- enqueue
+    if (e.ev_pool.size() < waves.size() + 2) {
+        const size_t old = e.ev_pool.size();
+        e.ev_pool.resize(waves.size() + 2);
+        for (size_t i = old; i < e.ev_pool.size(); ++i)
+            OPPO_CUDA_CHECK(cudaEventCreateWithFlags(&e.ev_pool[i], cudaEventDisableTiming));
+    }
+    OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, e.ev_begin, 0));
+    // the scorer stream must also see the arena upload and admission prefill on sa
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_pool[0], e.sa));
+    OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, e.ev_pool[0], 0));
+    size_t wi = 0;
+    int64_t prefill_tokens = 0, decode_tokens = 0;
+    auto fire_waves_at = [&](int64_t it) {
+        while (wi < waves.size() && waves[wi].at_iter == it) {
+            cudaEvent_t ev = e.ev_pool[wi + 1];
+            OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));
+            OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, ev, 0));
+            for (const auto& p : waves[wi].passes) run_scorer_pass<T>(e, p, A, e.ss, prefill_tokens);
+            ++wi;
+        }
+    };
+    fire_waves_at(0);
+    size_t active_n = dseq.size();
+    for (int64_t it = 1; it <= t_end; ++it) {
+        while (active_n > 0 && rem_sorted[active_n - 1] < it) --active_n;
+        if (active_n == 0) break;
+        int max_ctx = 0;
+        for (size_t r = 0; r < active_n; ++r)
+            max_ctx = std::max(max_ctx, dseq[r].prompt_len + dseq[r].generated + static_cast<int>(it) - 1);
+        decode_iteration<T>(e, d_dseq, static_cast<int>(active_n), static_cast<int>(it), max_ctx, e.sa);
+        decode_tokens += static_cast<int64_t>(active_n);
+        fire_waves_at(it);
+    }
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_dec_end, e.sa));
+    fire_waves_at(t_end);  // (t_end == 0 or already fired: no-op)
+    if (wi != waves.size()) internal_error("unfired scorer waves");
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_sc_end, e.ss));
+    OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.sa, e.ev_sc_end, 0));
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_done, e.sa));
+    OPPO_CUDA_CHECK(cudaEventSynchronize(e.ev_done));
+    OPPO_CUDA_CHECK(cudaGetLastError());
+    e.step_open = false;
+
+    out = plan.outcomes;
+    ledger = plan.ledger;
+    float ms = 0;
+    OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_begin, e.ev_done));
+    ledger.step_us = ms * 1e3;
+    OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_begin, e.ev_dec_end));
+    ledger.decode_us = ms * 1e3;
+    OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_begin, e.ev_sc_end));
+    ledger.score_us = ms * 1e3;
+    ledger.decode_iters = t_end;
+    ledger.decode_tokens = decode_tokens;
+    ledger.prefill_tokens = prefill_tokens;
+    ledger.kernel_launches = e.launches;
+}
+
+// =============================================================== PPO update
+template <class T>
+__global__ void gather_batch(const int32_t* __restrict__ slots, const int32_t* __restrict__ off,
+                             int n, const int32_t* __restrict__ tok, const float* __restrict__ old_lp,
+                             const float* __restrict__ ref_lp, const float* __restrict__ vals,
+                             const float* __restrict__ reward, int stride, int32_t* o_tok,
+                             float* o_old, float* o_ref, float* o_vtok, float* o_vals,
+                             float* o_score) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    const int s = slots[i], a = off[i], L = off[i + 1] - a;
+    for (int t = threadIdx.x; t < L; t += blockDim.x) {
+        const size_t src = static_cast<size_t>(s) * stride + t + 1;
+        o_tok[a + t] = tok[src];
+        o_old[a + t] = old_lp[src];
+        o_ref[a + t] = ref_lp[src];
+        o_vtok[a + t] = vals[src];
+        o_vals[a + i + t] = vals[src];
+    }
+    if (threadIdx.x == 0) {
+        o_vals[a + i + L] = 0.f;  // terminal convention (ppo.cpp:278)
+        o_score[i] = reward[s];
+    }
+}
+template <class T>
+__global__ void gather_hidden(const int32_t* __restrict__ slots, const int32_t* __restrict__ off,
+                              int n, const T* __restrict__ cache, int stride, int d, T* out) {
+    const int i = blockIdx.y;
+    const int s = slots[i], a = off[i], L = off[i + 1] - a;
+    for (int t = blockIdx.x; t < L; t += gridDim.x) {
+        const T* src = cache + (static_cast<size_t>(s) * stride + t + 1) * d;
+        T* dst = out + static_cast<size_t>(a + t) * d;
+        for (int k = threadIdx.x; k < d; k += blockDim.x) dst[k] = src[k];
+    }
+}
+template <class T>
+__global__ void transpose_rows(const T* __restrict__ in, int rows, int cols, int ld_out, T* out) {
+    __shared__ T tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < rows && c < cols) ? in[static_cast<size_t>(r) * cols + c] : fromf<T>(0.f);
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < ld_out) out[static_cast<size_t>(c) * ld_out + r] = tile[threadIdx.x][i];
+    }
+}
+__global__ void sum_partials(const double* p, int n, double* out) {
+    if (threadIdx.x) return;
+    double s = 0;
+    for (int i = 0; i < n; ++i) s += p[i];
+    out[0] = s;
+}
+__global__ void head_sgd(float* w, const float* g, int d, float lr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < d) w[i] -= lr * g[i];
+}
+__global__ void sq_err_sum(const float* v, const float* r, int n, double* out) {
+    double s = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += (double(v[i]) - r[i]) * (double(v[i]) - r[i]);
+    s = warp_sum_d(s);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += sh[i];
+        out[0] = t;
+    }
+}
+
+template <class T>
+void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hparams& hp,
+                     oppo_ppo_stats& st_out) {
+    cudaStream_t st = e.sa;
+    cudaEvent_t t0, t1;
+    OPPO_CUDA_CHECK(cudaEventCreate(&t0));
+    OPPO_CUDA_CHECK(cudaEventCreate(&t1));
+    OPPO_CUDA_CHECK(cudaEventRecord(t0, st));
+    const int n = static_cast<int>(slots.size());
+    std::vector<int32_t> off(n + 1, 0), sl(slots.begin(), slots.end());
+    for (int i = 0; i < n; ++i) off[i + 1] = off[i] + e.slots[slots[i]].target_len;
+    const int N = off[n];
+    Model& actor = e.models[ACTOR];
+    Model& critic = e.models[CRITIC];
+    const int Da = actor.dims.d_model, Dc = critic.dims.d_model, V = actor.dims.vocab;
+    const int Npad = (N + 7) / 8 * 8;
+    // device buffers (grown on demand)
+    const size_t need = static_cast<size_t>(Npad) * (4 * 12) + static_cast<size_t>(n + 1) * 16 * 4 +
+                        static_cast<size_t>(Npad) * (Da + Dc) * sizeof(T) + 4096 * 8 + 1024;
+    if (need > e.ppo_buf_bytes) {
+        if (e.ppo_buf) cudaFree(e.ppo_buf);
+        e.ppo_buf_bytes = need * 3 / 2;
+        e.ppo_buf = dalloc(e.ppo_buf_bytes);
+    }
+    uint8_t* p = static_cast<uint8_t*>(e.ppo_buf);
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p;
+        p += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    int32_t* d_slots = reinterpret_cast<int32_t*>(take(n * 4));
+    int32_t* d_off = reinterpret_cast<int32_t*>(take((n + 1) * 4));
+    int32_t* d_tokv = reinterpret_cast<int32_t*>(take(Npad * 4));
+    float* d_old = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_ref = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_vtok = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_vals = reinterpret_cast<float*>(take((N + n) * 4));
+    float* d_score = reinterpret_cast<float*>(take(n * 4));
+    float* d_rew = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_kl = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_adv = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_ret = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_new = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_lse = reinterpret_cast<float*>(take(Npad * 4));
+    float* d_dobj = reinterpret_cast<float*>(take(Npad * 4));
+    double* d_part = reinterpret_cast<double*>(take(4096 * 8));
+    double* d_stats = reinterpret_cast<double*>(take(16 * 8));
+    T* d_hf = reinterpret_cast<T*>(take(static_cast<size_t>(Npad) * Da * sizeof(T)));
+    T* d_hc = reinterpret_cast<T*>(take(static_cast<size_t>(Npad) * Dc * sizeof(T)));
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(d_slots, sl.data(), n * 4, cudaMemcpyHostToDevice, st));
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(d_off, off.data(), (n + 1) * 4, cudaMemcpyHostToDevice, st));
+    OPPO_CUDA_CHECK(cudaMemsetAsync(d_tokv, 0, Npad * 4, st));
+    OPPO_CUDA_CHECK(cudaMemsetAsync(d_hf, 0, static_cast<size_t>(Npad) * Da * sizeof(T), st));
+    gather_batch<T><<<n, 128, 0, st>>>(d_slots, d_off, n, e.d_tok, e.d_old_lp, e.d_ref_lp, e.d_values,
+                                       e.d_reward, e.tok_stride, d_tokv, d_old, d_ref, d_vtok, d_vals,
+                                       d_score);
+    gather_hidden<T><<<dim3(64, n), 128, 0, st>>>(d_slots, d_off, n, static_cast<const T*>(e.d_hf_actor),
+                                                  e.tok_stride, Da, d_hf);
+    gather_hidden<T><<<dim3(64, n), 128, 0, st>>>(d_slots, d_off, n, static_cast<const T*>(e.d_hf_critic),
+                                                  e.tok_stride, Dc, d_hc);
+    // K7 KL-shaped reward, K8 GAE
+    token_rewards<float><<<n, 128, 0, st>>>(n, d_off, d_score, d_old, d_ref,
+                                            static_cast<float>(hp.kl_coef), d_rew, d_kl);
+    gae_scan<float><<<cdiv(n * 32, 128), 128, 0, st>>>(n, d_off, d_rew, d_vals,
+                                                      static_cast<float>(hp.gamma),
+                                                      static_cast<float>(hp.lambda), d_adv, d_ret);
+    // K9 whitening statistics (+ NCCL allreduce across ranks in DP runs)
+    const int mb = std::min(1024, cdiv(N, 256));
+    double* stats = nullptr;
+    if (hp.whiten) {
+        moments<float><<<mb, 256, 0, st>>>(d_adv, N, d_part);
+        moments_final<<<1, 32, 0, st>>>(d_part, mb, static_cast<double>(N), d_stats);
+        stats = d_stats;
+    }
+    // current-policy log-probs of the sampled tokens from the cached actor hidden states
+    const int nt = cdiv(V, 128);
+    Work& w = e.ws;
+    const int chunk_rows = std::max(32, std::min(w.max_rows, static_cast<int>((static_cast<size_t>(64) << 20) / (nt * 16))));
+    for (int c0 = 0; c0 < N; c0 += chunk_rows) {
+        const int cn = std::min(chunk_rows, N - c0);
+        EpiParams ep{};
+        ep.mode = EPI_LOGITS;
+        ep.partials = w.partials;
+        ep.tgt_logit = w.tgt_logit;
+        ep.targets = d_tokv + c0;
+        gemm_run(e, w, st, d_hf + static_cast<size_t>(c0) * Da, cn, Da, Da, actor.lm_head, V, Da, ep);
+        // contiguous rows: new_lp[c0 + r] = logit[target] - lse
+        logits_combine<<<cdiv(cn, 4), 128, 0, st>>>(w.partials, nt, cn, nullptr, w.tgt_logit, nullptr,
+                                                    nullptr, nullptr, d_new + c0, 0, d_lse + c0, nullptr);
+    }
+    // K10 clipped objective and d obj / d logp
+    const int cb = std::min(1024, cdiv(N, 256));
+    ppo_clip<float><<<cb, 256, 0, st>>>(N, d_new, d_old, d_adv, static_cast<float>(hp.clip_epsilon),
+                                        stats, 1e-8, d_dobj, d_part, 1.0f / std::max(1, N));
+    sum_partials<<<1, 32, 0, st>>>(d_part, cb, d_stats + 4);
+    // K11 head update: lm_head += lr * dObj/dW  (gradient ascent, ppo.cpp:288-290)
+    if (e.cfg.train_heads && hp.learning_rate > 0) {
+        const int gc = e.g_chunk;
+        if (!e.g_buf) {
+            e.g_buf = dalloc(static_cast<size_t>(V) * gc * sizeof(T));
+            e.ht_buf = dalloc(static_cast<size_t>(std::max(Da, Dc)) * gc * sizeof(T));
+            e.vgrad = static_cast<float*>(dalloc(std::max(Da, Dc) * 4));
+        }
+        for (int c0 = 0; c0 < N; c0 += gc) {
+            const int cn = std::min(gc, N - c0);
+            const int cp = (cn + 7) / 8 * 8;
+            EpiParams ep{};
+            ep.mode = EPI_SOFTMAX_GRAD;
+            ep.y = e.g_buf;
+            ep.ldy = cp;
+            ep.lse = d_lse + c0;
+            ep.coef = d_dobj + c0;
+            ep.targets = d_tokv + c0;
+            if (cp != cn) OPPO_CUDA_CHECK(cudaMemsetAsync(e.g_buf, 0, static_cast<size_t>(V) * cp * sizeof(T), st));
+            gemm_run(e, w, st, d_hf + static_cast<size_t>(c0) * Da, cn, Da, Da, actor.lm_head, V, Da, ep);
+            transpose_rows<T><<<dim3(cdiv(Da, 32), cdiv(cp, 32)), dim3(32, 8), 0, st>>>(
+                d_hf + static_cast<size_t>(c0) * Da, cn, Da, cp, static_cast<T*>(e.ht_buf));
+            EpiParams eg{};
+            eg.mode = EPI_ADD_F32;
+            eg.y = actor.lm_master;
+            eg.ldy = Da;
+            eg.scale = static_cast<float>(hp.learning_rate);
+            gemm_run(e, w, st, e.g_buf, V, cp, cp, e.ht_buf, Da, cp, eg);
+        }
+        const size_t nn = static_cast<size_t>(V) * Da;
+        convert<float, T><<<cdiv(nn, 256), 256, 0, st>>>(actor.lm_master, static_cast<T*>(actor.lm_head), nn);
+        // critic value head: w -= vlr * (1/N) sum (V - R) h
+        value_head_grad<T><<<cdiv(Dc, 128), 128, 0, st>>>(d_hc, Dc, N, d_vtok, d_ret, e.vgrad,
+                                                          1.0f / std::max(1, N));
+        head_sgd<<<cdiv(Dc, 128), 128, 0, st>>>(critic.head, e.vgrad, Dc,
+                                                static_cast<float>(hp.value_learning_rate));
+    }
+    sq_err_sum<<<1, 256, 0, st>>>(d_vtok, d_ret, N, d_stats + 5);
+    // statistics back to the host
+    double hs[8] = {0};
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(hs, d_stats, 8 * 8, cudaMemcpyDeviceToHost, st));
+    std::vector<float> score(n), kl(N);
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(score.data(), d_score, n * 4, cudaMemcpyDeviceToHost, st));
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(kl.data(), d_kl, N * 4, cudaMemcpyDeviceToHost, st));
+    OPPO_CUDA_CHECK(cudaEventRecord(t1, st));
+    OPPO_CUDA_CHECK(cudaEventSynchronize(t1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    st_out = {};
+    double sr = 0, sk = 0;
+    for (float x : score) sr += x;
+    for (float x : kl) sk += x;
+    st_out.mean_reward = n ? sr / n : 0.0;
+    st_out.kl_mean = N ? sk / N : 0.0;
+    st_out.ppo_objective = N ? hs[4] / N : 0.0;
+    st_out.value_loss = N ? 0.5 * hs[5] / N : 0.0;
+    if (hp.whiten && N) {
+        st_out.adv_mean = hs[0] / N;
+        st_out.adv_std = std::sqrt(std::max(0.0, hs[1] / N - st_out.adv_mean * st_out.adv_mean));
+    }
+    st_out.n_tokens = N;
+    st_out.n_samples = n;
+    st_out.update_us = ms * 1e3;
+}
+
+}  // namespace
+
+}  // namespace oppo
+
+// ==================================================================== C ABI
+namespace oppo {
+namespace {
+
+template <class F>
+oppo_status eguard(Engine* e, F&& f) {
+    try {
+        f();
+        return OPPO_OK;
+    } catch (const Error& x) {
+        if (e) e->error = x.what();
+        return x.code;
+    } catch (const std::exception& x) {
+        if (e) e->error = x.what();
+        return OPPO_ERR_INTERNAL;
+    }
+}
+
+void release_slot(Engine& e, int64_t id) {
+    auto it = e.slot_of.find(id);
+    if (it == e.slot_of.end()) input_error("release of unknown sequence " + std::to_string(id));
+    auto& info = e.slots[it->second];
+    for (int p : info.pages) e.free_pages.push_back(p);
+    info = SlotInfo{};
+    e.free_slots.push_back(it->second);
+    e.slot_of.erase(it);
+}
+
+struct EngineHooks final : LoopHooks {
+    Engine& e;
+    oppo_ppo_hparams hp;
+    explicit EngineHooks(Engine& en, const oppo_ppo_hparams& h) : e(en), hp(h) {}
+    void admit(const std::vector<oppo_seq_state>& fresh) override {
+        if (fresh.empty()) return;
+        if (e.dtype == OPPO_DTYPE_F32) admit_impl<float>(e, fresh.data(), static_cast<int>(fresh.size()), nullptr);
+        else admit_impl<__nv_bfloat16>(e, fresh.data(), static_cast<int>(fresh.size()), nullptr);
+    }
+    void execute(const std::vector<oppo_seq_state>& active, int chunk, int mode, int stop,
+                 std::vector<oppo_seq_outcome>& out, oppo_ledger& ledger) override {
+        if (e.dtype == OPPO_DTYPE_F32) run_step_impl<float>(e, active, chunk, mode, stop, out, ledger);
+        else run_step_impl<__nv_bfloat16>(e, active, chunk, mode, stop, out, ledger);
+    }
+    double update(const std::vector<oppo_seq_state>& batch, bool train, oppo_step_record& rec) override {
+        if (!train || batch.empty()) return 0.0;
+        std::vector<int> slots;
+        for (const auto& s : batch) slots.push_back(e.slot_of.at(s.id));
+        oppo_ppo_stats st{};
+        if (e.dtype == OPPO_DTYPE_F32) ppo_update_impl<float>(e, slots, hp, st);
+        else ppo_update_impl<__nv_bfloat16>(e, slots, hp, st);
+        rec.update_us = st.update_us;
+        rec.ppo_loss = st.ppo_objective;
+        rec.kl_mean = st.kl_mean;
+        rec.batch_tokens = st.n_tokens;
+        return st.mean_reward;
+    }
+    void release(const std::vector<oppo_seq_state>& batch) override {
+        for (const auto& s : batch) release_slot(e, s.id);
+    }
+};
+
+}  // namespace
+}  // namespace oppo
+
+using oppo::Engine;
+
+extern "C" {
+
+oppo_status oppo_engine_create(const oppo_engine_cfg* cfg, oppo_engine** out) {
+    *out = nullptr;
+    try {
+        *out = reinterpret_cast<oppo_engine*>(oppo::engine_new(*cfg));
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    } catch (const std::exception& x) {
+        oppo_set_global_error(x.what());
+        return OPPO_ERR_INTERNAL;
+    }
+}
+
+void oppo_engine_destroy(oppo_engine* e) { oppo::engine_free(reinterpret_cast<Engine*>(e)); }
+
+const char* oppo_last_error(const oppo_engine* e) {
+    return e ? reinterpret_cast<const Engine*>(e)->error.c_str() : oppo_last_error_global();
+}
+
+oppo_status oppo_admit(oppo_engine* eh, const oppo_seq_state* seqs, int32_t n,
+                       const int32_t* prompt_tokens) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        if (e->dtype == OPPO_DTYPE_F32) oppo::admit_impl<float>(*e, seqs, n, prompt_tokens);
+        else oppo::admit_impl<__nv_bfloat16>(*e, seqs, n, prompt_tokens);
+    });
+}
+
+oppo_status oppo_run_step(oppo_engine* eh, const oppo_seq_state* active, int32_t n_active,
+                          int32_t chunk_size, int32_t mode, int32_t stop_after,
+                          oppo_seq_outcome* out, oppo_ledger* ledger) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        std::vector<oppo_seq_state> v(active, active + n_active);
+        std::vector<oppo_seq_outcome> o;
+        oppo_ledger l{};
+        if (e->dtype == OPPO_DTYPE_F32) oppo::run_step_impl<float>(*e, v, chunk_size, mode, stop_after, o, l);
+        else oppo::run_step_impl<__nv_bfloat16>(*e, v, chunk_size, mode, stop_after, o, l);
+        std::copy(o.begin(), o.end(), out);
+        *ledger = l;
+    });
+}
+
+oppo_status oppo_ppo_update(oppo_engine* eh, const int64_t* ids, int32_t n,
+                            const oppo_ppo_hparams* hp, oppo_ppo_stats* out) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        std::vector<int> slots;
+        for (int i = 0; i < n; ++i) {
+            auto it = e->slot_of.find(ids[i]);
+            if (it == e->slot_of.end()) oppo::input_error("update of unknown sequence");
+            slots.push_back(it->second);
+        }
+        if (e->dtype == OPPO_DTYPE_F32) oppo::ppo_update_impl<float>(*e, slots, *hp, *out);
+        else oppo::ppo_update_impl<__nv_bfloat16>(*e, slots, *hp, *out);
+    });
+}
+
+oppo_status oppo_release(oppo_engine* eh, const int64_t* ids, int32_t n) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        for (int i = 0; i < n; ++i) oppo::release_slot(*e, ids[i]);
+    });
+}
+
+oppo_status oppo_read_rollout(oppo_engine* eh, int64_t id, int32_t* tokens, float* old_lp,
+                              float* ref_lp, float* values, float* reward, int32_t cap,
+                              int32_t* len) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        auto it = e->slot_of.find(id);
+        if (it == e->slot_of.end()) oppo::input_error("unknown sequence");
+        const int s = it->second;
+        const int L = e->slots[s].target_len;
+        *len = L;
+        if (cap < L + 2) oppo::input_error("buffer too small");
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(e->sa));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(e->ss));
+        const size_t o = static_cast<size_t>(s) * e->tok_stride;
+        if (tokens) OPPO_CUDA_CHECK(cudaMemcpy(tokens, e->d_tok + o, (L + 1) * 4, cudaMemcpyDeviceToHost));
+        if (old_lp) OPPO_CUDA_CHECK(cudaMemcpy(old_lp, e->d_old_lp + o, (L + 1) * 4, cudaMemcpyDeviceToHost));
+        if (ref_lp) OPPO_CUDA_CHECK(cudaMemcpy(ref_lp, e->d_ref_lp + o, (L + 1) * 4, cudaMemcpyDeviceToHost));
+        if (values) OPPO_CUDA_CHECK(cudaMemcpy(values, e->d_values + o, (L + 2) * 4, cudaMemcpyDeviceToHost));
+        if (reward) OPPO_CUDA_CHECK(cudaMemcpy(reward, e->d_reward + s, 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+oppo_status oppo_read_prompt(oppo_engine* eh, int64_t id, int32_t* out, int32_t cap, int32_t* len) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        auto it = e->slot_of.find(id);
+        if (it == e->slot_of.end()) oppo::input_error("unknown sequence");
+        const int s = it->second, P = e->slots[s].prompt_len;
+        *len = P;
+        if (cap < P) oppo::input_error("buffer too small");
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(e->sa));
+        OPPO_CUDA_CHECK(cudaMemcpy(out, e->d_prompt + static_cast<size_t>(s) * e->Pmax, P * 4,
+                                   cudaMemcpyDeviceToHost));
+    });
+}
+
+// Copies one weight tensor of a model to host as fp32 (oracle parity).
+// name: embed lm_head final_norm head wqkv bqkv wo wgu wdown ln1 ln2
+oppo_status oppo_get_tensor(oppo_engine* eh, int32_t model, const char* name, int32_t layer,
+                            float* out, int64_t cap, int64_t* n_out) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        if (model < 0 || model >= oppo::N_MODELS) oppo::input_error("bad model id");
+        auto& m = e->models[model];
+        const auto& d = m.dims;
+        const std::string nm(name);
+        const void* ptr = nullptr;
+        int64_t n = 0;
+        bool is_f32 = false;
+        const int64_t D = d.d_model;
+        if (nm == "embed") { ptr = m.embed; n = d.vocab * D; }
+        else if (nm == "lm_head") { ptr = m.lm_head; n = d.vocab * D; }
+        else if (nm == "final_norm") { ptr = m.final_norm; n = D; is_f32 = true; }
+        else if (nm == "head") { ptr = m.head; n = m.head ? D : 0; is_f32 = true; }
+        else {
+            if (layer < 0 || layer >= d.n_layers) oppo::input_error("bad layer");
+            const auto& L = m.layers[layer];
+            if (nm == "wqkv") { ptr = L.wqkv; n = m.qkv_width() * D; }
+            else if (nm == "bqkv") { ptr = L.bqkv; n = m.qkv_width(); is_f32 = true; }
+            else if (nm == "wo") { ptr = L.wo; n = D * m.q_width(); }
+            else if (nm == "wgu") { ptr = L.wgu; n = 2 * d.d_ff * D; }
+            else if (nm == "wdown") { ptr = L.wdown; n = D * d.d_ff; }
+            else if (nm == "ln1") { ptr = L.ln1; n = D; is_f32 = true; }
+            else if (nm == "ln2") { ptr = L.ln2; n = D; is_f32 = true; }
+            else oppo::input_error("unknown tensor " + nm);
+        }
+        *n_out = n;
+        if (!ptr || n == 0) return;
+        if (cap < n) oppo::input_error("buffer too small");
+        OPPO_CUDA_CHECK(cudaDeviceSynchronize());
+        if (is_f32 || e->dtype == OPPO_DTYPE_F32) {
+            OPPO_CUDA_CHECK(cudaMemcpy(out, ptr, n * 4, cudaMemcpyDeviceToHost));
+        } else {
+            float* tmp = nullptr;
+            OPPO_CUDA_CHECK(cudaMalloc(&tmp, n * 4));
+            oppo::convert<__nv_bfloat16, float><<<(n + 255) / 256, 256>>>(
+                static_cast<const __nv_bfloat16*>(ptr), tmp, n);
+            OPPO_CUDA_CHECK(cudaMemcpy(out, tmp, n * 4, cudaMemcpyDeviceToHost));
+            cudaFree(tmp);
+        }
+    });
+}
+
+oppo_status oppo_run_seed(oppo_engine* eh, const oppo_run_config* cfg, uint64_t seed,
+                          oppo_step_record* records, int32_t* n_records, int64_t* sel_ids) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    std::string err;
+    const oppo_status st = oppo::eguard(e, [&] {
+        oppo::EngineHooks hooks(*e, cfg->ppo);
+        if (cfg->carry_granularity != e->cfg.carry_granularity)
+            oppo::config_error("run config and engine disagree on carry_granularity");
+        *n_records = oppo::run_seed_loop(*cfg, seed, hooks, records, sel_ids, &err);
+        // sequences still buffered at the end keep their slots; free them
+        std::vector<int64_t> left;
+        for (auto& kv : e->slot_of) left.push_back(kv.first);
+        for (auto id : left) oppo::release_slot(*e, id);
+    });
+    if (st != OPPO_OK) return st;
+    if (!err.empty()) {
+        e->error = err;
+        return OPPO_ERR_INTERNAL;
+    }
+    return OPPO_OK;
+}
+
+oppo_status oppo_k_ppo_token(int32_t is_f64, int32_t n_seq, const int32_t* d_off,
+                             const void* d_score, const void* d_token_rewards, const void* d_values,
+                             const void* d_new_lp, const void* d_old_lp, double gamma, double lambda,
+                             double eps, int32_t whiten, void* d_adv, void* d_returns,
+                             void* d_dobj, void* d_obj_sum, void* stream) {
+    try {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        std::vector<int32_t> off(n_seq + 1);
+        OPPO_CUDA_CHECK(cudaMemcpy(off.data(), d_off, (n_seq + 1) * 4, cudaMemcpyDeviceToHost));
+        const int N = off[n_seq];
+        double* part = nullptr;
+        OPPO_CUDA_CHECK(cudaMalloc(&part, 4096 * 8 + 64));
+        double* stats = part + 4096;
+        const int cb = std::max(1, std::min(1024, (N + 255) / 256));
+        auto run = [&](auto tag) {
+            using R = decltype(tag);
+            R* rew = static_cast<R*>(const_cast<void*>(d_token_rewards));
+            if (d_score) {  // terminal rewards from per-sequence scores (ppo.cpp:87-91)
+                OPPO_CUDA_CHECK(cudaMalloc(&rew, std::max(1, N) * sizeof(R)));
+                oppo::token_rewards<R><<<n_seq, 128, 0, st>>>(n_seq, d_off, static_cast<const R*>(d_score),
+                                                              nullptr, nullptr, R(0), rew, nullptr);
+            }
+            oppo::gae_scan<R><<<(n_seq * 32 + 127) / 128, 128, 0, st>>>(
+                n_seq, d_off, rew, static_cast<const R*>(d_values), static_cast<R>(gamma),
+                static_cast<R>(lambda), static_cast<R*>(d_adv), static_cast<R*>(d_returns));
+            const double* sp = nullptr;
+            if (whiten) {
+                oppo::moments<R><<<cb, 256, 0, st>>>(static_cast<R*>(d_adv), N, part);
+                oppo::moments_final<<<1, 32, 0, st>>>(part, cb, double(N), stats);
+                sp = stats;
+            }
+            if (d_new_lp) {
+                oppo::ppo_clip<R><<<cb, 256, 0, st>>>(N, static_cast<const R*>(d_new_lp),
+                                                      static_cast<const R*>(d_old_lp),
+                                                      static_cast<R*>(d_adv), static_cast<R>(eps), sp,
+                                                      1e-8, static_cast<R*>(d_dobj), part,
+                                                      R(1) / static_cast<R>(std::max(1, N)));
+                oppo::sum_partials<<<1, 32, 0, st>>>(part, cb, static_cast<double*>(d_obj_sum));
+            }
+            OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (d_score) cudaFree(rew);
+        };
+        if (is_f64) run(double{});
+        else run(float{});
+        cudaFree(part);
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
+
+oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* d_x,
+                        const void* d_w, const void* d_bias, void* d_y, int32_t epilogue,
+                        void* stream) {
+    try {
+        oppo::gemm_standalone(dtype, M, N, K, d_x, d_w, static_cast<const float*>(d_bias), d_y,
+                              epilogue, static_cast<cudaStream_t>(stream));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// engine.cuh — device state of the OPPO step executor (one per GPU).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "host/sched.hpp"
+#include "kernels/gemm.cuh"
+#include "kernels/model.cuh"
+#include "oppo/oppo.h"
+
+namespace oppo {
+
+enum ModelId { ACTOR = 0, REWARD = 1, CRITIC = 2, REF = 3, N_MODELS = 4 };
+
+struct LayerW {
+    void* wqkv;   // [(H+2KV)hd, d]
+    float* bqkv;  // [(H+2KV)hd]
+    void* wo;     // [d, H hd]
+    void* wgu;    // [2 dff, d], rows interleaved (gate_i, up_i)
+    void* wdown;  // [d, dff]
+    float* ln1;
+    float* ln2;
+};
+
+struct Model {
+    oppo_model_dims dims{};
+    bool used = false;
+    void* embed = nullptr;    // [V, d] (T)
+    void* lm_head = nullptr;  // == embed when tied
+    float* lm_master = nullptr;  // fp32 master of lm_head (actor, when training)
+    std::vector<LayerW> layers;
+    float* final_norm = nullptr;
+    float* head = nullptr;    // value / reward head [d] (critic / reward)
+    void* k_pool = nullptr;
+    void* v_pool = nullptr;
+    int64_t layer_stride = 0;  // elements per layer in a pool
+    KvView kv(const int32_t* page_table, int max_pages, int page_size) const {
+        return KvView{k_pool, v_pool, layer_stride, page_size, dims.n_kv_heads, dims.head_dim,
+                      page_table, max_pages};
+    }
+    int qkv_width() const { return (dims.n_heads + 2 * dims.n_kv_heads) * dims.head_dim; }
+    int q_width() const { return dims.n_heads * dims.head_dim; }
+};
+
+// Activation workspace of one stream (actor decode or scorer prefill).
+struct Work {
+    int max_rows = 0;
+    RowMeta meta{};
+    float* x = nullptr;      // residual [R, dmax] fp32
+    void* h = nullptr;       // normed   [R, dmax]
+    void* qkv = nullptr;     // [R, qkv_max]
+    void* q = nullptr;       // [R, qmax]
+    void* attn = nullptr;    // [R, qmax]
+    void* ff = nullptr;      // [R, dff_max]
+    float* head_out = nullptr;   // [R]
+    float4* partials = nullptr;  // [R, vocab/128]
+    float* tgt_logit = nullptr;  // [R]
+    float* lse = nullptr;        // [R]
+    void* lm_in = nullptr;       // [R, dmax] gathered lm_head rows
+    int32_t* lm_tgt = nullptr;   // [R]
+    int32_t* lm_slot = nullptr;
+    int32_t* lm_t = nullptr;
+    float* gemm_ws = nullptr;    // split-K partials
+    size_t gemm_ws_floats = 0;
+    int* gemm_cnt = nullptr;     // per-tile arrival counters (zeroed)
+    int gemm_cnt_n = 0;
+    float* attn_ws_o = nullptr;
+    float* attn_ws_ml = nullptr;
+    size_t attn_ws_rows = 0;     // rows*heads*splits capacity
+    // per-wave metadata staging (device)
+    QBlock* qblocks = nullptr;
+    Segment* segs = nullptr;
+    LmRow* lmrows = nullptr;
+    int32_t* pend_src = nullptr;
+    int32_t* pend_slot = nullptr;
+    int meta_cap = 0;
+};
+
+struct TmaKey {
+    const void* ptr;
+    int rows, cols, box_rows, ld;
+    bool operator<(const TmaKey& o) const {
+        return std::tie(ptr, rows, cols, box_rows, ld) <
+               std::tie(o.ptr, o.rows, o.cols, o.box_rows, o.ld);
+    }
+};
+
+struct SlotInfo {
+    int64_t id = -1;
+    int prompt_len = 0;
+    int target_len = 0;
+    bool ref_pending = false;  // reference lm_head row waiting for its target token
+    bool scored_prompt = false;
+    std::vector<int> pages;
+};
+
+struct Engine {
+    oppo_engine_cfg cfg{};
+    std::string error;
+    int dtype = OPPO_DTYPE_BF16;
+    size_t esz = 2;
+    int num_sms = 148;
+    Model models[N_MODELS];
+
+    int S = 0, Pmax = 0, Lmax = 0, page_size = 64, max_pages = 0, n_pages = 0;
+    int tok_stride = 0;  // Lmax + 2
+    std::vector<int> free_slots;
+    std::vector<int> free_pages;
+    std::unordered_map<int64_t, int> slot_of;
+    std::vector<SlotInfo> slots;
+
+    int32_t* d_page_table = nullptr;   // [S, max_pages]
+    int32_t* d_prompt = nullptr;       // [S, Pmax]
+    int32_t* d_tok = nullptr;          // [S, tok_stride] response tokens, index 1..L
+    float* d_old_lp = nullptr;         // [S, tok_stride]
+    float* d_ref_lp = nullptr;         // [S, tok_stride]
+    float* d_values = nullptr;         // [S, tok_stride] index 1..L (+ L+1 terminal)
+    float* d_reward = nullptr;         // [S]
+    int32_t* d_target_len = nullptr;   // [S]
+    void* d_hf_actor = nullptr;        // [S, tok_stride, d_actor]
+    void* d_hf_critic = nullptr;       // [S, tok_stride, d_critic]
+    void* d_ref_pending = nullptr;     // [S, d_ref]
+
+    Work wa, ws;                        // actor decode / scorer prefill
+    int prefill_rows = 8192;
+    cudaStream_t sa = nullptr, ss = nullptr;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr;
+    bool step_open = false;
+    int64_t launches = 0;
+
+    std::map<TmaKey, CUtensorMap> tma_cache;
+
+    // PPO update buffers (grown on demand)
+    size_t ppo_cap_tok = 0;
+    void* ppo_buf = nullptr;
+    size_t ppo_buf_bytes = 0;
+    void* g_buf = nullptr;   // softmax-grad G [V, chunk]
+    void* ht_buf = nullptr;  // transposed hidden [d, chunk]
+    int g_chunk = 4096;
+    float* vgrad = nullptr;
+    void* nccl = nullptr;
+};
+
+// engine.cu
+Engine* engine_new(const oppo_engine_cfg& cfg);
+void engine_free(Engine* e);
+
+// gemm_host.cu
+void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
+              const void* wt, int N, int ldw, const EpiParams& ep);
+void gemm_standalone(int dtype, int M, int N, int K, const void* x, const void* w,
+                     const float* bias, void* y, int epi, cudaStream_t st);
+CUtensorMap make_tma_2d(const void* ptr, int rows, int cols, int ld, int box_rows);
+
+}  // namespace oppo

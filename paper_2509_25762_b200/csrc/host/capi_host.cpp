@@ -44,6 +44,8 @@ extern "C" {
 
 const char* oppo_last_error_global(void) { return g_error.c_str(); }
 
+void oppo_set_global_error(const char* msg) { g_error = msg ? msg : ""; }
+
 void oppo_run_config_default(oppo_run_config* cfg) { oppo::config_defaults(*cfg); }
 
 void oppo_run_config_baseline(const oppo_run_config* cfg, oppo_run_config* out) {
