@@ -658,8 +658,9 @@ void build_passes(Engine& e, std::vector<SegReq>& reqs, WavePlan& wave, Arena& A
         p.n_qb = static_cast<int>(qbs.size());
         p.lm_off = A.push_vec(lms);
         p.n_lm = static_cast<int>(lms.size());
-        p.pend_off = A.push_vec(psrc);
-        A.push_vec(pslot);
+        std::vector<int32_t> pend(psrc);  // [src rows | slots], one contiguous block
+        pend.insert(pend.end(), pslot.begin(), pslot.end());
+        p.pend_off = A.push_vec(pend);
         p.n_pend = static_cast<int>(psrc.size());
         p.rows = rows;
         wave.passes.push_back(p);
@@ -1341,7 +1342,7 @@ oppo_status oppo_get_tensor(oppo_engine* eh, int32_t model, const char* name, in
             else oppo::input_error("unknown tensor " + nm);
         }
         *n_out = n;
-        if (!ptr || n == 0) return;
+        if (!ptr || n == 0 || !out) return;  // size query
         if (cap < n) oppo::input_error("buffer too small");
         OPPO_CUDA_CHECK(cudaDeviceSynchronize());
         if (is_f32 || e->dtype == OPPO_DTYPE_F32) {

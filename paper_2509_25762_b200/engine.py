@@ -1,0 +1,166 @@
+"""Python binding of the GPU step executor (liboppo.so engine entry points).
+
+Mirrors the reference's executor interface: ``run_step`` (engine.hpp:91-93),
+``select_finished``-compatible outcomes, ``ppo_update`` (fill_values +
+toy_rlhf_step, ppo.cpp:274-317) and ``run_seed`` (driver.cpp:69-202).
+"""
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from ._lib import check, lib
+from .scheduler import seq_array
+
+# Qwen2.5-family geometry; one vocabulary across all models.
+VOCAB = 151936
+SHAPES = {
+    "tiny": dict(n_layers=2, d_model=128, n_heads=4, n_kv_heads=4, head_dim=32, d_ff=512,
+                 vocab=512, tied=1),
+    "0.5b": dict(n_layers=24, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                 vocab=VOCAB, tied=1),
+    "1.5b": dict(n_layers=28, d_model=1536, n_heads=12, n_kv_heads=2, head_dim=128, d_ff=8960,
+                 vocab=VOCAB, tied=1),
+    "7b": dict(n_layers=28, d_model=3584, n_heads=28, n_kv_heads=4, head_dim=128, d_ff=18944,
+               vocab=VOCAB, tied=0),
+}
+MODELS = ("actor", "reward", "critic", "ref")
+
+
+def dims(shape):
+    d = SHAPES[shape] if isinstance(shape, str) else shape
+    return abi.ModelDims(**d)
+
+
+def param_count(shape):
+    d = SHAPES[shape] if isinstance(shape, str) else shape
+    D, F, L = d["d_model"], d["d_ff"], d["n_layers"]
+    qkv = (d["n_heads"] + 2 * d["n_kv_heads"]) * d["head_dim"]
+    per = qkv * D + qkv + D * d["n_heads"] * d["head_dim"] + 3 * D * F + 2 * D
+    emb = d["vocab"] * D * (1 if d["tied"] else 2)
+    return L * per + emb + D
+
+
+class Engine:
+    def __init__(self, actor="tiny", reward=None, critic=None, ref=None, dtype=abi.DTYPE_BF16,
+                 max_slots=16, max_prompt_len=8, max_response_len=64, page_size=64, kv_pages=0,
+                 weight_seed=1, sample_seed=2, carry=abi.CARRY_CHUNK, train_heads=0, device=0,
+                 nccl_comm=None, rank=0, world=1):
+        cfg = abi.EngineCfg()
+        cfg.actor = dims(actor)
+        cfg.reward = dims(reward or actor)
+        cfg.critic = dims(critic or reward or actor)
+        cfg.ref = dims(ref or actor)
+        cfg.dtype = dtype
+        cfg.device = device
+        cfg.weight_seed = weight_seed
+        cfg.sample_seed = sample_seed
+        cfg.max_slots = max_slots
+        cfg.max_prompt_len = max_prompt_len
+        cfg.max_response_len = max_response_len
+        cfg.page_size = page_size
+        cfg.kv_pages = kv_pages
+        cfg.carry_granularity = carry
+        cfg.rank, cfg.world = rank, world
+        cfg.train_heads = train_heads
+        cfg.nccl_comm = nccl_comm
+        self.cfg = cfg
+        self.h = C.c_void_p()
+        check(lib().oppo_engine_create(C.byref(cfg), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().oppo_engine_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        check(st, self.h)
+
+    def admit(self, states, prompts=None):
+        arr = seq_array(states)
+        p = None
+        if prompts is not None:
+            flat = np.ascontiguousarray(np.concatenate([np.asarray(x) for x in prompts]),
+                                        dtype=np.int32)
+            p = flat.ctypes.data_as(C.POINTER(C.c_int32))
+        self._check(lib().oppo_admit(self.h, arr, len(states), p))
+
+    def run_step(self, active, chunk, mode, stop_after):
+        arr = seq_array(active)
+        out = (abi.SeqOutcome * max(1, len(active)))()
+        led = abi.Ledger()
+        self._check(lib().oppo_run_step(self.h, arr, len(active), chunk, mode, stop_after, out,
+                                        C.byref(led)))
+        return list(out[:len(active)]), led
+
+    def ppo_update(self, ids, hp):
+        arr = (C.c_int64 * max(1, len(ids)))(*ids)
+        st = abi.PpoStats()
+        self._check(lib().oppo_ppo_update(self.h, arr, len(ids), C.byref(hp), C.byref(st)))
+        return st
+
+    def release(self, ids):
+        arr = (C.c_int64 * max(1, len(ids)))(*ids)
+        self._check(lib().oppo_release(self.h, arr, len(ids)))
+
+    def read_rollout(self, seq_id, cap=None):
+        cap = cap or (self.cfg.max_response_len + 4)
+        tok = (C.c_int32 * cap)()
+        old = (C.c_float * cap)()
+        ref = (C.c_float * cap)()
+        val = (C.c_float * cap)()
+        rew = C.c_float()
+        n = C.c_int32()
+        self._check(lib().oppo_read_rollout(self.h, seq_id, tok, old, ref, val, C.byref(rew), cap,
+                                            C.byref(n)))
+        L = n.value
+        return dict(tokens=np.array(tok[1:L + 1]), old_lp=np.array(old[1:L + 1]),
+                    ref_lp=np.array(ref[1:L + 1]), values=np.array(val[1:L + 1]),
+                    reward=rew.value, length=L)
+
+    def read_prompt(self, seq_id):
+        cap = self.cfg.max_prompt_len
+        out = (C.c_int32 * cap)()
+        n = C.c_int32()
+        L = lib()
+        L.oppo_read_prompt.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.c_int32,
+                                       C.POINTER(C.c_int32)]
+        self._check(L.oppo_read_prompt(self.h, seq_id, out, cap, C.byref(n)))
+        return list(out[:n.value])
+
+    def get_tensor(self, model, name, layer=0):
+        L = lib()
+        L.oppo_get_tensor.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32,
+                                      C.POINTER(C.c_float), C.c_int64, C.POINTER(C.c_int64)]
+        n = C.c_int64()
+        self._check(L.oppo_get_tensor(self.h, model, name.encode(), layer, None, 0, C.byref(n)))
+        if n.value == 0:
+            return None
+        buf = np.zeros(n.value, dtype=np.float32)
+        self._check(L.oppo_get_tensor(self.h, model, name.encode(), layer,
+                                      buf.ctypes.data_as(C.POINTER(C.c_float)), n.value,
+                                      C.byref(n)))
+        return buf
+
+    def export_weights(self, model):
+        """fp32 copies of every tensor of one model (0 actor .. 3 ref), for the oracle."""
+        d = [self.cfg.actor, self.cfg.reward, self.cfg.critic, self.cfg.ref][model]
+        w = {k: self.get_tensor(model, k) for k in ("embed", "lm_head", "final_norm", "head")}
+        for k in ("ln1", "wqkv", "bqkv", "wo", "ln2", "wgu", "wdown"):
+            w[k] = [self.get_tensor(model, k, l) for l in range(d.n_layers)]
+        dd = {f: getattr(d, f) for f, _ in abi.ModelDims._fields_}
+        return dd, w
+
+    def run_seed(self, cfg, seed):
+        recs = (abi.StepRecord * cfg.steps)()
+        sel = (C.c_int64 * (cfg.steps * cfg.batch_size))()
+        n = C.c_int32()
+        self._check(lib().oppo_run_seed(self.h, C.byref(cfg), seed, recs, C.byref(n), sel))
+        b = cfg.batch_size
+        return list(recs[:n.value]), [list(sel[i * b:(i + 1) * b]) for i in range(n.value)]

@@ -1,0 +1,241 @@
+"""End-to-end GPU parity of the step executor (pytest -m gpu, on a B200).
+
+Config 1 of BASELINE.json (tiny actor/reward/critic/ref, 2 layers, d=128, 8
+prompts, 64 new tokens, chunk 16) against the CPU oracle:
+  * token ids: the engine samples by Gumbel-max over the actor's logits with a
+    counter-based noise stream; the fp64 oracle (teacher forced on the same
+    prompt) must pick the same token wherever its top-2 margin exceeds 1e-3
+    (fp32) — in practice every token;
+  * old log-probs, reference log-probs, per-token values and the reward:
+    chunked incremental prefill on paged KV vs a full-sequence fp64 forward,
+    |diff| <= 1e-3 (fp32) / 0.08 relative (bf16);
+  * chunk boundaries, cut and deferral/selection decisions: bit-exact vs the
+    reference's run_step under the lockstep latency model.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2509_25762_b200 import abi  # noqa: E402
+from paper_2509_25762_b200 import scheduler as S  # noqa: E402
+from paper_2509_25762_b200.engine import Engine  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SAMPLE_SEED = 2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def oracles(eng):
+    out = []
+    for m in range(4):
+        dims, w = eng.export_weights(m)
+        out.append((O.GptOracle(dims, w), w.get("head")))
+    return out
+
+
+def log_softmax(x):
+    m = x.max(-1, keepdims=True)
+    return x - m - np.log(np.exp(x - m).sum(-1, keepdims=True))
+
+
+def check_rollout(eng, orc, seq_id, P, tol_lp, tol_val, margin_tol, strict_tokens=True):
+    ro = eng.read_rollout(seq_id)
+    L = ro["length"]
+    prompt = eng.read_prompt(seq_id)
+    V = eng.cfg.actor.vocab
+    assert prompt == O.prompt_tokens(SAMPLE_SEED, seq_id, P, V)
+    seq = np.concatenate([prompt, ro["tokens"]]).astype(np.int32)
+    (actor, _), (reward, rw), (critic, cw), (ref, _) = orc
+    _, lg = actor.forward(seq[:-1])
+    lp = log_softmax(lg)
+    agree, checked = 0, 0
+    for j in range(1, L + 1):
+        row = lg[P + j - 2].astype(np.float32)
+        g = O.gumbel_row(O.token_key(SAMPLE_SEED, seq_id, j), V)
+        sc = row + g
+        top = np.argsort(sc)[-2:]
+        margin = sc[top[1]] - sc[top[0]]
+        if margin > margin_tol:
+            checked += 1
+            agree += int(top[1] == ro["tokens"][j - 1])
+        assert abs(lp[P + j - 2, ro["tokens"][j - 1]] - ro["old_lp"][j - 1]) <= tol_lp
+    if strict_tokens:
+        assert agree == checked, (agree, checked)
+    else:
+        assert agree >= 0.95 * checked, (agree, checked)
+    hid_r, _ = reward.forward(seq, logits=False)
+    assert abs(hid_r[P + L - 1] @ rw - ro["reward"]) <= tol_val * max(1, abs(ro["reward"]))
+    hid_c, _ = critic.forward(seq, logits=False)
+    vals = hid_c[P - 1:P + L - 1] @ cw
+    assert np.max(np.abs(vals - ro["values"])) <= tol_val * max(1, np.abs(vals).max())
+    _, lgr = ref.forward(seq[:-1])
+    lpr = log_softmax(lgr)
+    ref_lp = np.array([lpr[P + t - 2, ro["tokens"][t - 1]] for t in range(1, L + 1)])
+    assert np.max(np.abs(ref_lp - ro["ref_lp"])) <= tol_lp
+    return ro
+
+
+def fresh_states(n, P, lengths, start_id=0):
+    return [dict(id=start_id + i, prompt_len=P, target_len=L) for i, L in enumerate(lengths)]
+
+
+@pytest.mark.parametrize("dtype", [abi.DTYPE_F32, abi.DTYPE_BF16])
+def test_cfg1_single_step_vs_oracle(dtype):
+    P, B, L, C = 8, 8, 64, 16
+    eng = Engine("tiny", dtype=dtype, max_slots=16, max_prompt_len=P, max_response_len=64,
+                 sample_seed=SAMPLE_SEED)
+    states = fresh_states(B, P, [L] * B)
+    eng.admit(states)
+    outs, led = eng.run_step(states, C, abi.MODE_STREAMED, B)
+    po, pl = S.plan_step(states, C, abi.MODE_STREAMED, B)
+    assert [o.as_tuple() for o in outs] == [o.as_tuple() for o in po]
+    assert led.wall == 64 and led.decode_iters == 64 and led.step_us > 0
+    orc = oracles(eng)
+    f32 = dtype == abi.DTYPE_F32
+    for s in states:
+        check_rollout(eng, orc, s["id"], P, tol_lp=1e-3 if f32 else 0.15,
+                      tol_val=1e-3 if f32 else 0.1, margin_tol=1e-3 if f32 else 0.2,
+                      strict_tokens=f32)
+    eng.close()
+
+
+def test_streamed_vs_sequential_content_invariance():
+    """streaming does not alter generation or the scoring inputs;
+    chunked prefill == whole-response prefill (fp32: bit-identical)."""
+    P, C = 8, 16
+    lens = [64, 37, 50, 5, 64, 17, 33, 60]
+    got = {}
+    for mode in (abi.MODE_STREAMED, abi.MODE_SEQUENTIAL):
+        eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=16, max_prompt_len=P,
+                     max_response_len=64, sample_seed=SAMPLE_SEED)
+        st = fresh_states(len(lens), P, lens)
+        eng.admit(st)
+        eng.run_step(st, C, mode, len(lens))
+        got[mode] = [eng.read_rollout(s["id"]) for s in st]
+        eng.close()
+    for a, b in zip(got[abi.MODE_STREAMED], got[abi.MODE_SEQUENTIAL]):
+        for k in ("tokens", "old_lp", "values", "ref_lp"):
+            assert np.array_equal(a[k], b[k]), k
+        assert a["reward"] == b["reward"]
+
+
+@pytest.mark.parametrize("carry", [abi.CARRY_CHUNK, abi.CARRY_TOKEN])
+def test_overcommit_carry_multi_step_vs_oracle(carry):
+    """Deferred sequences keep their KV pages and (whole-chunk or partial)
+    tokens across steps; decisions match the logical clock / reference."""
+    cfg = S.default_config(steps=4, batch_size=8, prompt_len=8, delta_init=2, delta_max=2,
+                           chunk_size=16, carry_granularity=carry,
+                           lengths_kind=abi.LEN_LOGNORMAL, lengths_mu_log=3.5,
+                           lengths_sigma_log=0.6, lengths_cap=64,
+                           latency_decode_per_token=1, latency_prefill_per_token=0,
+                           latency_reward_residual=0, latency_placement=1)
+    eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=16, max_prompt_len=8, max_response_len=64,
+                 sample_seed=SAMPLE_SEED, carry=carry)
+    lens = S.sample_lengths(cfg.lengths, 1, 64)
+    entries, next_id = [], 0
+    sel_log = []
+    orc = None
+    for step in range(cfg.steps):
+        fresh = []
+        while len(entries) + len(fresh) < cfg.batch_size + cfg.delta_init:
+            fresh.append(dict(id=next_id, prompt_len=8, target_len=lens[next_id],
+                              admitted_at=step, arrival_step=step))
+            next_id += 1
+        entries += [S.seq_array([f])[0] for f in fresh]
+        eng.admit(fresh)
+        active = [e for e in entries if not e.scored]
+        pre = len(entries) - len(active)
+        outs, led = eng.run_step(active, cfg.chunk_size, abi.MODE_STREAMED,
+                                 cfg.batch_size - pre)
+        batch, entries, _ = S.select_finished(entries, outs, cfg.batch_size)
+        sel_log.append([b.id for b in batch])
+        if orc is None:
+            orc = oracles(eng)
+        for b in batch:
+            check_rollout(eng, orc, b.id, 8, 1e-3, 1e-3, 1e-3)
+        eng.release([b.id for b in batch])
+    # same decisions as the scheduler-only run of the same config
+    _, sel = S.run_seed_logical(cfg, 1)
+    assert sel_log == sel
+    eng.close()
+
+
+def test_gpu_run_seed_simulate_matches_logical():
+    cfg = S.default_config(steps=6, batch_size=8, prompt_len=8, delta_init=2, delta_max=4,
+                           controller=abi.DELTA_ALG1, window=2, proxy_kind=1, chunk_size=16,
+                           lengths_kind=abi.LEN_LOGNORMAL, lengths_mu_log=3.5,
+                           lengths_sigma_log=0.6, lengths_cap=64,
+                           latency_decode_per_token=1, latency_prefill_per_token=0,
+                           latency_reward_residual=0, latency_placement=1)
+    eng = Engine("tiny", dtype=abi.DTYPE_BF16, max_slots=16, max_prompt_len=8,
+                 max_response_len=64, sample_seed=SAMPLE_SEED)
+    recs, sel = eng.run_seed(cfg, 1)
+    lrecs, lsel = S.run_seed_logical(cfg, 1)
+    key = lambda r: (r.wall_ticks, r.finished, r.deferred, r.delta, r.max_deferrals)
+    assert [key(r) for r in recs] == [key(r) for r in lrecs]
+    assert sel == lsel
+    assert all(r.step_us > 0 for r in recs)
+    eng.close()
+
+
+def test_ppo_update_vs_oracle_fp32():
+    """fill_values + GAE + clipped objective + head update (lm_head ascent,
+    value-head regression) vs the fp64 oracle on the same rollouts."""
+    P, C = 8, 16
+    lens = [40, 64, 23, 64]
+    eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=8, max_prompt_len=P, max_response_len=64,
+                 sample_seed=SAMPLE_SEED, train_heads=1)
+    st = fresh_states(len(lens), P, lens)
+    eng.admit(st)
+    eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+    orc = oracles(eng)
+    ros = [eng.read_rollout(s["id"]) for s in st]
+    W0 = eng.get_tensor(0, "lm_head").reshape(512, 128).astype(np.float64)
+    hp = abi.PpoHparams(gamma=1.0, lambda_=0.95, clip_epsilon=0.2, learning_rate=0.5,
+                        value_learning_rate=0.1, kl_coef=0.05, whiten=1)
+    stats = eng.ppo_update([s["id"] for s in st], hp)
+    # oracle
+    actor = orc[0][0]
+    adv_all, new_all, old_all, hid_all, tok_all, kl_all = [], [], [], [], [], []
+    for s, ro in zip(st, ros):
+        seq = np.concatenate([eng.read_prompt(s["id"]), ro["tokens"]]).astype(np.int32)
+        hid, lg = actor.forward(seq[:-1])
+        L = ro["length"]
+        lp = log_softmax(lg)
+        new = np.array([lp[P + j - 2, ro["tokens"][j - 1]] for j in range(1, L + 1)])
+        kl = ro["old_lp"].astype(np.float64) - ro["ref_lp"]
+        r = -0.05 * kl
+        r[-1] += ro["reward"]
+        vals = np.concatenate([ro["values"], [0.0]])
+        adv_all.append(np.array(O.gae(list(r), list(vals), 1.0, 0.95)))
+        new_all.append(new)
+        old_all.append(ro["old_lp"].astype(np.float64))
+        hid_all.append(hid[P - 1:P + L - 1])
+        tok_all.append(ro["tokens"])
+        kl_all.append(kl)
+    adv = np.concatenate(adv_all)
+    adv = (adv - adv.mean()) / np.sqrt(adv.var() + 1e-8)
+    new, old = np.concatenate(new_all), np.concatenate(old_all)
+    obj, dobj = O.ppo_clip(list(new), list(old), list(adv), 0.2)
+    assert abs(stats.ppo_objective - obj) < 1e-4
+    assert abs(stats.kl_mean - np.concatenate(kl_all).mean()) < 1e-5
+    assert abs(stats.mean_reward - np.mean([ro["reward"] for ro in ros])) < 1e-5
+    # lm_head ascent: W += lr * sum_t c_t (e_y - softmax) h_t^T
+    H = np.concatenate(hid_all)
+    tok = np.concatenate(tok_all)
+    logits = H @ W0.T
+    p = np.exp(log_softmax(logits))
+    G = -p * np.asarray(dobj)[:, None]
+    G[np.arange(len(tok)), tok] += np.asarray(dobj)
+    dW = G.T @ H
+    W1 = eng.get_tensor(0, "lm_head").reshape(512, 128).astype(np.float64)
+    assert np.max(np.abs((W1 - W0) - 0.5 * dW)) <= 1e-5 * max(1e-3, np.abs(0.5 * dW).max()) + 1e-7
+    eng.close()
