@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""OPPO PPO-RLHF step benchmark on B200 (BASELINE.json metric).
+
+Workload (configs[1]): 0.5B-shaped actor + 0.5B reward / critic / reference,
+bf16, 256 prompts of 128 tokens per GPU, lognormal(5.0, 1.0) response lengths
+capped at 1024, chunk 64, overcommit delta 26 (10%).  One step = refill ->
+run_step (lockstep actor decode || streamed scorer prefill) -> select the
+first B finishers -> PPO update (GAE, whitening, clipped loss, lm_head and
+value-head update).  Reported next to the same binary with overlap disabled
+(RunConfig::baseline(): delta 0, sequential scoring) and next to the
+reference's own CPU path (oracle/_ref run_seed, toy policy) on the host cores.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPO samples/sec per step (overlap vs sequential) at 1/2/4/8 B200; roofline %"
+CFG2 = dict(name="cfg2", actor="0.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
+            sigma=1.0, cap=1024, chunk=64, delta=26)
+TINY = dict(name="cfg1", actor="tiny", scorer="tiny", batch=8, prompt_len=8, mu=3.5, sigma=0.6,
+            cap=64, chunk=16, delta=2)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, gpu=0):
+        self.samples, self.proc, self.gpu = [], None, gpu
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- our arm
+def host_prompts(ids, P, V, seed):
+    """Synthetic prompt tokens on the host (the e2e path copies them in)."""
+    out = []
+    for i in ids:
+        rng = np.random.default_rng([seed, int(i)])
+        out.append(rng.integers(0, V, size=P, dtype=np.int32))
+    return out
+
+
+def run_arm(eng, wl, cfg, seed, steps, warmup, rank, world, dist):
+    """Python-side driver loop over the C ABI (driver.cpp:103-195), host prompts
+    copied in at admission and step results read back every step."""
+    from paper_2509_25762_b200 import abi
+    from paper_2509_25762_b200 import scheduler as S
+    import torch
+
+    B = cfg.batch_size
+    lengths = S.sample_lengths(cfg.lengths, seed ^ rank, 50000)
+    ctl = S.DeltaController(cfg.controller, cfg.window, cfg.delta_min, cfg.delta_max,
+                            cfg.delta_inc, cfg.delta_dec)
+    hp = cfg.ppo
+    entries, next_id, delta = [], 0, cfg.delta_init
+    V = eng.cfg.actor.vocab
+    P = cfg.prompt_len
+    recs = []
+
+    def one_step(step):
+        nonlocal entries, next_id, delta
+        t0 = time.perf_counter()
+        fresh = []
+        while len(entries) + len(fresh) < B + delta:
+            fresh.append(S.seq_array([dict(id=next_id, prompt_len=P, target_len=lengths[next_id],
+                                           admitted_at=step, arrival_step=step)])[0])
+            next_id += 1
+        h2d = 0
+        if fresh:
+            pr = host_prompts([f.id for f in fresh], P, V, 1234 + rank)
+            eng.admit(fresh, prompts=pr)
+            h2d += sum(p.nbytes for p in pr) + len(fresh) * C.sizeof(abi.SeqState)
+        entries = entries + fresh
+        active = [e for e in entries if not e.scored]
+        pre = len(entries) - len(active)
+        need = B - pre
+        outs, led = [], abi.Ledger()
+        if active and need > 0:
+            outs, led = eng.run_step(active, cfg.chunk_size, cfg.schedule_mode, need)
+            h2d += len(active) * C.sizeof(abi.SeqState)
+        batch, entries, _ = S.select_finished(entries, outs, B)
+        ids = [b.id for b in batch]
+        st = eng.ppo_update(ids, hp) if ids else abi.PpoStats()
+        eng.release(ids)
+        ctl.observe(st.mean_reward)
+        delta, _ = ctl.update(delta)
+        d2h = len(outs) * C.sizeof(abi.SeqOutcome) + C.sizeof(abi.PpoStats) + \
+            int(st.n_tokens) * 4 + len(ids) * 4
+        wall = time.perf_counter() - t0
+        return dict(samples=len(ids), step_us=led.step_us, update_us=st.update_us, wall_s=wall,
+                    decode_us=led.decode_us, score_us=led.score_us, iters=led.decode_iters,
+                    decode_tokens=led.decode_tokens, prefill_tokens=led.prefill_tokens,
+                    launches=led.kernel_launches, h2d=h2d, d2h=d2h, tokens=int(st.n_tokens),
+                    reward=st.mean_reward, obj=st.ppo_objective)
+
+    for s in range(warmup):
+        one_step(s)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(warmup, warmup + steps):
+        recs.append(one_step(s))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    wall = time.perf_counter() - t0
+    return recs, wall
+
+
+def make_cfg(wl, baseline=False):
+    from paper_2509_25762_b200 import abi
+    from paper_2509_25762_b200 import scheduler as S
+    cfg = S.default_config(
+        mode=abi.RUN_TRAIN, steps=1000, batch_size=wl["batch"], prompt_len=wl["prompt_len"],
+        delta_init=wl["delta"], delta_min=0, delta_max=wl["delta"], chunk_size=wl["chunk"],
+        schedule_mode=abi.MODE_STREAMED, carry_granularity=abi.CARRY_TOKEN,
+        lengths_kind=abi.LEN_LOGNORMAL, lengths_mu_log=wl["mu"], lengths_sigma_log=wl["sigma"],
+        lengths_cap=wl["cap"], latency_decode_per_token=1, latency_prefill_per_token=0,
+        latency_reward_residual=0, latency_placement=abi.PLACE_DISAGGREGATED,
+        ppo_gamma=1.0, ppo_lambda=0.95, ppo_clip_epsilon=0.2, ppo_learning_rate=1e-3,
+        ppo_value_learning_rate=1e-3, ppo_kl_coef=0.05, ppo_whiten=1)
+    return S.baseline(cfg) if baseline else cfg
+
+
+def kernel_roofline(hbm_peak):
+    """Dominant decode kernel class alone: the gate|up projection GEMM of the
+    0.5B actor at the step's full decode batch (M=282 sequences), swept over 24
+    distinct layer weights so they stream from HBM (24 x 17.4 MB > 126 MB L2)."""
+    from paper_2509_25762_b200._lib import lib
+    M, N, K = 282, 2 * 4864, 896
+    us = C.c_float()
+    st = lib().oppo_k_gemm_bench(M, N, K, 24, 240, 2, C.byref(us))
+    if st != 0:
+        return None
+    algo = N * K * 2 + M * K * 2 + M * (N // 2) * 2  # weights + activations in + SwiGLU out
+    ach = algo / (us.value * 1e-6) / 1e9
+    return {"kernel": "gemm_bf16_tc (tcgen05+TMA) decode gate|up, M=282 N=9728 K=896",
+            "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(ach / hbm_peak, 4), "traffic": None,
+            "algorithmic_bytes_per_launch": algo, "avg_launch_us": round(us.value, 3)}
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    """The reference's own path (oracle/_ref = /root/reference core compiled here):
+    run_seed in train mode (tabular policy, V=16) at this workload's B / delta /
+    chunk / length distribution, one seed per host core."""
+    try:
+        from oracle import ref as R
+        if not R.available():
+            return None
+        from paper_2509_25762_b200 import abi
+        from paper_2509_25762_b200 import scheduler as S
+        cores = os.cpu_count() or 1
+        cfg = make_cfg(wl)
+        S.set_field(cfg, "vocab", 16)
+        S.set_field(cfg, "ppo_learning_rate", 0.1)
+        S.set_field(cfg, "ppo_value_learning_rate", 0.2)
+        cfg.carry_granularity = 0
+        cfg.steps = 2
+        t = time.perf_counter()
+        R.run_seeds_parallel(cfg, list(range(1, cores + 1)))
+        per = (time.perf_counter() - t) / 2
+        cfg.steps = max(2, int(budget_s / max(per, 1e-3)))
+        t = time.perf_counter()
+        fin = R.run_seeds_parallel(cfg, list(range(1, cores + 1)))
+        dt = time.perf_counter() - t
+        return {"value": round(fin / dt, 1), "unit": "samples/s", "cores": cores,
+                "kind": "reference",
+                "sample": f"rlpipe::run_seed train mode (toy tabular policy V=16), B={wl['batch']}, "
+                          f"delta={wl['delta']}, C={wl['chunk']}, LN({wl['mu']},{wl['sigma']}) cap "
+                          f"{wl['cap']}, {cfg.steps} steps x {cores} seeds in {dt:.1f}s"}
+    except Exception as ex:  # the baseline is reported, never required
+        return {"value": None, "error": str(ex)[:200]}
+
+
+def ours(args):
+    import torch
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    torch.cuda.set_device(local)
+    from paper_2509_25762_b200 import abi
+    from paper_2509_25762_b200.engine import Engine, param_count, SHAPES
+
+    wl = TINY if args.workload == "cfg1" else CFG2
+    hbm, tflops, peak_src = peaks()
+    res = {}
+    arms = [("oppo", False)] + ([] if args.no_sequential else [("sequential", True)])
+    clocks = ClockSampler(local)
+    with clocks:
+        for name, base in arms:
+            cfg = make_cfg(wl, base)
+            eng = Engine(wl["actor"], wl["scorer"], wl["scorer"], wl["scorer"], dtype=abi.DTYPE_BF16,
+                         max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
+                         max_response_len=wl["cap"], page_size=64, device=local,
+                         carry=cfg.carry_granularity, train_heads=1, sample_seed=2 + rank,
+                         weight_seed=1)
+            recs, wall = run_arm(eng, wl, cfg, 7, args.steps, args.warmup, rank, world, dist)
+            eng.close()
+            torch.cuda.empty_cache()
+            dev_s = sum(r["step_us"] + r["update_us"] for r in recs) * 1e-6
+            gen_s = sum(r["step_us"] for r in recs) * 1e-6
+            samples = sum(r["samples"] for r in recs)
+            t = torch.tensor([dev_s, gen_s, wall, float(samples)], dtype=torch.float64, device="cuda")
+            if dist:
+                mx = t.clone()
+                dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+                sm = t.clone()
+                dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+                dev_s, gen_s, wall = mx[0].item(), mx[1].item(), mx[2].item()
+                samples = sm[3].item()
+            res[name] = dict(recs=recs, dev_s=dev_s, gen_s=gen_s, wall=wall, samples=samples)
+    if rank != 0:
+        return
+    o = res["oppo"]
+    value = o["samples"] / o["dev_s"]
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(o["dev_s"] / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic prompts (host-generated tokens), random-init N(0,0.02) weights",
+        "config": {"workload": f"{wl['name']}: {wl['actor']} actor + 3x {wl['scorer']} scorers "
+                               f"(reward/critic/ref), B={wl['batch']}/GPU, prompt {wl['prompt_len']}, "
+                               f"LN({wl['mu']},{wl['sigma']}) cap {wl['cap']}, chunk {wl['chunk']}, "
+                               f"delta {wl['delta']}, token-granular carry",
+                   "global_batch": wl["batch"] * world, "parallelism": f"dp{world}",
+                   "params_per_model": param_count(SHAPES[wl["actor"]]),
+                   "l2": "working set > L2 (4 models x ~1 GB bf16 weights + paged KV)",
+                   "value_def": "samples / device time of (generation + scoring + PPO update)"},
+        "gen_score_samples_per_s": round(o["samples"] / o["gen_s"], 2),
+    }
+    if "sequential" in res:
+        s = res["sequential"]
+        line["sequential"] = {"value": round(s["samples"] / s["dev_s"], 2),
+                              "gen_score_samples_per_s": round(s["samples"] / s["gen_s"], 2),
+                              "ms_per_step": round(s["dev_s"] / args.steps * 1e3, 3)}
+        line["speedup_vs_sequential"] = round(value / line["sequential"]["value"], 3)
+        line["speedup_vs_sequential_gen_score"] = round(
+            line["gen_score_samples_per_s"] / line["sequential"]["gen_score_samples_per_s"], 3)
+    rec = o["recs"]
+    line["e2e"] = {"value": round(o["samples"] / o["wall"], 2), "unit": "samples/s",
+                   "h2d_bytes_per_step": int(np.mean([r["h2d"] for r in rec])),
+                   "d2h_bytes_per_step": int(np.mean([r["d2h"] for r in rec]))}
+    line["step_detail"] = {
+        "decode_iters": int(np.mean([r["iters"] for r in rec])),
+        "decode_ms": round(np.mean([r["decode_us"] for r in rec]) / 1e3, 2),
+        "score_end_ms": round(np.mean([r["score_us"] for r in rec]) / 1e3, 2),
+        "update_ms": round(np.mean([r["update_us"] for r in rec]) / 1e3, 2),
+        "tokens_per_step": int(np.mean([r["tokens"] for r in rec])),
+        "prefill_tokens_per_step": int(np.mean([r["prefill_tokens"] for r in rec])),
+    }
+    line["roofline"] = kernel_roofline(hbm)
+    if line["roofline"]:
+        line["roofline"]["peak_source"] = peak_src + " (MEASURED_PEAKS.json hbm_gbs, burst)"
+    line["cpu_baseline"] = cpu_baseline(wl) if not args.no_cpu else None
+    line["clocks"] = clocks.summary()
+    line["gpu_launches"] = int(sum(r["launches"] for r in rec))
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, the unmodified /root/reference core) on the host cores."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    wl = TINY if args.workload == "cfg1" else CFG2
+    try:
+        from oracle import ref as R
+        from paper_2509_25762_b200 import scheduler as S
+        if not R.available():
+            raise FileNotFoundError("oracle/_ref/librlpipe_ref.so not built")
+        cores = os.cpu_count() or 1
+        cfg = make_cfg(wl)
+        S.set_field(cfg, "vocab", 16)
+        S.set_field(cfg, "ppo_learning_rate", 0.1)
+        S.set_field(cfg, "ppo_value_learning_rate", 0.2)
+        cfg.carry_granularity = 0
+        cfg.steps = 1
+        for _ in range(args.warmup):
+            R.run_seeds_parallel(cfg, list(range(1, cores + 1)))
+        tot, fin = 0.0, 0
+        for k in range(args.steps):
+            t = time.perf_counter()
+            fin += R.run_seeds_parallel(cfg, list(range(100 + k * cores, 100 + (k + 1) * cores)))
+            tot += time.perf_counter() - t
+        v = fin / tot
+        line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "samples/s",
+                "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference toy policy)",
+                "config": {"workload": f"{wl['name']} scheduling shape, reference toy policy V=16"},
+                "cpu_baseline": {"value": round(v, 2), "unit": "samples/s", "cores": cores,
+                                 "kind": "reference",
+                                 "sample": f"one rlpipe::run_seed step per seed x {cores} seeds per step"},
+                "e2e": {"value": round(v, 2), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+    except Exception as ex:
+        line = {"impl": "reference", "unavailable": str(ex)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg1"])
+    ap.add_argument("--no-sequential", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -384,6 +384,10 @@ oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
                         const void* d_w, const void* d_bias, void* d_y, int32_t epilogue,
                         void* stream);
 
+/* Times the engine GEMM alone over `copies` distinct weight matrices; avg_us per launch. */
+oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_t copies, int32_t reps,
+                              int32_t epilogue, float* avg_us);
+
 #ifdef __cplusplus
 }
 #endif

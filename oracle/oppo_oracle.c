@@ -588,7 +588,7 @@ float oracle_gumbel(uint64_t key, uint32_t v) {
     uint32_t x = (uint32_t)key ^ (v * 0x9e3779b9u);
     x = lowbias32(x) ^ (uint32_t)(key >> 32);
     x = lowbias32(x);
-    const float u = ((float)(x >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float u = ((float)(x >> 9) + 0.5f) * (1.0f / 8388608.0f);
     return -logf(-logf(u));
 }
 int32_t oracle_prompt_token(uint64_t seed, int64_t id, int32_t q, int32_t vocab) {

@@ -108,6 +108,7 @@ def _declare(L):
         "oppo_k_ppo_token": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, dbl, dbl, dbl, i32, vp,
                                    vp, vp, vp, vp]),
         "oppo_k_gemm": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, vp]),
+        "oppo_k_gemm_bench": (i32, [i32, i32, i32, i32, i32, i32, P(C.c_float)]),
     }
     for name, (res, args) in eng.items():
         f = getattr(L, name, None)

@@ -1448,3 +1448,47 @@ oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
 }
 
 }  // extern "C"
+
+// Times the engine GEMM alone: `copies` distinct weight matrices (a layer
+// stack, so weights stream from HBM rather than L2), `reps` back-to-back
+// launches on one stream bracketed by CUDA events.  avg_us = per launch.
+extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_t copies,
+                                         int32_t reps, int32_t epilogue, float* avg_us) {
+    try {
+        cudaStream_t st;
+        OPPO_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        __nv_bfloat16 *x = nullptr, *w = nullptr, *y = nullptr;
+        const size_t wn = static_cast<size_t>(N) * K;
+        OPPO_CUDA_CHECK(cudaMalloc(&x, static_cast<size_t>(M) * K * 2));
+        OPPO_CUDA_CHECK(cudaMalloc(&w, wn * copies * 2));
+        OPPO_CUDA_CHECK(cudaMalloc(&y, static_cast<size_t>(M) * N * 4));
+        oppo::init_normal<__nv_bfloat16><<<(M * K + 255) / 256, 256, 0, st>>>(x, static_cast<int64_t>(M) * K, 1, 1, 1.0f);
+        oppo::init_normal<__nv_bfloat16><<<static_cast<int>((wn * copies + 255) / 256), 256, 0, st>>>(
+            w, static_cast<int64_t>(wn * copies), 1, 2, 0.02f);
+        for (int i = 0; i < 3; ++i)
+            oppo::gemm_standalone(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, nullptr, y,
+                                  epilogue, st);
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        OPPO_CUDA_CHECK(cudaEventRecord(a, st));
+        for (int i = 0; i < reps; ++i)
+            oppo::gemm_standalone(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, nullptr, y,
+                                  epilogue, st);
+        OPPO_CUDA_CHECK(cudaEventRecord(b, st));
+        OPPO_CUDA_CHECK(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        *avg_us = ms * 1e3f / reps;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(x);
+        cudaFree(w);
+        cudaFree(y);
+        cudaStreamDestroy(st);
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}

@@ -47,7 +47,9 @@ __host__ __device__ __forceinline__ float key_uniform(uint64_t key, uint32_t v) 
     uint32_t x = static_cast<uint32_t>(key) ^ (v * 0x9e3779b9u);
     x = lowbias32(x) ^ static_cast<uint32_t>(key >> 32);
     x = lowbias32(x);
-    return (static_cast<float>(x >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    // 23 random bits: the largest value, 1 - 2^-24, is exactly representable (24 bits
+    // would round up to 1.0f and give an infinite Gumbel draw)
+    return (static_cast<float>(x >> 9) + 0.5f) * (1.0f / 8388608.0f);
 }
 __device__ __forceinline__ float gumbel_noise(uint64_t key, uint32_t v) {
     return -logf(-logf(key_uniform(key, v)));

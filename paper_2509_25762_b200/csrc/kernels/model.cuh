@@ -395,6 +395,7 @@ static __global__ void logits_combine(const float4* __restrict__ partials, int n
     if (lse_out) lse_out[r] = lse;
     const size_t at = slot ? static_cast<size_t>(slot[r]) * buf_stride + tidx[r] : r;
     if (keys) {  // sampled: logit = perturbed score - its noise
+        if (bi < 0 || bi >= n_tiles * 128) bi = 0;  // memory safety only (non-finite logits)
         const float logit = best - gumbel_noise(keys[r], static_cast<uint32_t>(bi));
         tok_buf[at] = bi;
         lp_buf[at] = logit - lse;
