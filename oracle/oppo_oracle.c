@@ -595,3 +595,54 @@ int32_t oracle_prompt_token(uint64_t seed, int64_t id, int32_t q, int32_t vocab)
     const uint64_t h = mix64(seed ^ 0x70726f6d7074ull ^ mix64((uint64_t)id * 0x100000001b3ull + (uint64_t)q));
     return (int32_t)(h % (uint64_t)vocab);
 }
+
+/* The engine's two-level categorical draw (kernels/gemm.cuh logits_tile +
+ * kernels/model.cuh logits_combine) on fp64 logits:
+ *   block b* = argmax_b (lse_b + Gumbel(key ^ kBlockKey, b)), blocks of 256 ids;
+ *   inside b*: first id whose running sum of exp(x - max_b) exceeds
+ *   U(key ^ kInBlockKey, b*) * sum_b (fallback: the block's last id).
+ * margins: gap between the two best block scores, and the relative distance
+ * of the in-block threshold from the nearest cumulative-sum boundary. */
+static float key_uniform_o(uint64_t key, uint32_t v) {
+    uint32_t x = (uint32_t)key ^ (v * 0x9e3779b9u);
+    x = lowbias32(x) ^ (uint32_t)(key >> 32);
+    x = lowbias32(x);
+    return ((float)(x >> 9) + 0.5f) * (1.0f / 8388608.0f);
+}
+int oracle_sample_token(const double* x, int V, uint64_t key, double* lp_out,
+                        double* margin_block, double* margin_inblock) {
+    const uint64_t kIn = 0x696e626c6f636bull, kBlk = 0x626c6f636b6e7a65ull;
+    const int SB = 256, nb = (V + SB - 1) / SB;
+    double best = -INFINITY, second = -INFINITY, tot_m = -INFINITY;
+    int bb = 0;
+    for (int b = 0; b < nb; ++b)
+        for (int i = b * SB; i < V && i < (b + 1) * SB; ++i) if (x[i] > tot_m) tot_m = x[i];
+    double tot = 0.0;
+    for (int i = 0; i < V; ++i) tot += exp(x[i] - tot_m);
+    for (int b = 0; b < nb; ++b) {
+        const int a = b * SB, e = (b + 1) * SB < V ? (b + 1) * SB : V;
+        double m = -INFINITY, se = 0.0;
+        for (int i = a; i < e; ++i) if (x[i] > m) m = x[i];
+        for (int i = a; i < e; ++i) se += exp(x[i] - m);
+        const double sc = m + log(se) + (double)oracle_gumbel(key ^ kBlk, (uint32_t)b);
+        if (sc > best) { second = best; best = sc; bb = b; }
+        else if (sc > second) second = sc;
+    }
+    *margin_block = best - second;
+    const int a = bb * SB, e = (bb + 1) * SB < V ? (bb + 1) * SB : V;
+    double m = -INFINITY, se = 0.0;
+    for (int i = a; i < e; ++i) if (x[i] > m) m = x[i];
+    for (int i = a; i < e; ++i) se += exp(x[i] - m);
+    const double thr = (double)key_uniform_o(key ^ kIn, (uint32_t)bb) * se;
+    double run = 0.0, gap = INFINITY;
+    int pick = e - 1;
+    for (int i = a; i < e; ++i) {
+        run += exp(x[i] - m);
+        const double d = fabs(run - thr);
+        if (d < gap) gap = d;
+        if (run > thr) { pick = i; break; }
+    }
+    *margin_inblock = gap / se;
+    *lp_out = x[pick] - tot_m - log(tot);
+    return pick;
+}

@@ -36,6 +36,8 @@ def lib():
         L.oracle_token_key.restype = u64
         L.oracle_gumbel.argtypes = [u64, C.c_uint32]
         L.oracle_gumbel.restype = C.c_float
+        L.oracle_sample_token.argtypes = [P(dbl), C.c_int, u64, P(dbl), P(dbl), P(dbl)]
+        L.oracle_sample_token.restype = C.c_int
         L.oracle_prompt_token.argtypes = [u64, i64, i32, i32]
         L.oracle_prompt_token.restype = i32
         _L = L
@@ -141,6 +143,15 @@ def token_key(seed, seq, pos):
 def gumbel_row(key, V):
     g = lib().oracle_gumbel
     return np.array([g(key, v) for v in range(V)], dtype=np.float32)
+
+
+def sample_token(logits, key):
+    """(token, log-prob, block margin, in-block margin) of the engine's two-level draw."""
+    x = np.ascontiguousarray(logits, dtype=np.float64)
+    lp, mb, mi = C.c_double(), C.c_double(), C.c_double()
+    tok = lib().oracle_sample_token(x.ctypes.data_as(C.POINTER(C.c_double)), len(x), key,
+                                    C.byref(lp), C.byref(mb), C.byref(mi))
+    return tok, lp.value, mb.value, mi.value
 
 
 def prompt_tokens(seed, seq_id, P, V):

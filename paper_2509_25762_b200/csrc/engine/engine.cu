@@ -189,7 +189,7 @@ void alloc_work(Engine& e, Work& w, int rows, bool lm_rows) {
     w.ff = dalloc(R * fmax_ * sizeof(T));
     w.head_out = static_cast<float*>(dalloc(R * 4));
     const int lm_R = lm_rows ? rows : rows;
-    w.partials = static_cast<float4*>(dalloc(static_cast<size_t>(lm_R) * cdiv(vmax, 128) * 16));
+    w.partials = static_cast<float4*>(dalloc(static_cast<size_t>(lm_R) * gemm_logit_tiles(dtype_of<T>(), vmax) * 16));
     w.tgt_logit = static_cast<float*>(dalloc(R * 4));
     w.lse = static_cast<float*>(dalloc(R * 4));
     w.lm_in = dalloc(R * dmax * sizeof(T));
@@ -716,7 +716,7 @@ void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, in
             ep.keys = nullptr;
             gemm_run(e, w, st, w.lm_in, p.n_lm, D, D, m.lm_head, m.dims.vocab, D, ep);
             logits_combine<<<cdiv(p.n_lm, 4), 128, 0, st>>>(
-                w.partials, cdiv(m.dims.vocab, 128), p.n_lm, nullptr, w.tgt_logit, w.lm_slot, w.lm_t,
+                w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, p.n_lm, nullptr, w.tgt_logit, w.lm_slot, w.lm_t,
                 nullptr, e.d_ref_lp, e.tok_stride, nullptr, nullptr);
         }
         if (p.n_pend > 0)
@@ -749,7 +749,7 @@ void decode_iteration(Engine& e, const DecodeSeq* dseq, int M, int it, int max_c
     ep.keys = w.meta.key;
     const int D = m.dims.d_model;
     gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
-    logits_combine<<<cdiv(M, 4), 128, 0, st>>>(w.partials, cdiv(m.dims.vocab, 128), M, w.meta.key,
+    logits_combine<<<cdiv(M, 4), 128, 0, st>>>(w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, M, w.meta.key,
                                                nullptr, w.meta.slot, w.meta.t, e.d_tok, e.d_old_lp,
                                                e.tok_stride, nullptr, nullptr);
     e.launches += 3;
@@ -1051,7 +1051,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         stats = d_stats;
     }
     // current-policy log-probs of the sampled tokens from the cached actor hidden states
-    const int nt = cdiv(V, 128);
+    const int nt = gemm_logit_tiles(e.dtype, V);
     Work& w = e.ws;
     const int chunk_rows = std::max(32, std::min(w.max_rows, static_cast<int>((static_cast<size_t>(64) << 20) / (nt * 16))));
     for (int c0 = 0; c0 < N; c0 += chunk_rows) {
@@ -1063,7 +1063,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         ep.targets = d_tokv + c0;
         gemm_run(e, w, st, d_hf + static_cast<size_t>(c0) * Da, cn, Da, Da, actor.lm_head, V, Da, ep);
         // contiguous rows: new_lp[c0 + r] = logit[target] - lse
-        logits_combine<<<cdiv(cn, 4), 128, 0, st>>>(w.partials, nt, cn, nullptr, w.tgt_logit, nullptr,
+        logits_combine<<<cdiv(cn, 4), 128, 0, st>>>(w.partials, nt, V, cn, nullptr, w.tgt_logit, nullptr,
                                                     nullptr, nullptr, d_new + c0, 0, d_lse + c0, nullptr);
     }
     // K10 clipped objective and d obj / d logp
@@ -1465,16 +1465,35 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
         oppo::init_normal<__nv_bfloat16><<<(M * K + 255) / 256, 256, 0, st>>>(x, static_cast<int64_t>(M) * K, 1, 1, 1.0f);
         oppo::init_normal<__nv_bfloat16><<<static_cast<int>((wn * copies + 255) / 256), 256, 0, st>>>(
             w, static_cast<int64_t>(wn * copies), 1, 2, 0.02f);
-        for (int i = 0; i < 3; ++i)
-            oppo::gemm_standalone(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, nullptr, y,
-                                  epilogue, st);
+        // LOGITS needs partials / keys: run through an EpiParams with real buffers
+        float4* parts = nullptr;
+        uint64_t* keys = nullptr;
+        float* tl = nullptr;
+        if (epilogue == oppo::EPI_LOGITS) {
+            OPPO_CUDA_CHECK(cudaMalloc(&parts, static_cast<size_t>(M) * oppo::gemm_logit_tiles(OPPO_DTYPE_BF16, N) * 16));
+            OPPO_CUDA_CHECK(cudaMalloc(&keys, static_cast<size_t>(M) * 8));
+            OPPO_CUDA_CHECK(cudaMalloc(&tl, static_cast<size_t>(M) * 4));
+            OPPO_CUDA_CHECK(cudaMemset(keys, 0x5a, static_cast<size_t>(M) * 8));
+        }
+        auto launch = [&](int i) {
+            if (epilogue == oppo::EPI_LOGITS) {
+                oppo::EpiParams ep{};
+                ep.mode = oppo::EPI_LOGITS;
+                ep.partials = parts;
+                ep.keys = keys;
+                ep.tgt_logit = tl;
+                oppo::gemm_with_params(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, ep, st);
+            } else {
+                oppo::gemm_standalone(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, nullptr, y,
+                                      epilogue, st);
+            }
+        };
+        for (int i = 0; i < 3; ++i) launch(i);
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         OPPO_CUDA_CHECK(cudaEventRecord(a, st));
-        for (int i = 0; i < reps; ++i)
-            oppo::gemm_standalone(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, nullptr, y,
-                                  epilogue, st);
+        for (int i = 0; i < reps; ++i) launch(i);
         OPPO_CUDA_CHECK(cudaEventRecord(b, st));
         OPPO_CUDA_CHECK(cudaEventSynchronize(b));
         float ms = 0;
@@ -1485,6 +1504,9 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
         cudaFree(x);
         cudaFree(w);
         cudaFree(y);
+        if (parts) cudaFree(parts);
+        if (keys) cudaFree(keys);
+        if (tl) cudaFree(tl);
         cudaStreamDestroy(st);
         return OPPO_OK;
     } catch (const oppo::Error& x) {

@@ -159,5 +159,8 @@ void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, 
 void gemm_standalone(int dtype, int M, int N, int K, const void* x, const void* w,
                      const float* bias, void* y, int epi, cudaStream_t st);
 CUtensorMap make_tma_2d(const void* ptr, int rows, int cols, int ld, int box_rows);
+int gemm_logit_tiles(int dtype, int N);  // partial tiles per row of an EPI_LOGITS GEMM
+void gemm_with_params(int dtype, int M, int N, int K, const void* x, const void* w,
+                      const EpiParams& ep, cudaStream_t st);
 
 }  // namespace oppo

@@ -27,7 +27,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <int BN>
-void launch_tc(const CUtensorMap& mw, const CUtensorMap& mx, dim3 grid, const GemmShape& sh,
+void launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, dim3 grid, const GemmShape& sh,
                const EpiParams& ep, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
@@ -36,7 +36,7 @@ void launch_tc(const CUtensorMap& mw, const CUtensorMap& mx, dim3 grid, const Ge
                                              tc::Cfg<BN>::SMEM));
         attr = true;
     }
-    tc::gemm_bf16_tc<BN><<<grid, 128, tc::Cfg<BN>::SMEM, st>>>(mw, mx, sh, ep);
+    tc::gemm_bf16_tc<BN><<<grid, 128, tc::Cfg<BN>::SMEM, st>>>(mx, mw, sh, ep);
 }
 }  // namespace
 
@@ -70,9 +70,12 @@ static const CUtensorMap& cached_map(Engine* e, const void* ptr, int rows, int c
     return it->second;
 }
 
-// x: [M, K] (ld ldx), w: [N, K] (ld ldw).  For bf16 the token rows of the
-// TMA map span the whole workspace (w.max_rows) so the cached descriptor is
-// reused across iterations; rows >= M only feed masked output columns.
+int gemm_logit_tiles(int, int N) { return (N + kSampleBlock - 1) / kSampleBlock; }
+
+// x: [M, K] (ld ldx), w: [N, K] (ld ldw).  bf16: 128-token tiles (A operand,
+// zero-filled past M by TMA) x BN-row weight tiles; BN = 256 for prefill and
+// the lm_head, 64/128 for decode so the grid covers the SMs; split-K when the
+// tile count is still under half the SMs.
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
                       const void* wt, int N, int ldw, const EpiParams& ep_in, int dtype,
                       int num_sms, float* ws, size_t ws_floats, int* cnt, int cnt_n) {
@@ -80,35 +83,28 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     EpiParams ep = ep_in;
     ep.M = M;
     ep.N = N;
-    GemmShape sh{M, N, K, 1, 0, nullptr, nullptr, 32};
+    ep.n_tiles = gemm_logit_tiles(dtype, N);
+    GemmShape sh{M, N, K, 1, 0, nullptr, nullptr};
+    const int m_tiles = (M + 127) / 128;
     if (dtype == OPPO_DTYPE_F32) {
-        ep.n_tiles = (N + 127) / 128;
-        dim3 grid((N + 127) / 128, (M + 31) / 32);
         if (ldx != K || ldw != K) throw Error(OPPO_ERR_INTERNAL, "SIMT GEMM needs packed rows");
-        gemm_simt<float><<<grid, 128, 0, st>>>(static_cast<const float*>(x),
-                                               static_cast<const float*>(wt), sh, ep);
+        gemm_simt<float><<<dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock), 128, 0, st>>>(
+            static_cast<const float*>(x), static_cast<const float*>(wt), sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
-    // token tile: UMMA_N = bn (multiple of 16, <= 256)
-    const int m_tiles = (M + 255) / 256;
-    int bn = (M + m_tiles - 1) / m_tiles;
-    bn = (bn + 15) / 16 * 16;
-    int BN = 32;
-    while (BN < bn) BN *= 2;
-    const int n_tiles = (N + 127) / 128;
-    ep.n_tiles = n_tiles;
+    int BN;
+    if (ep.mode == EPI_LOGITS || M > 256) BN = 256;
+    else BN = N >= 128 * (num_sms / 2) ? 128 : 64;
+    const int n_tiles = (N + BN - 1) / BN;
     const int kb = (K + 63) / 64;
     const int tiles = n_tiles * m_tiles;
     int splits = 1;
-    if (ws && cnt && tiles * 2 <= num_sms && kb >= 8) {
-        splits = std::min(kb / 4, (num_sms + tiles - 1) / tiles);
-        splits = std::max(1, splits);
-        const size_t need = static_cast<size_t>(splits) * tiles * 128 * BN;
+    if (ws && cnt && ep.mode != EPI_LOGITS && tiles * 2 <= num_sms && kb >= 4) {
+        splits = std::max(1, std::min(kb / 2, num_sms / tiles));
         while (splits > 1 && (static_cast<size_t>(splits) * tiles * 128 * BN > ws_floats ||
                               tiles > cnt_n))
             --splits;
-        (void)need;
     }
     const int kbps = (kb + splits - 1) / splits;
     splits = (kb + kbps - 1) / kbps;
@@ -116,29 +112,23 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     sh.kb_per_split = kbps;
     sh.workspace = ws;
     sh.counters = cnt;
-    sh.bn = bn;
-    const int x_rows = wk ? std::max(wk->max_rows, M) : M;
     CUtensorMap s1, s2;
-    const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 128, s1);
-    const CUtensorMap& mx = cached_map(wk ? e : nullptr, x, x_rows, K, ldx, bn, s2);
-    dim3 grid(n_tiles, m_tiles, splits);
-    (void)BN;
-    // the runtime UMMA_N is bn; BN picks the TMEM allocation / smem carve-out
+    const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
+    const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, BN, s2);
+    const dim3 grid(m_tiles, n_tiles, splits);
     switch (BN) {
-    case 32:
-        launch_tc<32>(mw, mx, grid, sh, ep, st);
-        break;
     case 64:
-        launch_tc<64>(mw, mx, grid, sh, ep, st);
+        launch_tc<64>(mx, mw, grid, sh, ep, st);
         break;
     case 128:
-        launch_tc<128>(mw, mx, grid, sh, ep, st);
+        launch_tc<128>(mx, mw, grid, sh, ep, st);
         break;
     default:
-        launch_tc<256>(mw, mx, grid, sh, ep, st);
+        launch_tc<256>(mx, mw, grid, sh, ep, st);
         break;
     }
     OPPO_CUDA_CHECK(cudaGetLastError());
+    (void)wk;
 }
 
 void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
@@ -156,6 +146,14 @@ void gemm_standalone(int dtype, int M, int N, int K, const void* x, const void* 
     ep.ldy = epi == EPI_SWIGLU ? N / 2 : N;
     ep.bias = bias;
     ep.scale = 1.0f;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gemm_impl(nullptr, nullptr, st, x, M, K, K, w, N, K, ep, dtype, sms, nullptr, 0, nullptr, 0);
+}
+
+void gemm_with_params(int dtype, int M, int N, int K, const void* x, const void* w,
+                      const EpiParams& ep, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

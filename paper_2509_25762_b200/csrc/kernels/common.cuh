@@ -55,6 +55,12 @@ __device__ __forceinline__ float gumbel_noise(uint64_t key, uint32_t v) {
     return -logf(-logf(key_uniform(key, v)));
 }
 
+// Two-level sampling streams (see gemm.cuh logits_tile / model.cuh logits_combine):
+// vocabulary blocks of kSampleBlock ids, per-block Gumbel noise and in-block uniform.
+constexpr int kSampleBlock = 256;
+constexpr uint64_t kInBlockKey = 0x696e626c6f636bull;  // "inblock"
+constexpr uint64_t kBlockKey = 0x626c6f636b6e7a65ull;  // "blocknze"
+
 // ------------------------------------------------------------ reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -356,13 +356,18 @@ __global__ void __launch_bounds__(128)
 }
 
 // ---------------------------------------------- sampling / log-prob combine
-// Reduces the lm_head GEMM's per-tile partials of one row: log-sum-exp,
-// Gumbel-max token, and its log-prob (decode), or the target's log-prob.
-static __global__ void logits_combine(const float4* __restrict__ partials, int n_tiles, int rows,
-                               const uint64_t* keys, const float* tgt_logit,
-                               const int32_t* __restrict__ slot, const int32_t* __restrict__ tidx,
-                               int32_t* tok_buf, float* lp_buf, int buf_stride, float* lse_out,
-                               int32_t* tok_rows) {
+// Reduces the lm_head GEMM's per-block partials of one row (one warp per row):
+// log-sum-exp over the vocabulary, then either
+//   sampling: block b* = argmax_b (lse_b + Gumbel(key ^ kBlockKey, b)) (ties to
+//     the lower block), token = the block's inverse-CDF pick, log-prob =
+//     its logit - lse; or
+//   scoring: log-prob of the given target = target logit - lse.
+static __global__ void logits_combine(const float4* __restrict__ partials, int n_tiles, int vocab,
+                                      int rows, const uint64_t* keys, const float* tgt_logit,
+                                      const int32_t* __restrict__ slot,
+                                      const int32_t* __restrict__ tidx, int32_t* tok_buf,
+                                      float* lp_buf, int buf_stride, float* lse_out,
+                                      int32_t* tok_rows) {
     const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (r >= rows) return;
     const float4* pr = partials + static_cast<size_t>(r) * n_tiles;
@@ -370,36 +375,41 @@ static __global__ void logits_combine(const float4* __restrict__ partials, int n
     for (int i = lane; i < n_tiles; i += 32) mx = fmaxf(mx, pr[i].x);
     mx = warp_max(mx);
     float s = 0.f, best = -INFINITY;
-    int bi = 0x7fffffff;
+    int bb = 0x7fffffff;
+    const uint64_t bkey = keys ? keys[r] ^ kBlockKey : 0;
     for (int i = lane; i < n_tiles; i += 32) {
         const float4 v = pr[i];
         if (v.x > -INFINITY) s += v.y * __expf(v.x - mx);
-        const int idx = __float_as_int(v.w);
-        if (v.z > best || (v.z == best && idx < bi)) {
-            best = v.z;
-            bi = idx;
+        if (keys) {
+            const float sc = v.x + logf(v.y) + gumbel_noise(bkey, static_cast<uint32_t>(i));
+            if (sc > best || (sc == best && i < bb)) {
+                best = sc;
+                bb = i;
+            }
         }
     }
     s = warp_sum(s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const float b2 = __shfl_xor_sync(0xffffffffu, best, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (b2 > best || (b2 == best && i2 < bi)) {
+        const int i2 = __shfl_xor_sync(0xffffffffu, bb, o);
+        if (b2 > best || (b2 == best && i2 < bb)) {
             best = b2;
-            bi = i2;
+            bb = i2;
         }
     }
     if (lane != 0) return;
     const float lse = mx + logf(s);
     if (lse_out) lse_out[r] = lse;
     const size_t at = slot ? static_cast<size_t>(slot[r]) * buf_stride + tidx[r] : r;
-    if (keys) {  // sampled: logit = perturbed score - its noise
-        if (bi < 0 || bi >= n_tiles * 128) bi = 0;  // memory safety only (non-finite logits)
-        const float logit = best - gumbel_noise(keys[r], static_cast<uint32_t>(bi));
-        tok_buf[at] = bi;
-        lp_buf[at] = logit - lse;
-        if (tok_rows) tok_rows[r] = bi;
+    if (keys) {
+        if (bb < 0 || bb >= n_tiles) bb = 0;  // memory safety only (non-finite logits)
+        const float4 v = pr[bb];
+        int tok = __float_as_int(v.z);
+        if (tok < 0 || tok >= vocab) tok = 0;
+        tok_buf[at] = tok;
+        lp_buf[at] = v.w - lse;
+        if (tok_rows) tok_rows[r] = tok;
     } else if (lp_buf) {
         lp_buf[at] = tgt_logit[r] - lse;
     }
