@@ -13,7 +13,10 @@
 // from plan_step() (host), i.e. the reference's run_step under the lockstep
 // latency model; the GPU realises exactly that work.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -141,7 +144,7 @@ void build_model(Engine& e, Model& m, int id, cudaStream_t st) {
         init_tensor(m.head, D, seed, tid(-1, 7), id == REWARD ? 0.5f : 0.02f, st);
     }
     // KV pools
-    m.layer_stride = static_cast<int64_t>(e.n_pages) * d.n_kv_heads * e.page_size * d.head_dim;
+    m.layer_stride = static_cast<int64_t>(e.n_pages + 1) * d.n_kv_heads * e.page_size * d.head_dim;
     const size_t kvb = static_cast<size_t>(m.layer_stride) * d.n_layers * sizeof(T);
     m.k_pool = dalloc(kvb);
     m.v_pool = dalloc(kvb);
@@ -254,14 +257,13 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
     const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
     embed_rows<T><<<R, 128, 0, st>>>(static_cast<const T*>(m.embed), w.meta.tok, w.x, R, D);
     const int nrm_blocks = cdiv(R, 4);
-    int splits = 1, split_len = std::max(1, max_ctx);
+    int splits = 1, split_len = 0;  // 0: each row splits its own context (graph-stable)
     if (decode) {
         const int base = R * KV;
-        const int want = cdiv(2 * e.num_sms, base);
-        splits = std::max(1, std::min({want, cdiv(max_ctx, 128), 32}));
+        splits = std::max(1, std::min(cdiv(2 * e.num_sms, base), 16));
         while (splits > 1 && static_cast<size_t>(R) * H * splits > w.attn_ws_rows) --splits;
-        split_len = cdiv(max_ctx, splits);
     }
+    (void)max_ctx;
     for (int l = 0; l < d.n_layers; ++l) {
         const auto& L = m.layers[l];
         rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(w.x, L.ln1, static_cast<T*>(w.h), R, D, kRmsEps,
@@ -355,15 +357,18 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->page_size = cfg.page_size > 0 ? cfg.page_size : 64;
         e->max_pages = cdiv(e->Pmax + e->Lmax + 1, e->page_size);
         e->n_pages = cfg.kv_pages > 0 ? cfg.kv_pages : e->S * e->max_pages;
+        // one scratch slot (index S) and page (index n_pages) absorb padded /
+        // finished rows of bucketed decode graphs
         e->tok_stride = e->Lmax + 2;
         for (int s = e->S - 1; s >= 0; --s) e->free_slots.push_back(s);
         for (int p = e->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
         e->slots.resize(e->S);
 
-        const size_t S = e->S, TS = e->tok_stride;
+        const size_t S = e->S + 1, TS = e->tok_stride;
         e->d_page_table = static_cast<int32_t*>(dalloc(S * e->max_pages * 4));
         OPPO_CUDA_CHECK(cudaMemset(e->d_page_table, 0, S * e->max_pages * 4));
         e->d_prompt = static_cast<int32_t*>(dalloc(S * e->Pmax * 4));
+        OPPO_CUDA_CHECK(cudaMemset(e->d_prompt, 0, S * e->Pmax * 4));  // incl. the scratch slot
         e->d_tok = static_cast<int32_t*>(dalloc(S * TS * 4));
         OPPO_CUDA_CHECK(cudaMemset(e->d_tok, 0, S * TS * 4));
         e->d_old_lp = static_cast<float*>(dalloc(S * TS * 4));
@@ -372,6 +377,13 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         OPPO_CUDA_CHECK(cudaMemset(e->d_values, 0, S * TS * 4));
         OPPO_CUDA_CHECK(cudaMemset(e->d_ref_lp, 0, S * TS * 4));
         e->d_reward = static_cast<float*>(dalloc(S * 4));
+        e->d_dseq = static_cast<DecodeSeq*>(dalloc((S + 16) * sizeof(DecodeSeq)));
+        {
+            std::vector<int32_t> dummy_row(e->max_pages, e->n_pages);
+            OPPO_CUDA_CHECK(cudaMemcpy(e->d_page_table + static_cast<size_t>(e->S) * e->max_pages,
+                                       dummy_row.data(), e->max_pages * 4, cudaMemcpyHostToDevice));
+        }
+        e->d_iter = static_cast<int32_t*>(dalloc(64));
         e->d_target_len = static_cast<int32_t*>(dalloc(S * 4));
         e->d_hf_actor = dalloc(S * TS * cfg.actor.d_model * e->esz);
         e->d_hf_critic = dalloc(S * TS * cfg.critic.d_model * e->esz);
@@ -394,10 +406,10 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         e->prefill_rows = std::max(1024, std::min(8192, e->S * (e->Pmax + 64)));
         if (e->dtype == OPPO_DTYPE_F32) {
-            alloc_work<float>(*e, e->wa, std::max(e->S, 32), false);
+            alloc_work<float>(*e, e->wa, std::max(e->S + 16, 32), false);
             alloc_work<float>(*e, e->ws, e->prefill_rows, true);
         } else {
-            alloc_work<__nv_bfloat16>(*e, e->wa, std::max(e->S, 32), false);
+            alloc_work<__nv_bfloat16>(*e, e->wa, std::max(e->S + 16, 32), false);
             alloc_work<__nv_bfloat16>(*e, e->ws, e->prefill_rows, true);
         }
         e->nccl = cfg.nccl_comm;
@@ -443,6 +455,7 @@ void engine_free(Engine* e) {
     for (void* p : {static_cast<void*>(e->d_hf_actor), static_cast<void*>(e->d_hf_critic),
                     static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf})
         if (p) cudaFree(p);
+    for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     if (e->sa) cudaStreamDestroy(e->sa);
     if (e->ss) cudaStreamDestroy(e->ss);
     delete e;
@@ -506,6 +519,9 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
     if (prompts) {
         size_t tot = 0;
         for (int i = 0; i < n; ++i) tot += lens[i];
+        const int V = e.models[ACTOR].dims.vocab;
+        for (size_t i = 0; i < tot; ++i)
+            if (prompts[i] < 0 || prompts[i] >= V) input_error("prompt token outside the vocabulary");
         o_prompts = A.push(prompts, tot * 4);
     }
     // actor prompt prefill: positions 0..P-2 (the last prompt token feeds decode step 1)
@@ -730,11 +746,12 @@ void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, in
 }
 
 template <class T>
-void decode_iteration(Engine& e, const DecodeSeq* dseq, int M, int it, int max_ctx, cudaStream_t st) {
+void decode_iteration(Engine& e, int M, cudaStream_t st) {
     Work& w = e.wa;
     Model& m = e.models[ACTOR];
-    decode_rows<<<cdiv(M, 128), 128, 0, st>>>(dseq, M, it, e.d_prompt, e.Pmax, e.d_tok, e.tok_stride,
-                                              e.cfg.sample_seed, w.meta);
+    const int max_ctx = e.Pmax + e.Lmax;
+    decode_rows<<<cdiv(M, 128), 128, 0, st>>>(e.d_dseq, M, e.d_iter, e.d_prompt, e.Pmax, e.d_tok,
+                                              e.tok_stride, e.cfg.sample_seed, w.meta, e.S);
     Final<T> fin;
     fin.write_h = true;
     fin.cache = static_cast<T*>(e.d_hf_actor);
@@ -751,8 +768,39 @@ void decode_iteration(Engine& e, const DecodeSeq* dseq, int M, int it, int max_c
     gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
     logits_combine<<<cdiv(M, 4), 128, 0, st>>>(w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, M, w.meta.key,
                                                nullptr, w.meta.slot, w.meta.t, e.d_tok, e.d_old_lp,
-                                               e.tok_stride, nullptr, nullptr);
+                                               e.tok_stride, nullptr, nullptr, e.d_iter);
     e.launches += 3;
+}
+
+// One decode iteration for batch size M: replay the captured graph (capture on
+// first use).  Host cost per iteration is one cudaGraphLaunch.
+template <class T>
+void decode_iteration_graph(Engine& e, int M, cudaStream_t st) {
+    if (!e.cfg.use_graphs) {
+        decode_iteration<T>(e, M, st);
+        return;
+    }
+    auto it = e.decode_graphs.find(M);
+    if (it == e.decode_graphs.end()) {
+        const int64_t before = e.launches;
+        cudaGraph_t g;
+        OPPO_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            decode_iteration<T>(e, M, st);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            throw;
+        }
+        OPPO_CUDA_CHECK(cudaStreamEndCapture(st, &g));
+        cudaGraphExec_t ge;
+        OPPO_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+        OPPO_CUDA_CHECK(cudaGraphDestroy(g));
+        it = e.decode_graphs.emplace(M, ge).first;
+        e.decode_graph_launches[M] = e.launches - before;
+        e.launches = before;
+    }
+    OPPO_CUDA_CHECK(cudaGraphLaunch(it->second, st));
+    e.launches += e.decode_graph_launches[M];
 }
 
 template <class T>
@@ -783,11 +831,15 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     for (int i : order) {
         const int rem = active[i].target_len - active[i].generated;
         if (rem <= 0) continue;
-        dseq.push_back({slot[i], active[i].prompt_len, active[i].generated, 0, active[i].id});
+        dseq.push_back({slot[i], active[i].prompt_len, active[i].generated, active[i].target_len,
+                        active[i].id});
         rem_sorted.push_back(rem);
     }
     auto& A = g_extra[&e].step_arena;
     A.host.clear();
+    const size_t n_dec = dseq.size();
+    while (static_cast<int>(dseq.size()) < e.S + 16)  // padding rows -> scratch slot on device
+        dseq.push_back({e.S, 1, 0, -1, -1});
     const size_t o_dseq = A.push_vec(dseq);
 
     // ---------------------------------------------------------- wave plans
@@ -842,7 +894,9 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
                            std::to_string(active[i].id) + ")");
     }
     A.upload(e.sa);
-    const DecodeSeq* d_dseq = A.at<DecodeSeq>(o_dseq);
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_dseq, A.at<DecodeSeq>(o_dseq), dseq.size() * sizeof(DecodeSeq),
+                                    cudaMemcpyDeviceToDevice, e.sa));
+    set_int<<<1, 1, 0, e.sa>>>(e.d_iter, 1);
 
     // ------------------------------------------------------------- enqueue
     if (e.ev_pool.size() < waves.size() + 2) {
@@ -867,18 +921,24 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
         }
     };
     fire_waves_at(0);
-    size_t active_n = dseq.size();
+    const auto host_t0 = std::chrono::steady_clock::now();
+    size_t active_n = n_dec;
     for (int64_t it = 1; it <= t_end; ++it) {
         while (active_n > 0 && rem_sorted[active_n - 1] < it) --active_n;
         if (active_n == 0) break;
-        int max_ctx = 0;
-        for (size_t r = 0; r < active_n; ++r)
-            max_ctx = std::max(max_ctx, dseq[r].prompt_len + dseq[r].generated + static_cast<int>(it) - 1);
-        decode_iteration<T>(e, d_dseq, static_cast<int>(active_n), static_cast<int>(it), max_ctx, e.sa);
+        // bucketed batch: rows [active_n, bucket) decode into the scratch slot
+        const int bucket = e.cfg.use_graphs ? std::min(cdiv(active_n, 16) * 16, e.S + 16)
+                                            : static_cast<int>(active_n);
+        decode_iteration_graph<T>(e, bucket, e.sa);
         decode_tokens += static_cast<int64_t>(active_n);
         fire_waves_at(it);
     }
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_dec_end, e.sa));
+    const double host_enqueue_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count();
+    if (std::getenv("OPPO_DEBUG_TIMING"))
+        std::fprintf(stderr, "[oppo] decode enqueue host %.1f ms for %lld iterations, tma maps %zu\n",
+                     host_enqueue_us / 1e3, static_cast<long long>(t_end), e.tma_cache.size());
     fire_waves_at(t_end);  // (t_end == 0 or already fired: no-op)
     if (wi != waves.size()) internal_error("unfired scorer waves");
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_sc_end, e.ss));

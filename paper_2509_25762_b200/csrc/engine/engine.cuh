@@ -138,6 +138,13 @@ struct Engine {
 
     std::map<TmaKey, CUtensorMap> tma_cache;
 
+    // decode iteration as CUDA graphs, one per active batch size M (kernel
+    // arguments depend on M only; the iteration index lives in d_iter)
+    DecodeSeq* d_dseq = nullptr;   // [S] fixed, so captured graphs stay valid
+    int32_t* d_iter = nullptr;
+    std::unordered_map<int, cudaGraphExec_t> decode_graphs;
+    std::unordered_map<int, int64_t> decode_graph_launches;
+
     // PPO update buffers (grown on demand)
     size_t ppo_cap_tok = 0;
     void* ppo_buf = nullptr;

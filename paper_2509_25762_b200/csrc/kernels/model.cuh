@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(128)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPP, sub = lane % LPP;
     const int ctx = pos[r] + 1, s = slot[r];
-    const int p0 = sp * split_len, p1 = min(ctx, p0 + split_len);
+    const int slen = split_len > 0 ? split_len : (ctx + nsp - 1) / nsp;  // per-row split (graphs)
+    const int p0 = sp * slen, p1 = min(ctx, p0 + slen);
     const int H = kv.kv_heads * G;
     const float scale = rsqrtf(static_cast<float>(HD));
 
@@ -367,8 +368,9 @@ static __global__ void logits_combine(const float4* __restrict__ partials, int n
                                       const int32_t* __restrict__ slot,
                                       const int32_t* __restrict__ tidx, int32_t* tok_buf,
                                       float* lp_buf, int buf_stride, float* lse_out,
-                                      int32_t* tok_rows) {
+                                      int32_t* tok_rows, int32_t* iter_inc = nullptr) {
     const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (iter_inc && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(iter_inc, 1);  // next decode step
     if (r >= rows) return;
     const float4* pr = partials + static_cast<size_t>(r) * n_tiles;
     float mx = -INFINITY;
@@ -420,19 +422,27 @@ struct DecodeSeq {   // per decode row (sorted by remaining length, descending)
     int32_t slot;
     int32_t prompt_len;
     int32_t generated;  // g at step start
-    int32_t _pad;
+    int32_t target_len;
     int64_t id;
 };
 
 // Rows of decode iteration `it` (1-based): row r produces response token
 // j = g + it from input token j-1 (or the last prompt token) at position P+j-2.
-static __global__ void decode_rows(const DecodeSeq* __restrict__ seqs, int rows, int it,
-                            const int32_t* __restrict__ prompt_buf, int prompt_stride,
-                            const int32_t* __restrict__ tok_buf, int tok_stride, uint64_t seed,
-                            RowMeta meta) {
+static __global__ void decode_rows(const DecodeSeq* __restrict__ seqs, int rows,
+                                   const int32_t* __restrict__ iter,
+                                   const int32_t* __restrict__ prompt_buf, int prompt_stride,
+                                   const int32_t* __restrict__ tok_buf, int tok_stride,
+                                   uint64_t seed, RowMeta meta, int dummy_slot) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
-    const DecodeSeq s = seqs[r];
+    const int it = *iter;  // device-resident so one captured graph serves every iteration
+    DecodeSeq s = seqs[r];
+    if (s.generated + it > s.target_len) {  // finished (or padding) row of a bucketed batch:
+        s.slot = dummy_slot;                 // decode into the scratch slot instead
+        s.prompt_len = 1;
+        s.generated = 0;
+        s.id = -1;
+    }
     const int j = s.generated + it;
     meta.slot[r] = s.slot;
     meta.pos[r] = s.prompt_len + j - 2;
@@ -522,6 +532,8 @@ __global__ void store_pending(const int32_t* __restrict__ src_rows, const int32_
     T* dst = pending + static_cast<size_t>(slots[r]) * d;
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = s[i];
 }
+
+static __global__ void set_int(int32_t* p, int v) { *p = v; }
 
 // Synthetic prompt tokens keyed by (seed, sequence id, position).
 static __global__ void prompt_tokens(int32_t* prompt_buf, int stride, const int32_t* slots,
