@@ -14,6 +14,7 @@
 // latency model; the GPU realises exactly that work.
 #include <algorithm>
 #include <chrono>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -155,6 +156,7 @@ void build_model(Engine& e, Model& m, int id, cudaStream_t st) {
 
 void check_dims(const oppo_model_dims& d, const char* who) {
     auto bad = [&](const std::string& m) { config_error(std::string(who) + ": " + m); };
+    if (d.d_model > 32 * 4 * 28) bad("d_model above 3584 is not supported by rmsnorm_rows");
     if (d.n_layers < 1 || d.d_model < 64 || d.d_model % 64) bad("d_model must be a multiple of 64");
     if (d.n_heads < 1 || d.n_kv_heads < 1 || d.n_heads % d.n_kv_heads)
         bad("n_heads must be a multiple of n_kv_heads");
@@ -211,13 +213,13 @@ void alloc_work(Engine& e, Work& w, int rows, bool lm_rows) {
 
 // --------------------------------------------------------------- forward
 template <class T>
-void launch_attn_decode(int hd, int G, dim3 grid, cudaStream_t st, const T* q, T* out,
+void launch_attn_decode(bool pdl, int hd, int G, dim3 grid, cudaStream_t st, const T* q, T* out,
                         const KvView& kv, int layer, const int32_t* slot, const int32_t* pos,
                         int rows, int split_len, float* wo, float* wml) {
 #define OPPO_ATTN(HD_, G_)                                                                   \
     if (hd == HD_ && G == G_) {                                                              \
-        attn_decode<T, HD_, G_><<<grid, 128, 0, st>>>(q, out, kv, layer, slot, pos, rows,     \
-                                                     split_len, wo, wml);                    \
+        launch(pdl, attn_decode<T, HD_, G_>, grid, dim3(128), 0, st, q, out, kv, layer, slot,   \
+               pos, rows, split_len, wo, wml);                                               \
         return;                                                                              \
     }
     OPPO_ATTN(32, 1)
@@ -234,11 +236,32 @@ void launch_attn_decode(int hd, int G, dim3 grid, cudaStream_t st, const T* q, T
 }
 
 template <class T>
-void launch_attn_prefill(int hd, dim3 grid, cudaStream_t st, const T* q, T* out, const KvView& kv,
-                         int layer, const QBlock* blocks, int n_heads) {
-    if (hd == 32) attn_prefill<T, 32><<<grid, 128, 0, st>>>(q, out, kv, layer, blocks, n_heads);
-    else if (hd == 64) attn_prefill<T, 64><<<grid, 128, 0, st>>>(q, out, kv, layer, blocks, n_heads);
-    else attn_prefill<T, 128><<<grid, 128, 0, st>>>(q, out, kv, layer, blocks, n_heads);
+void launch_attn_prefill(bool pdl, int hd, dim3 grid, cudaStream_t st, const T* q, T* out,
+                         const KvView& kv, int layer, const QBlock* blocks, int n_heads) {
+    if (hd == 32) launch(pdl, attn_prefill<T, 32>, grid, dim3(128), 0, st, q, out, kv, layer, blocks, n_heads);
+    else if (hd == 64) launch(pdl, attn_prefill<T, 64>, grid, dim3(128), 0, st, q, out, kv, layer, blocks, n_heads);
+    else launch(pdl, attn_prefill<T, 128>, grid, dim3(128), 0, st, q, out, kv, layer, blocks, n_heads);
+}
+
+void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
+                     bool decode, int splits, const QBlock* qblocks, int n_qblocks) {
+    const auto& d = m.dims;
+    const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
+    const auto* q = static_cast<const __nv_bfloat16*>(w.q);
+    auto* o = static_cast<__nv_bfloat16*>(w.attn);
+    auto go = [&](auto kernel, dim3 grid, int threads) {
+        launch(e.pdl, kernel, grid, dim3(threads), 0, st, q, o, kv, layer, d.n_heads, w.meta.slot,
+               w.meta.pos, R, w.attn_ws_o, w.attn_ws_ml, decode ? nullptr : qblocks);
+    };
+    const dim3 grid = decode ? dim3(R, d.n_kv_heads, splits) : dim3(n_qblocks, d.n_kv_heads);
+    switch (d.head_dim) {
+    case 32: decode ? go(attn_mma<32, 1>, grid, 32) : go(attn_mma<32, 4>, grid, 128); break;
+    case 64: decode ? go(attn_mma<64, 1>, grid, 32) : go(attn_mma<64, 4>, grid, 128); break;
+    default: decode ? go(attn_mma<128, 1>, grid, 32) : go(attn_mma<128, 4>, grid, 128); break;
+    }
+    if (decode && splits > 1)
+        launch(e.pdl, attn_split_combine<__nv_bfloat16>, dim3(R, d.n_heads), dim3(64), 0, st,
+               w.attn_ws_o, w.attn_ws_ml, o, R, d.n_heads, d.head_dim, splits);
 }
 
 template <class T>
@@ -255,18 +278,19 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
     const auto& d = m.dims;
     const int D = d.d_model, H = d.n_heads, KV = d.n_kv_heads, hd = d.head_dim;
     const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
-    embed_rows<T><<<R, 128, 0, st>>>(static_cast<const T*>(m.embed), w.meta.tok, w.x, R, D);
+    launch(e.pdl, embed_rows<T>, dim3(R), dim3(128), 0, st, static_cast<const T*>(m.embed), w.meta.tok, w.x, R, D);
     const int nrm_blocks = cdiv(R, 4);
     int splits = 1, split_len = 0;  // 0: each row splits its own context (graph-stable)
     if (decode) {
         const int base = R * KV;
-        splits = std::max(1, std::min(cdiv(2 * e.num_sms, base), 16));
+        const int per_sm = std::is_same_v<T, __nv_bfloat16> ? 8 : 4;  // bf16: 1-warp CTAs
+        splits = std::max(1, std::min(cdiv(per_sm * e.num_sms, base), 16));
         while (splits > 1 && static_cast<size_t>(R) * H * splits > w.attn_ws_rows) --splits;
     }
     (void)max_ctx;
     for (int l = 0; l < d.n_layers; ++l) {
         const auto& L = m.layers[l];
-        rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(w.x, L.ln1, static_cast<T*>(w.h), R, D, kRmsEps,
+        launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, w.x, L.ln1, static_cast<T*>(w.h), R, D, kRmsEps,
                                                     nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
         EpiParams ep{};
         ep.mode = EPI_STORE;
@@ -275,18 +299,20 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         ep.bias = L.bqkv;
         ep.scale = 1.f;
         gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
-        rope_append<T><<<R, 128, 0, st>>>(static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l,
+        launch(e.pdl, rope_append<T>, dim3(R), dim3(128), 0, st, static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l,
                                           w.meta.slot, w.meta.pos, R, H, kRopeTheta);
-        if (decode) {
-            launch_attn_decode<T>(hd, H / KV, dim3(R, KV, splits), st, static_cast<const T*>(w.q),
+        if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+            attn_mma_launch(e, m, w, st, l, R, decode, splits, qblocks, n_qblocks);
+        } else if (decode) {
+            launch_attn_decode<T>(e.pdl, hd, H / KV, dim3(R, KV, splits), st, static_cast<const T*>(w.q),
                                   static_cast<T*>(w.attn), kv, l, w.meta.slot, w.meta.pos, R,
                                   split_len, w.attn_ws_o, w.attn_ws_ml);
-            if (splits > 1)
-                attn_split_combine<T><<<dim3(R, H), 64, 0, st>>>(w.attn_ws_o, w.attn_ws_ml,
+            if (splits > 1 && !std::is_same_v<T, __nv_bfloat16>)
+                launch(e.pdl, attn_split_combine<T>, dim3(dim3(R, H)), dim3(64), 0, st, w.attn_ws_o, w.attn_ws_ml,
                                                                 static_cast<T*>(w.attn), R, H, hd,
                                                                 splits);
         } else {
-            launch_attn_prefill<T>(hd, dim3(n_qblocks, H), st, static_cast<const T*>(w.q),
+            launch_attn_prefill<T>(e.pdl, hd, dim3(n_qblocks, H), st, static_cast<const T*>(w.q),
                                    static_cast<T*>(w.attn), kv, l, qblocks, H);
         }
         ep = EpiParams{};
@@ -295,7 +321,7 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         ep.ldy = D;
         ep.scale = 1.f;
         gemm_run(e, w, st, w.attn, R, m.q_width(), m.q_width(), L.wo, D, m.q_width(), ep);
-        rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(w.x, L.ln2, static_cast<T*>(w.h), R, D, kRmsEps,
+        launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, w.x, L.ln2, static_cast<T*>(w.h), R, D, kRmsEps,
                                                     nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
         ep = EpiParams{};
         ep.mode = EPI_SWIGLU;
@@ -311,7 +337,7 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         gemm_run(e, w, st, w.ff, R, d.d_ff, d.d_ff, L.wdown, D, d.d_ff, ep);
         e.launches += 6 + (splits > 1);
     }
-    rmsnorm_rows<T><<<nrm_blocks, 128, 0, st>>>(
+    launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, 
         w.x, m.final_norm, fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, fin.head,
         w.head_out, fin.cache, w.meta.slot, w.meta.t, e.tok_stride, fin.t_lo, fin.t_hi);
     e.launches += 2;
@@ -405,6 +431,9 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
                     static_cast<__nv_bfloat16*>(a.lm_head), a.lm_master, n);
         }
         e->prefill_rows = std::max(1024, std::min(8192, e->S * (e->Pmax + 64)));
+        if (e->dtype == OPPO_DTYPE_BF16)
+            for (const auto& m : e->models)
+                e->qblock = std::min(e->qblock, 64 / (m.dims.n_heads / m.dims.n_kv_heads));
         if (e->dtype == OPPO_DTYPE_F32) {
             alloc_work<float>(*e, e->wa, std::max(e->S + 16, 32), false);
             alloc_work<float>(*e, e->ws, e->prefill_rows, true);
@@ -413,6 +442,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
             alloc_work<__nv_bfloat16>(*e, e->ws, e->prefill_rows, true);
         }
         e->nccl = cfg.nccl_comm;
+        e->pdl = cfg.use_graphs != 0;
         OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
         g_extra[e];
     } catch (...) {
@@ -532,8 +562,8 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
         const int np = lens[i] - 1;
         if (np <= 0) continue;
         segs.push_back({slots[i], 0, np, rows_total, lens[i], 0});
-        for (int b = 0; b < np; b += 32)
-            qbs.push_back({rows_total + b, std::min(32, np - b), slots[i], b});
+        for (int b = 0; b < np; b += e.qblock)
+            qbs.push_back({rows_total + b, std::min(e.qblock, np - b), slots[i], b});
         rows_total += np;
     }
     const size_t o_segs = A.push_vec(segs), o_qbs = A.push_vec(qbs);
@@ -640,8 +670,8 @@ void build_passes(Engine& e, std::vector<SegReq>& reqs, WavePlan& wave, Arena& A
             const int take = std::min(r.n - off_in_seg, cap - rows);
             const int pos0 = r.pos0 + off_in_seg;
             segs.push_back({r.slot, pos0, take, rows, r.prompt_len, 0});
-            for (int b = 0; b < take; b += 32)
-                qbs.push_back({rows + b, std::min(32, take - b), r.slot, pos0 + b});
+            for (int b = 0; b < take; b += e.qblock)
+                qbs.push_back({rows + b, std::min(e.qblock, take - b), r.slot, pos0 + b});
             auto& info = e.slots[r.slot];
             const int P = r.prompt_len, L = info.target_len;
             // resolve this slot's pending reference row: its target is the token at pos0
@@ -750,7 +780,7 @@ void decode_iteration(Engine& e, int M, cudaStream_t st) {
     Work& w = e.wa;
     Model& m = e.models[ACTOR];
     const int max_ctx = e.Pmax + e.Lmax;
-    decode_rows<<<cdiv(M, 128), 128, 0, st>>>(e.d_dseq, M, e.d_iter, e.d_prompt, e.Pmax, e.d_tok,
+    launch(e.pdl, decode_rows, dim3(cdiv(M, 128)), dim3(128), 0, st, e.d_dseq, M, e.d_iter, e.d_prompt, e.Pmax, e.d_tok,
                                               e.tok_stride, e.cfg.sample_seed, w.meta, e.S);
     Final<T> fin;
     fin.write_h = true;
@@ -766,7 +796,7 @@ void decode_iteration(Engine& e, int M, cudaStream_t st) {
     ep.keys = w.meta.key;
     const int D = m.dims.d_model;
     gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
-    logits_combine<<<cdiv(M, 4), 128, 0, st>>>(w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, M, w.meta.key,
+    launch(e.pdl, logits_combine, dim3(cdiv(M, 4)), dim3(128), 0, st, w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, M, w.meta.key,
                                                nullptr, w.meta.slot, w.meta.t, e.d_tok, e.d_old_lp,
                                                e.tok_stride, nullptr, nullptr, e.d_iter);
     e.launches += 3;

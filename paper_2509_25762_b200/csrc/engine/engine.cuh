@@ -12,7 +12,9 @@
 
 #include "host/sched.hpp"
 #include "kernels/gemm.cuh"
+#include "engine/launch.cuh"
 #include "kernels/model.cuh"
+#include "kernels/attn_mma.cuh"
 #include "oppo/oppo.h"
 
 namespace oppo {
@@ -130,11 +132,13 @@ struct Engine {
 
     Work wa, ws;                        // actor decode / scorer prefill
     int prefill_rows = 8192;
+    int qblock = 32;  // queries per prefill attention block (bf16: rows = queries x G <= 64)
     cudaStream_t sa = nullptr, ss = nullptr;
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr;
     bool step_open = false;
     int64_t launches = 0;
+    bool pdl = false;  // programmatic dependent launch on the decode / prefill chains
 
     std::map<TmaKey, CUtensorMap> tma_cache;
 

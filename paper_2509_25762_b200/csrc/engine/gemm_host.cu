@@ -28,7 +28,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <int BN>
 void launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, dim3 grid, const GemmShape& sh,
-               const EpiParams& ep, cudaStream_t st) {
+               const EpiParams& ep, cudaStream_t st, bool pdl) {
     static bool attr = false;
     if (!attr) {
         OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc<BN>,
@@ -36,7 +36,7 @@ void launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, dim3 grid, const Ge
                                              tc::Cfg<BN>::SMEM));
         attr = true;
     }
-    tc::gemm_bf16_tc<BN><<<grid, 128, tc::Cfg<BN>::SMEM, st>>>(mx, mw, sh, ep);
+    launch(pdl, tc::gemm_bf16_tc<BN>, grid, dim3(128), tc::Cfg<BN>::SMEM, st, mx, mw, sh, ep);
 }
 }  // namespace
 
@@ -88,20 +88,32 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     const int m_tiles = (M + 127) / 128;
     if (dtype == OPPO_DTYPE_F32) {
         if (ldx != K || ldw != K) throw Error(OPPO_ERR_INTERNAL, "SIMT GEMM needs packed rows");
-        gemm_simt<float><<<dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock), 128, 0, st>>>(
-            static_cast<const float*>(x), static_cast<const float*>(wt), sh, ep);
+        launch(e && e->pdl, gemm_simt<float>, dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock),
+               dim3(128), 0, st, static_cast<const float*>(x), static_cast<const float*>(wt), sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
+    // Token-rich (prefill) GEMMs use 128x256 tiles.  Decode GEMMs (a few token
+    // tiles) are weight-streaming: pick the widest weight tile that still gives
+    // ~one CTA per SM, then split K (at most 4 ways, so the deterministic
+    // last-arriver fixup stays small) until the grid covers the SMs.
     int BN;
-    if (ep.mode == EPI_LOGITS || M > 256) BN = 256;
-    else BN = N >= 128 * (num_sms / 2) ? 128 : 64;
+    if (ep.mode == EPI_LOGITS || m_tiles > 4) {
+        BN = 256;
+    } else {
+        BN = 64;
+        for (int b : {256, 128})
+            if (m_tiles * ((N + b - 1) / b) >= num_sms) {
+                BN = b;
+                break;
+            }
+    }
     const int n_tiles = (N + BN - 1) / BN;
     const int kb = (K + 63) / 64;
     const int tiles = n_tiles * m_tiles;
     int splits = 1;
     if (ws && cnt && ep.mode != EPI_LOGITS && tiles * 2 <= num_sms && kb >= 4) {
-        splits = std::max(1, std::min(kb / 2, num_sms / tiles));
+        splits = std::max(1, std::min(std::min(kb / 2, (num_sms + tiles - 1) / tiles), 4));
         while (splits > 1 && (static_cast<size_t>(splits) * tiles * 128 * BN > ws_floats ||
                               tiles > cnt_n))
             --splits;
@@ -118,13 +130,13 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     const dim3 grid(m_tiles, n_tiles, splits);
     switch (BN) {
     case 64:
-        launch_tc<64>(mx, mw, grid, sh, ep, st);
+        launch_tc<64>(mx, mw, grid, sh, ep, st, e && e->pdl);
         break;
     case 128:
-        launch_tc<128>(mx, mw, grid, sh, ep, st);
+        launch_tc<128>(mx, mw, grid, sh, ep, st, e && e->pdl);
         break;
     default:
-        launch_tc<256>(mx, mw, grid, sh, ep, st);
+        launch_tc<256>(mx, mw, grid, sh, ep, st, e && e->pdl);
         break;
     }
     OPPO_CUDA_CHECK(cudaGetLastError());

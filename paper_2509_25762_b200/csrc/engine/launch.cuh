@@ -1,0 +1,27 @@
+// launch.cuh — kernel launch helper: optional programmatic dependent launch
+// (PDL) so a kernel's prologue overlaps the tail of its predecessor.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels/common.cuh"
+
+namespace oppo {
+
+template <typename... KArgs, typename... Args>
+inline void launch(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    OPPO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
+}  // namespace oppo

@@ -61,6 +61,14 @@ constexpr int kSampleBlock = 256;
 constexpr uint64_t kInBlockKey = 0x696e626c6f636bull;  // "inblock"
 constexpr uint64_t kBlockKey = 0x626c6f636b6e7a65ull;  // "blocknze"
 
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue now / wait until the previous kernel's results are visible.  Both
+// are no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------ reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -66,6 +66,8 @@ __global__ void convert(const S* s, D* d, int64_t n) {
 template <class T>
 __global__ void embed_rows(const T* __restrict__ emb, const int32_t* __restrict__ tok, float* x,
                            int rows, int d) {
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x;
     if (r >= rows) return;
     const T* src = emb + static_cast<size_t>(tok[r]) * d;
@@ -82,11 +84,24 @@ __global__ void rmsnorm_rows(const float* __restrict__ x, const float* __restric
                              int rows, int d, float eps, const float* head_w, float* head_out,
                              T* cache, const int32_t* slot, const int32_t* tidx, int cache_rows,
                              int t_lo, int t_hi) {
+    pdl_trigger();
+    pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= rows) return;
     const float* xr = x + static_cast<size_t>(warp) * d;
+    // all of the row's float4 loads are issued before the reduction (one
+    // memory round trip); d <= 32 * 4 * kMaxV4
+    constexpr int kMaxV4 = 28;
+    const int nv = d >> 2;
+    float4 v[kMaxV4];
     float ss = 0.0f;
-    for (int i = lane; i < d; i += 32) ss += xr[i] * xr[i];
+#pragma unroll
+    for (int i = 0; i < kMaxV4; ++i) {
+        const int c = lane + 32 * i;
+        v[i] = c < nv ? __ldg(reinterpret_cast<const float4*>(xr) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxV4; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
     ss = warp_sum(ss);
     const float inv = rsqrtf(ss / d + eps);
     float hd = 0.0f;
@@ -97,12 +112,27 @@ __global__ void rmsnorm_rows(const float* __restrict__ x, const float* __restric
         if (t >= t_lo && t <= t_hi)
             crow = cache + (static_cast<size_t>(slot[warp]) * cache_rows + t) * d;
     }
-    for (int i = lane; i < d; i += 32) {
-        const float v = xr[i] * inv * w[i];
-        const T vt = fromf<T>(v);
-        if (orow) orow[i] = vt;
-        if (crow) crow[i] = vt;
-        if (head_w) hd += tof(vt) * head_w[i];
+#pragma unroll
+    for (int i = 0; i < kMaxV4; ++i) {
+        const int c = lane + 32 * i;
+        if (c >= nv) break;
+        const float4 g = __ldg(reinterpret_cast<const float4*>(w) + c);
+        float y[4] = {v[i].x * inv * g.x, v[i].y * inv * g.y, v[i].z * inv * g.z, v[i].w * inv * g.w};
+        T t4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) t4[k] = fromf<T>(y[k]);
+        if (orow) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) orow[4 * c + k] = t4[k];
+        }
+        if (crow) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) crow[4 * c + k] = t4[k];
+        }
+        if (head_w) {
+            const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w) + c);
+            hd += tof(t4[0]) * hw.x + tof(t4[1]) * hw.y + tof(t4[2]) * hw.z + tof(t4[3]) * hw.w;
+        }
     }
     if (head_w) {
         hd = warp_sum(hd);
@@ -116,6 +146,8 @@ template <class T>
 __global__ void rope_append(const T* __restrict__ qkv, T* q_out, KvView kv, int layer,
                             const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
                             int rows, int n_heads, float theta) {
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x;
     if (r >= rows) return;
     const int hd = kv.head_dim, half = hd / 2;
@@ -158,6 +190,8 @@ __global__ void __launch_bounds__(128)
     attn_decode(const T* __restrict__ q, T* out, KvView kv, int layer,
                 const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int rows,
                 int split_len, float* ws_o, float* ws_ml) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int VEC = 16 / sizeof(T);
     constexpr int LPP = HD / VEC;
     static_assert(LPP >= 1 && LPP <= 32 && (32 % LPP) == 0, "head dim / vector mismatch");
@@ -189,39 +223,43 @@ __global__ void __launch_bounds__(128)
     }
     const T* kc = static_cast<const T*>(kv.k);
     const T* vc = static_cast<const T*>(kv.v);
-    for (int pb = p0 + warp * PPW; pb < p1; pb += 4 * PPW) {  // warp-uniform trip count
-        const int p = pb + grp;
-        const bool valid = p < p1;
-        float kf[VEC], vf[VEC];
-        if (valid) {
-            const size_t base = kv_index<T>(kv, layer, s, p, h) + sub * VEC;
-            const uint4 kraw = *reinterpret_cast<const uint4*>(kc + base);
-            const uint4 vraw = *reinterpret_cast<const uint4*>(vc + base);
-            const T* kk = reinterpret_cast<const T*>(&kraw);
-            const T* vv = reinterpret_cast<const T*>(&vraw);
+    // U positions per lane group per iteration: all K/V loads are issued
+    // before any math so each lane keeps 2U 16-byte loads in flight.
+    constexpr int U = 4;
+    for (int pb = p0 + warp * PPW * U; pb < p1; pb += 4 * PPW * U) {  // warp-uniform trip count
+        uint4 kr[U], vr[U];
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                kf[e] = tof(kk[e]);
-                vf[e] = tof(vv[e]);
+        for (int u = 0; u < U; ++u) {
+            const int p = pb + u * PPW + grp;
+            if (p < p1) {
+                const size_t base = kv_index<T>(kv, layer, s, p, h) + sub * VEC;
+                kr[u] = __ldg(reinterpret_cast<const uint4*>(kc + base));
+                vr[u] = __ldg(reinterpret_cast<const uint4*>(vc + base));
+            } else {
+                kr[u] = make_uint4(0, 0, 0, 0);
+                vr[u] = make_uint4(0, 0, 0, 0);
             }
-        } else {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) kf[e] = vf[e] = 0.0f;
         }
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float sc = 0.0f;
+        for (int u = 0; u < U; ++u) {
+            const bool valid = pb + u * PPW + grp < p1;
+            const T* kk = reinterpret_cast<const T*>(&kr[u]);
+            const T* vv = reinterpret_cast<const T*>(&vr[u]);
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) sc = fmaf(qv[g][e], kf[e], sc);
+            for (int g = 0; g < G; ++g) {
+                float sc = 0.0f;
 #pragma unroll
-            for (int o = LPP / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-            if (valid) {
-                const float mn = fmaxf(m[g], sc);
-                const float corr = __expf(m[g] - mn), pe = __expf(sc - mn);
-                l[g] = l[g] * corr + pe;
+                for (int e = 0; e < VEC; ++e) sc = fmaf(qv[g][e], tof(kk[e]), sc);
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) acc[g][e] = fmaf(acc[g][e], corr, pe * vf[e]);
-                m[g] = mn;
+                for (int o = LPP / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+                if (valid) {
+                    const float mn = fmaxf(m[g], sc);
+                    const float corr = __expf(m[g] - mn), pe = __expf(sc - mn);
+                    l[g] = l[g] * corr + pe;
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) acc[g][e] = fmaf(acc[g][e], corr, pe * tof(vv[e]));
+                    m[g] = mn;
+                }
             }
         }
     }
@@ -268,6 +306,8 @@ __global__ void __launch_bounds__(128)
 template <class T>
 __global__ void attn_split_combine(const float* ws_o, const float* ws_ml, T* out, int rows,
                                    int H, int hd, int nsp) {
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x, head = blockIdx.y;
     if (r >= rows) return;
     const size_t o = (static_cast<size_t>(r) * H + head) * nsp;
@@ -302,6 +342,8 @@ template <class T, int HD>
 __global__ void __launch_bounds__(128)
     attn_prefill(const T* __restrict__ q, T* out, KvView kv, int layer,
                  const QBlock* __restrict__ blocks, int n_heads) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int TILE = HD >= 128 ? 32 : 64, DPT = HD / 4;  // <= 48 KB static smem
     const QBlock b = blocks[blockIdx.x];
     const int head = blockIdx.y, G = n_heads / kv.kv_heads, h = head / G;
@@ -369,6 +411,8 @@ static __global__ void logits_combine(const float4* __restrict__ partials, int n
                                       const int32_t* __restrict__ tidx, int32_t* tok_buf,
                                       float* lp_buf, int buf_stride, float* lse_out,
                                       int32_t* tok_rows, int32_t* iter_inc = nullptr) {
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (iter_inc && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(iter_inc, 1);  // next decode step
     if (r >= rows) return;
@@ -433,6 +477,8 @@ static __global__ void decode_rows(const DecodeSeq* __restrict__ seqs, int rows,
                                    const int32_t* __restrict__ prompt_buf, int prompt_stride,
                                    const int32_t* __restrict__ tok_buf, int tok_stride,
                                    uint64_t seed, RowMeta meta, int dummy_slot) {
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     const int it = *iter;  // device-resident so one captured graph serves every iteration

@@ -237,3 +237,23 @@ def test_ppo_update_vs_oracle_fp32():
     W1 = eng.get_tensor(0, "lm_head").reshape(512, 128).astype(np.float64)
     assert np.max(np.abs((W1 - W0) - 0.5 * dW)) <= 1e-5 * max(1e-3, np.abs(0.5 * dW).max()) + 1e-7
     eng.close()
+
+
+def test_gqa_05b_width_bf16_vs_oracle():
+    """0.5B geometry (d=896, 14 q heads over 2 kv heads, head_dim 64, SwiGLU
+    4864) at 2 layers / small vocabulary: tensor-core attention (decode and
+    chunked prefill, G=7 rows per KV head) and tcgen05 GEMMs vs fp64."""
+    shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                 vocab=1024, tied=1)
+    P, C = 16, 16
+    lens = [40, 70, 23, 64]
+    eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=80,
+                 sample_seed=SAMPLE_SEED)
+    st = fresh_states(len(lens), P, lens)
+    eng.admit(st)
+    eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+    orc = oracles(eng)
+    for s in st:
+        check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.1, margin_tol=0.2,
+                      strict_tokens=False)
+    eng.close()
