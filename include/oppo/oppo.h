@@ -96,6 +96,12 @@ typedef struct oppo_ledger {
     int64_t decode_tokens; /* tokens sampled (including discarded tails)  */
     int64_t prefill_tokens;/* scorer tokens prefilled (per scorer)        */
     int64_t kernel_launches;
+    /* actor decode loop alone (first decode iteration .. last), and its
+     * algorithmic HBM bytes: actor weights (non-embedding + lm_head) once per
+     * iteration + the KV cache each active row reads and appends */
+    double decode_loop_us;
+    double decode_weight_bytes;
+    double decode_kv_bytes;
 } oppo_ledger;
 
 enum { OPPO_MODE_STREAMED = 0, OPPO_MODE_SEQUENTIAL = 1 };      /* ScheduleMode */
@@ -384,7 +390,16 @@ oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
                         const void* d_w, const void* d_bias, void* d_y, int32_t epilogue,
                         void* stream);
 
-/* Times the engine GEMM alone over `copies` distinct weight matrices; avg_us per launch. */
+/* Decode-shaped GEMM (swap-AB tcgen05, M <= 512 tokens) behind the actor's
+ * decode iteration.  mode 0: fp32 split-K partials into d_ws[splits][M][N]
+ * (*splits receives the count; the sum over splits is Y); mode 1: SwiGLU over
+ * interleaved (gate, up) weight rows into d_y[M][N/2] bf16; mode 2: store
+ * (+bias) into d_y[M][N] bf16.  K must be a multiple of 64. */
+oppo_status oppo_k_gemm_dec(int32_t M, int32_t N, int32_t K, const void* d_x, const void* d_w,
+                            const void* d_bias, void* d_y, int32_t mode, void* d_ws,
+                            int64_t ws_floats, int32_t* splits, void* stream);
+
+/* Times the engine GEMM alone (epilogue >= 16: the decode GEMM, mode epilogue-16) over `copies` distinct weight matrices; avg_us per launch. */
 oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_t copies, int32_t reps,
                               int32_t epilogue, float* avg_us);
 

@@ -109,6 +109,7 @@ def _declare(L):
                                    vp, vp, vp, vp]),
         "oppo_k_gemm": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, vp]),
         "oppo_k_gemm_bench": (i32, [i32, i32, i32, i32, i32, i32, P(C.c_float)]),
+        "oppo_k_gemm_dec": (i32, [i32, i32, i32, vp, vp, vp, vp, i32, vp, i64, P(i32), vp]),
     }
     for name, (res, args) in eng.items():
         f = getattr(L, name, None)

@@ -48,7 +48,9 @@ class Ledger(C.Structure):
                 ("work_generation", C.c_int64), ("work_scoring", C.c_int64),
                 ("step_us", C.c_double), ("decode_us", C.c_double), ("score_us", C.c_double),
                 ("decode_iters", C.c_int64), ("decode_tokens", C.c_int64),
-                ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64),
+                ("decode_loop_us", C.c_double), ("decode_weight_bytes", C.c_double),
+                ("decode_kv_bytes", C.c_double)]
 
 
 class Latency(C.Structure):

@@ -14,6 +14,11 @@
 // latency model; the GPU realises exactly that work.
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <exception>
+#include <functional>
+#include <thread>
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
@@ -86,8 +91,77 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
     }
 };
 
+// Host thread that enqueues the scorer waves on the scorer stream.  A wave is
+// hundreds of launches; enqueued from the driver thread they can fill the
+// launch queue and block it, starving the actor stream of its next decode
+// graph.  With this thread the driver only records the wave's event on the
+// actor stream and posts the wave here.  drain() ends every run_step, so the
+// engine's API stays single-threaded.
+struct ScorerWorker {
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv, cv_idle;
+    std::deque<std::function<void()>> q;
+    bool stop = false, busy = false, started = false;
+    std::exception_ptr err;
+    void start(int device) {
+        if (started) return;
+        started = true;
+        th = std::thread([this, device] {
+            cudaSetDevice(device);
+            for (;;) {
+                std::function<void()> job;
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return stop || !q.empty(); });
+                    if (q.empty()) return;  // stop requested and nothing left
+                    job = std::move(q.front());
+                    q.pop_front();
+                    busy = true;
+                }
+                try {
+                    job();
+                } catch (...) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (!err) err = std::current_exception();
+                }
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    busy = false;
+                }
+                cv_idle.notify_all();
+            }
+        });
+    }
+    void post(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            q.push_back(std::move(f));
+        }
+        cv.notify_one();
+    }
+    void drain() {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_idle.wait(lk, [&] { return q.empty() && !busy; });
+        if (err) {
+            std::exception_ptr x = err;
+            err = nullptr;
+            std::rethrow_exception(x);
+        }
+    }
+    void shutdown() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        if (th.joinable()) th.join();
+    }
+};
+
 struct EngineExtra {
     Arena step_arena, admit_arena, upd_arena;
+    ScorerWorker scorer;
 };
 std::unordered_map<const Engine*, EngineExtra> g_extra;
 
@@ -249,9 +323,16 @@ void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
     const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
     const auto* q = static_cast<const __nv_bfloat16*>(w.q);
     auto* o = static_cast<__nv_bfloat16*>(w.attn);
+    // decode split-KV: the splits of one row form a cluster and merge in DSMEM
+    const bool cluster = decode && splits > 1 && e.attn_cluster;
     auto go = [&](auto kernel, dim3 grid, int threads) {
-        launch(e.pdl, kernel, grid, dim3(threads), 0, st, q, o, kv, layer, d.n_heads, w.meta.slot,
-               w.meta.pos, R, w.attn_ws_o, w.attn_ws_ml, decode ? nullptr : qblocks);
+        if (cluster)
+            launch_cluster_z(e.pdl, splits, kernel, grid, dim3(threads), 0, st, q, o, kv, layer, d.n_heads,
+                             w.meta.slot, w.meta.pos, R, static_cast<float*>(nullptr),
+                             static_cast<float*>(nullptr), static_cast<const QBlock*>(nullptr));
+        else
+            launch(e.pdl, kernel, grid, dim3(threads), 0, st, q, o, kv, layer, d.n_heads, w.meta.slot,
+                   w.meta.pos, R, w.attn_ws_o, w.attn_ws_ml, decode ? nullptr : qblocks);
     };
     const dim3 grid = decode ? dim3(R, d.n_kv_heads, splits) : dim3(n_qblocks, d.n_kv_heads);
     switch (d.head_dim) {
@@ -259,9 +340,11 @@ void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
     case 64: decode ? go(attn_mma<64, 1>, grid, 32) : go(attn_mma<64, 4>, grid, 128); break;
     default: decode ? go(attn_mma<128, 1>, grid, 32) : go(attn_mma<128, 4>, grid, 128); break;
     }
-    if (decode && splits > 1)
+    if (decode && splits > 1 && !cluster) {
         launch(e.pdl, attn_split_combine<__nv_bfloat16>, dim3(R, d.n_heads), dim3(64), 0, st,
                w.attn_ws_o, w.attn_ws_ml, o, R, d.n_heads, d.head_dim, splits);
+        e.launches += 1;
+    }
 }
 
 template <class T>
@@ -283,15 +366,97 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
     int splits = 1, split_len = 0;  // 0: each row splits its own context (graph-stable)
     if (decode) {
         const int base = R * KV;
-        const int per_sm = std::is_same_v<T, __nv_bfloat16> ? 8 : 4;  // bf16: 1-warp CTAs
-        splits = std::max(1, std::min(cdiv(per_sm * e.num_sms, base), 16));
+        // bf16: 1-warp CTAs, split into clusters of <= 8 (DSMEM merge) until
+        // ~4 CTAs per SM; fp32 (parity path): workspace + combine kernel
+        const int per_sm = e.attn_per_sm;
+        const int max_split = e.attn_max_split > 0 ? e.attn_max_split
+                              : (!std::is_same_v<T, __nv_bfloat16> || !e.attn_cluster) ? 16
+                              : hd == 32 ? attn_merge_splits<32>()
+                              : hd == 64 ? attn_merge_splits<64>() : attn_merge_splits<128>();
+        splits = std::max(1, std::min(cdiv(per_sm * e.num_sms, base), max_split));
         while (splits > 1 && static_cast<size_t>(R) * H * splits > w.attn_ws_rows) --splits;
     }
     (void)max_ctx;
+    // decode (bf16, <= 512 rows): swap-AB gemm_dec with split-K partials folded
+    // by the consumer kernels (RoPE/KV append, RMSNorm residual add)
+    const bool dec_gemm = std::is_same_v<T, __nv_bfloat16> && decode && R <= 512 && D <= 4096 &&
+                          D % 64 == 0 && m.q_width() % 64 == 0 && d.d_ff % 64 == 0;
+    if (dec_gemm) {
+        const size_t rope_smem = static_cast<size_t>(m.qkv_width()) * sizeof(T);
+        const float* part = w.gemm_ws;
+        int np = 0;  // partial splits pending for the next RMSNorm (0: none)
+        // Per-GEMM choice between the swap-AB decode GEMM (weight-streaming:
+        // wins while the token count is small or K is long) and the
+        // token-tiled GEMM (wins once ~128+ tokens re-read the weights);
+        // crossovers measured on B200 (tools/gemm_bench.py, profiles/).
+        auto residual = [&](const void* xin, int K, const void* wt) -> int {
+            if (K >= 2048 || R <= e.dec_res_max)
+                return gemm_dec_run(e, w, st, xin, R, K, K, wt, D, K, DEC_PARTIAL, nullptr, 0, nullptr);
+            EpiParams ep{};
+            ep.mode = EPI_ADD_F32;
+            ep.y = w.x;
+            ep.ldy = D;
+            ep.scale = 1.f;
+            gemm_run(e, w, st, xin, R, K, K, wt, D, K, ep);
+            return 0;
+        };
+        // OPPO_DEBUG_SKIP (perf diagnosis only; results are garbage): bit 1
+        // attention, 2 RoPE/KV append, 4 norms, 8 projection GEMMs
+        const int skip = e.debug_skip;
+        for (int l = 0; l < d.n_layers; ++l) {
+            const auto& L = m.layers[l];
+            if (!(skip & 4)) launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, L.ln1,
+                   static_cast<T*>(w.h), R, D, kRmsEps, part, np, static_cast<size_t>(R) * D, nullptr,
+                   nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
+            int sq = 0;
+            if (skip & 8) {
+            } else if (R <= e.dec_qkv_max) {
+                sq = gemm_dec_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, DEC_PARTIAL, nullptr,
+                                  0, nullptr);
+            } else {
+                EpiParams ep{};
+                ep.mode = EPI_STORE;
+                ep.y = w.qkv;
+                ep.ldy = m.qkv_width();
+                ep.bias = L.bqkv;
+                ep.scale = 1.f;
+                gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
+            }
+            if (!(skip & 2)) launch(e.pdl, rope_append<T>, dim3(R), dim3(128), sq ? rope_smem : 0, st,
+                   static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l, w.meta.slot, w.meta.pos, R,
+                   H, kRopeTheta, sq ? part : nullptr, sq, static_cast<size_t>(R) * m.qkv_width(), L.bqkv);
+            if (!(skip & 1)) attn_mma_launch(e, m, w, st, l, R, decode, splits, qblocks, n_qblocks);
+            np = (skip & 8) ? 0 : residual(w.attn, m.q_width(), L.wo);
+            if (!(skip & 4)) launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, L.ln2,
+                   static_cast<T*>(w.h), R, D, kRmsEps, part, np, static_cast<size_t>(R) * D, nullptr,
+                   nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
+            if (skip & 8) {
+            } else if (R <= e.dec_gu_max) {
+                gemm_dec_run(e, w, st, w.h, R, D, D, L.wgu, 2 * d.d_ff, D, DEC_SWIGLU, w.ff, d.d_ff, nullptr);
+            } else {
+                EpiParams ep{};
+                ep.mode = EPI_SWIGLU;
+                ep.y = w.ff;
+                ep.ldy = d.d_ff;
+                ep.scale = 1.f;
+                gemm_run(e, w, st, w.h, R, D, D, L.wgu, 2 * d.d_ff, D, ep);
+            }
+            np = (skip & 8) ? 0 : residual(w.ff, d.d_ff, L.wdown);
+            e.launches += 4;
+        }
+        launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, m.final_norm,
+               fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, part, np,
+               static_cast<size_t>(R) * D, fin.head, w.head_out, fin.cache, w.meta.slot, w.meta.t,
+               e.tok_stride, fin.t_lo, fin.t_hi);
+        e.launches += 2;
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     for (int l = 0; l < d.n_layers; ++l) {
         const auto& L = m.layers[l];
         launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, w.x, L.ln1, static_cast<T*>(w.h), R, D, kRmsEps,
-                                                    nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
+                                                    nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1,
+                                                    nullptr, 0, size_t(0));
         EpiParams ep{};
         ep.mode = EPI_STORE;
         ep.y = w.qkv;
@@ -300,7 +465,8 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         ep.scale = 1.f;
         gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
         launch(e.pdl, rope_append<T>, dim3(R), dim3(128), 0, st, static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l,
-                                          w.meta.slot, w.meta.pos, R, H, kRopeTheta);
+                                          w.meta.slot, w.meta.pos, R, H, kRopeTheta, nullptr, 0, size_t(0),
+                                          nullptr);
         if constexpr (std::is_same_v<T, __nv_bfloat16>) {
             attn_mma_launch(e, m, w, st, l, R, decode, splits, qblocks, n_qblocks);
         } else if (decode) {
@@ -322,7 +488,8 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         ep.scale = 1.f;
         gemm_run(e, w, st, w.attn, R, m.q_width(), m.q_width(), L.wo, D, m.q_width(), ep);
         launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, w.x, L.ln2, static_cast<T*>(w.h), R, D, kRmsEps,
-                                                    nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1);
+                                                    nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1,
+                                                    nullptr, 0, size_t(0));
         ep = EpiParams{};
         ep.mode = EPI_SWIGLU;
         ep.y = w.ff;
@@ -335,11 +502,12 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         ep.ldy = D;
         ep.scale = 1.f;
         gemm_run(e, w, st, w.ff, R, d.d_ff, d.d_ff, L.wdown, D, d.d_ff, ep);
-        e.launches += 6 + (splits > 1);
+        e.launches += 6 + (splits > 1 && !std::is_same_v<T, __nv_bfloat16>);
     }
     launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, 
         w.x, m.final_norm, fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, fin.head,
-        w.head_out, fin.cache, w.meta.slot, w.meta.t, e.tok_stride, fin.t_lo, fin.t_hi);
+        w.head_out, fin.cache, w.meta.slot, w.meta.t, e.tok_stride, fin.t_lo, fin.t_hi,
+        nullptr, 0, size_t(0));
     e.launches += 2;
     OPPO_CUDA_CHECK(cudaGetLastError());
 }
@@ -374,7 +542,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         OPPO_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
         OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
-        for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done})
+        for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
 
         e->S = cfg.max_slots;
@@ -441,8 +609,19 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
             alloc_work<__nv_bfloat16>(*e, e->wa, std::max(e->S + 16, 32), false);
             alloc_work<__nv_bfloat16>(*e, e->ws, e->prefill_rows, true);
         }
+        auto env_int = [](const char* k, int dflt) {
+            const char* v = std::getenv(k);
+            return v ? std::atoi(v) : dflt;
+        };
+        e->attn_cluster = env_int("OPPO_ATTN_CLUSTER", 1) != 0;
+        e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
+        e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
+        e->debug_skip = env_int("OPPO_DEBUG_SKIP", 0);
+        e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
+        e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
+        e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 128);
         e->nccl = cfg.nccl_comm;
-        e->pdl = cfg.use_graphs != 0;
+        e->pdl = cfg.use_graphs != 0 && env_int("OPPO_PDL", 1) != 0;
         OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
         g_extra[e];
     } catch (...) {
@@ -457,6 +636,7 @@ void engine_free(Engine* e) {
     cudaDeviceSynchronize();
     auto it = g_extra.find(e);
     if (it != g_extra.end()) {
+        it->second.scorer.shutdown();
         it->second.step_arena.release();
         it->second.admit_arena.release();
         it->second.upd_arena.release();
@@ -940,30 +1120,65 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_pool[0], e.sa));
     OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, e.ev_pool[0], 0));
     size_t wi = 0;
-    int64_t prefill_tokens = 0, decode_tokens = 0;
+    int64_t decode_tokens = 0;
+    std::atomic<int64_t> prefill_tokens{0};
+    ScorerWorker& worker = g_extra[&e].scorer;
+    worker.start(e.cfg.device);
+    struct DrainOnUnwind {  // posted jobs reference this frame: never leave it with jobs queued
+        ScorerWorker& w;
+        ~DrainOnUnwind() {
+            try {
+                w.drain();
+            } catch (...) {
+            }
+        }
+    } drain_guard{worker};
     auto fire_waves_at = [&](int64_t it) {
         while (wi < waves.size() && waves[wi].at_iter == it) {
             cudaEvent_t ev = e.ev_pool[wi + 1];
-            OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));
-            OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, ev, 0));
-            for (const auto& p : waves[wi].passes) run_scorer_pass<T>(e, p, A, e.ss, prefill_tokens);
+            OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));  // actor-stream order: after iteration `it`
+            const WavePlan* wave = &waves[wi];
+            worker.post([&e, &A, &prefill_tokens, ev, wave] {
+                OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, ev, 0));
+                int64_t tok = 0;
+                for (const auto& p : wave->passes) run_scorer_pass<T>(e, p, A, e.ss, tok);
+                prefill_tokens += tok;
+            });
             ++wi;
         }
     };
     fire_waves_at(0);
     const auto host_t0 = std::chrono::steady_clock::now();
     size_t active_n = n_dec;
+    // algorithmic bytes of the decode loop: weights once per
+    // iteration + per active row the KV it reads (ctx positions) and appends
+    const auto& ad = e.models[ACTOR].dims;
+    const double w_bytes = static_cast<double>(e.esz) *
+        (static_cast<double>(ad.n_layers) *
+             ((static_cast<double>(ad.n_heads + 2 * ad.n_kv_heads) * ad.head_dim + ad.n_heads * ad.head_dim) *
+                  ad.d_model +
+              3.0 * ad.d_model * ad.d_ff) +
+         static_cast<double>(ad.vocab) * ad.d_model);
+    const double kvb = 2.0 * ad.n_layers * ad.n_kv_heads * ad.head_dim * e.esz;  // K+V per token
+    double loop_w = 0, loop_kv = 0;
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_loop0, e.sa));
     for (int64_t it = 1; it <= t_end; ++it) {
         while (active_n > 0 && rem_sorted[active_n - 1] < it) --active_n;
         if (active_n == 0) break;
+        loop_w += w_bytes;
+        for (size_t r = 0; r < active_n; ++r) {
+            const DecodeSeq& q = dseq[r];
+            loop_kv += kvb * static_cast<double>(q.prompt_len + q.generated + it);  // ctx + appended row
+        }
         // bucketed batch: rows [active_n, bucket) decode into the scratch slot
         const int bucket = e.cfg.use_graphs ? std::min(cdiv(active_n, 16) * 16, e.S + 16)
                                             : static_cast<int>(active_n);
         decode_iteration_graph<T>(e, bucket, e.sa);
         decode_tokens += static_cast<int64_t>(active_n);
+        if (it == t_end) OPPO_CUDA_CHECK(cudaEventRecord(e.ev_dec_end, e.sa));
         fire_waves_at(it);
     }
-    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_dec_end, e.sa));
+    if (active_n == 0 || t_end == 0) OPPO_CUDA_CHECK(cudaEventRecord(e.ev_dec_end, e.sa));
     const double host_enqueue_us =
         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count();
     if (std::getenv("OPPO_DEBUG_TIMING"))
@@ -971,6 +1186,7 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
                      host_enqueue_us / 1e3, static_cast<long long>(t_end), e.tma_cache.size());
     fire_waves_at(t_end);  // (t_end == 0 or already fired: no-op)
     if (wi != waves.size()) internal_error("unfired scorer waves");
+    worker.drain();  // every scorer launch is enqueued on ss (rethrows a worker error)
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_sc_end, e.ss));
     OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.sa, e.ev_sc_end, 0));
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_done, e.sa));
@@ -987,6 +1203,10 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     ledger.decode_us = ms * 1e3;
     OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_begin, e.ev_sc_end));
     ledger.score_us = ms * 1e3;
+    OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_loop0, e.ev_dec_end));
+    ledger.decode_loop_us = ms * 1e3;
+    ledger.decode_weight_bytes = loop_w;
+    ledger.decode_kv_bytes = loop_kv;
     ledger.decode_iters = t_end;
     ledger.decode_tokens = decode_tokens;
     ledger.prefill_tokens = prefill_tokens;
@@ -1537,6 +1757,30 @@ oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
     }
 }
 
+// Decode GEMM (gemm_dec.cuh) alone: mode 0 partials (d_ws [splits][M][N] fp32,
+// *splits receives the split count), 1 SwiGLU (d_y [M][N/2] bf16), 2 store
+// (+bias, d_y [M][N] bf16).
+oppo_status oppo_k_gemm_dec(int32_t M, int32_t N, int32_t K, const void* d_x, const void* d_w,
+                            const void* d_bias, void* d_y, int32_t mode, void* d_ws,
+                            int64_t ws_floats, int32_t* splits, void* stream) {
+    try {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int ldy = mode == oppo::DEC_SWIGLU ? N / 2 : N;
+        const int sp = oppo::gemm_dec_impl(nullptr, static_cast<cudaStream_t>(stream), d_x, M, K, K, d_w, N,
+                                           K, mode, d_y, ldy, static_cast<const float*>(d_bias),
+                                           static_cast<float*>(d_ws), static_cast<size_t>(ws_floats), sms,
+                                           false);
+        if (splits) *splits = sp;
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
+
 }  // extern "C"
 
 // Times the engine GEMM alone: `copies` distinct weight matrices (a layer
@@ -1565,8 +1809,17 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
             OPPO_CUDA_CHECK(cudaMalloc(&tl, static_cast<size_t>(M) * 4));
             OPPO_CUDA_CHECK(cudaMemset(keys, 0x5a, static_cast<size_t>(M) * 8));
         }
+        float* ws = nullptr;
+        const size_t ws_floats = static_cast<size_t>(16) << 20;
+        if (epilogue >= 16) OPPO_CUDA_CHECK(cudaMalloc(&ws, ws_floats * 4));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         auto launch = [&](int i) {
-            if (epilogue == oppo::EPI_LOGITS) {
+            if (epilogue >= 16) {  // decode GEMM, PDL-chained as inside the decode graph
+                const int mode = epilogue - 16;
+                oppo::gemm_dec_impl(nullptr, st, x, M, K, K, w + (i % copies) * wn, N, K, mode, y,
+                                    mode == oppo::DEC_SWIGLU ? N / 2 : N, nullptr, ws, ws_floats, sms, true);
+            } else if (epilogue == oppo::EPI_LOGITS) {
                 oppo::EpiParams ep{};
                 ep.mode = oppo::EPI_LOGITS;
                 ep.partials = parts;
@@ -1597,6 +1850,7 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
         if (parts) cudaFree(parts);
         if (keys) cudaFree(keys);
         if (tl) cudaFree(tl);
+        if (ws) cudaFree(ws);
         cudaStreamDestroy(st);
         return OPPO_OK;
     } catch (const oppo::Error& x) {

@@ -4,7 +4,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <unordered_map>
@@ -12,6 +14,7 @@
 
 #include "host/sched.hpp"
 #include "kernels/gemm.cuh"
+#include "kernels/gemm_dec.cuh"
 #include "engine/launch.cuh"
 #include "kernels/model.cuh"
 #include "kernels/attn_mma.cuh"
@@ -135,12 +138,22 @@ struct Engine {
     int qblock = 32;  // queries per prefill attention block (bf16: rows = queries x G <= 64)
     cudaStream_t sa = nullptr, ss = nullptr;
     std::vector<cudaEvent_t> ev_pool;
-    cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr,
+                ev_loop0 = nullptr;
     bool step_open = false;
-    int64_t launches = 0;
+    std::atomic<int64_t> launches{0};  // driver thread and the scorer enqueue thread
     bool pdl = false;  // programmatic dependent launch on the decode / prefill chains
+    // decode-path tuning (defaults measured on B200; OPPO_* env overrides for sweeps)
+    bool attn_cluster = true;  // split-KV merge in DSMEM (else workspace + combine kernel)
+    int attn_per_sm = 4;       // target decode attention CTAs per SM
+    int attn_max_split = 0;
+    int debug_skip = 0;        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
+    int dec_qkv_max = 96;      // largest batch for which qkv uses the swap-AB decode GEMM
+    int dec_gu_max = 64;       // ... gate|up
+    int dec_res_max = 128;     // ... O and down (down always: K >= 2048)
 
     std::map<TmaKey, CUtensorMap> tma_cache;
+    std::mutex tma_mu;  // guards tma_cache (decode and scorer launches come from two threads)
 
     // decode iteration as CUDA graphs, one per active batch size M (kernel
     // arguments depend on M only; the iteration index lives in d_iter)
@@ -169,6 +182,11 @@ void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, 
               const void* wt, int N, int ldw, const EpiParams& ep);
 void gemm_standalone(int dtype, int M, int N, int K, const void* x, const void* w,
                      const float* bias, void* y, int epi, cudaStream_t st);
+int gemm_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
+                 const void* wt, int N, int ldw, int mode, void* y, int ldy, const float* bias);
+int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int ldx, const void* wt,
+                  int N, int ldw, int mode, void* y, int ldy, const float* bias, float* ws,
+                  size_t ws_floats, int num_sms, bool pdl);
 CUtensorMap make_tma_2d(const void* ptr, int rows, int cols, int ld, int box_rows);
 int gemm_logit_tiles(int dtype, int N);  // partial tiles per row of an EPI_LOGITS GEMM
 void gemm_with_params(int dtype, int M, int N, int K, const void* x, const void* w,

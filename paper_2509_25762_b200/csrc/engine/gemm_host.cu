@@ -7,6 +7,7 @@
 
 #include "engine.cuh"
 #include "kernels/gemm.cuh"
+#include "kernels/gemm_dec.cuh"
 
 namespace oppo {
 
@@ -29,13 +30,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <int BN>
 void launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, dim3 grid, const GemmShape& sh,
                const EpiParams& ep, cudaStream_t st, bool pdl) {
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr;
+    std::call_once(attr, [] {
         OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc<BN>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              tc::Cfg<BN>::SMEM));
-        attr = true;
-    }
+    });
     launch(pdl, tc::gemm_bf16_tc<BN>, grid, dim3(128), tc::Cfg<BN>::SMEM, st, mx, mw, sh, ep);
 }
 }  // namespace
@@ -64,6 +64,7 @@ static const CUtensorMap& cached_map(Engine* e, const void* ptr, int rows, int c
         return scratch;
     }
     const TmaKey k{ptr, rows, cols, box_rows, ld};
+    std::lock_guard<std::mutex> lk(e->tma_mu);  // std::map nodes stay put: the reference outlives the lock
     auto it = e->tma_cache.find(k);
     if (it == e->tma_cache.end())
         it = e->tma_cache.emplace(k, make_tma_2d(ptr, rows, cols, ld, box_rows)).first;
@@ -141,6 +142,74 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     }
     OPPO_CUDA_CHECK(cudaGetLastError());
     (void)wk;
+}
+
+// Decode-shaped GEMM (swap-AB, gemm_dec.cuh).  Chooses the token grouping,
+// the K split and the pipeline depth; returns the number of K splits whose
+// fp32 partials the consumer must fold (DEC_PARTIAL), 1 otherwise.
+// Split choice: minimise (waves x per-CTA stage bytes / per-SM TMA ingest)
+// + (partials written and re-read through L2), subject to the workspace.
+int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int ldx, const void* wt,
+                  int N, int ldw, int mode, void* y, int ldy, const float* bias, float* ws,
+                  size_t ws_floats, int num_sms, bool pdl) {
+    if (M <= 0 || N <= 0) return 1;
+    const int Mp = (M + 15) / 16 * 16;
+    if (Mp > 512 || K % 64 != 0) throw Error(OPPO_ERR_INTERNAL, "gemm_dec shape out of range");
+    DecShape s{};
+    s.M = M;
+    s.N = N;
+    s.K = K;
+    s.nbox = Mp > 256 ? 2 : 1;
+    s.box_rows = ((Mp + s.nbox - 1) / s.nbox + 15) / 16 * 16;
+    const int stage = dec::kWBytes + s.nbox * s.box_rows * 128;
+    const int kb_total = K / 64;
+    const int tiles = (N + 127) / 128;
+    int splits = 1;
+    if (mode == DEC_PARTIAL) {
+        double best = 1e30;
+        for (int sp = 1; sp <= std::min(kb_total, 64); ++sp) {
+            const int kbps = (kb_total + sp - 1) / sp;
+            const int se = (kb_total + kbps - 1) / kbps;
+            if (static_cast<size_t>(se) * M * N > ws_floats) break;
+            const int waves = (tiles * se + num_sms - 1) / num_sms;
+            const double t = waves * (kbps * static_cast<double>(stage) / 60.0) +
+                             se * static_cast<double>(M) * N * 8.0 / 8000.0;
+            if (t < best - 1e-9) {
+                best = t;
+                splits = se;
+            }
+        }
+    }
+    s.kb_per_split = (kb_total + splits - 1) / splits;
+    splits = (kb_total + s.kb_per_split - 1) / s.kb_per_split;
+    s.stages = std::max(1, std::min(s.kb_per_split, std::min(8, (200 * 1024) / stage)));
+    int cols = 32;
+    while (cols < (s.nbox == 2 ? 512 : s.box_rows)) cols *= 2;
+    s.tmem_cols = cols;
+    s.mode = mode;
+    s.y = y;
+    s.ldy = ldy;
+    s.bias = bias;
+    s.ws = ws;
+    const int smem = s.stages * stage + 1024 + 256;
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(dec::gemm_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024));
+    });
+    CUtensorMap s1, s2;
+    const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 128, s1);
+    const CUtensorMap& mx = cached_map(e, x, M, K, ldx, s.box_rows, s2);
+    launch(pdl, dec::gemm_dec, dim3(tiles, splits), dim3(128), smem, st, mw, mx, s);
+    OPPO_CUDA_CHECK(cudaGetLastError());
+    return mode == DEC_PARTIAL ? splits : 1;
+}
+
+int gemm_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
+                 const void* wt, int N, int ldw, int mode, void* y, int ldy, const float* bias) {
+    e.launches += 1;
+    return gemm_dec_impl(&e, st, x, M, K, ldx, wt, N, ldw, mode, y, ldy, bias, w.gemm_ws,
+                         w.gemm_ws_floats, e.num_sms, e.pdl);
 }
 
 void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,

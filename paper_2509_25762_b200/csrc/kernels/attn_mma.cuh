@@ -9,11 +9,16 @@
 // zero-filled past the context); S = Q K^T takes K fragments via ldmatrix,
 // P V takes V fragments via ldmatrix.trans; the running softmax is the usual
 // flash-attention recurrence on the accumulator fragments.
-//   decode : WARPS = 1, one query row per CTA, grid.z = split-KV chunks
-//            (partials merged by attn_split_combine);
+//   decode : WARPS = 1, one query row per CTA, grid.z = split-KV chunks; the
+//            split CTAs of a row form one thread-block cluster and rank 0
+//            merges the partials through distributed shared memory (no
+//            workspace round trip, no combine kernel; ws_o == nullptr);
+//            with ws_o set, partials go to the workspace instead and
+//            attn_split_combine merges them.
 //   prefill: WARPS = 4, a query block of one slot (QBlock), causal mask.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -61,6 +66,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 }  // namespace am
 
+// largest split-KV cluster whose partials fit the K/V buffers of rank 0
+template <int HD>
+constexpr int attn_merge_splits() {
+    constexpr int TP = HD >= 128 ? 32 : 64, LDS = HD + 8;
+    constexpr int n = (2 * 2 * TP * LDS * 2) / ((16 * HD + 32) * 4);
+    return n > 8 ? 8 : n;
+}
+
 template <int HD, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS)
     attn_mma(const __nv_bfloat16* __restrict__ q, __nv_bfloat16* out, KvView kv, int layer,
@@ -71,8 +84,11 @@ __global__ void __launch_bounds__(32 * WARPS)
     constexpr int LDS = HD + 8;  // padded smem row (elements): conflict-free ldmatrix
     constexpr int NT = TP / 8;   // score n-tiles per KV tile
     constexpr int DT = HD / 8;   // output n-tiles
-    __shared__ __align__(128) __nv_bfloat16 sK[2][TP][LDS];
-    __shared__ __align__(128) __nv_bfloat16 sV[2][TP][LDS];
+    // K/V double buffers; after the loop the same bytes hold the split-KV
+    // merge buffer of the cluster's rank 0 (kMergeSplits partials)
+    __shared__ __align__(128) uint8_t smraw[2 * 2 * TP * LDS * 2];
+    auto sK = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(smraw);
+    auto sV = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(smraw + 2 * TP * LDS * 2);
     pdl_trigger();
     pdl_wait();
 
@@ -242,6 +258,45 @@ __global__ void __launch_bounds__(32 * WARPS)
             if (ok1)
                 *reinterpret_cast<uint32_t*>(out + ((qrow0 + qi1) * n_heads + h * G + g1) * HD + c) =
                     pack_bf16(o[d][2] * i1, o[d][3] * i1);
+        }
+    } else if (!ws_o) {  // split-KV merge inside the cluster (DSMEM)
+        // every rank pushes its unnormalised O rows and (max, sum) into rank
+        // 0's shared memory with remote stores (no remote-load latency on the
+        // merge), then rank 0 merges from local shared memory.
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        const int nsp = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+        constexpr int SLOT = 16 * HD + 32;  // floats per split: O[16][HD], (m, l)[16]
+        cl.sync();                          // rank 0 is done with its K/V buffers
+        float* dst = cl.map_shared_rank(reinterpret_cast<float*>(smraw), 0) + rank * SLOT;
+#pragma unroll
+        for (int d = 0; d < DT; ++d) {
+            const int c = d * 8 + tig * 2;
+            *reinterpret_cast<float2*>(dst + row0 * HD + c) = make_float2(o[d][0], o[d][1]);
+            *reinterpret_cast<float2*>(dst + row1 * HD + c) = make_float2(o[d][2], o[d][3]);
+        }
+        if (tig == 0) {
+            *reinterpret_cast<float2*>(dst + 16 * HD + row0 * 2) = make_float2(m0, l0);
+            *reinterpret_cast<float2*>(dst + 16 * HD + row1 * 2) = make_float2(m1, l1);
+        }
+        cl.sync();  // release/acquire: the pushes are visible to rank 0
+        if (rank == 0) {
+            const float* buf = reinterpret_cast<const float*>(smraw);
+            const int valid_rows = min(16, nq * G);
+            for (int e = lane; e < valid_rows * HD; e += 32) {
+                const int r = e / HD, c = e % HD;
+                float mx = -INFINITY;
+                for (int sp = 0; sp < nsp; ++sp) mx = fmaxf(mx, buf[sp * SLOT + 16 * HD + r * 2]);
+                float L = 0.f, O = 0.f;
+                for (int sp = 0; sp < nsp; ++sp) {
+                    const float ms = buf[sp * SLOT + 16 * HD + r * 2];
+                    const float wgt = ms == -INFINITY ? 0.f : exp2f(ms - mx);
+                    L += buf[sp * SLOT + 16 * HD + r * 2 + 1] * wgt;
+                    O += buf[sp * SLOT + e] * wgt;
+                }
+                const int qi = r / G, g = r % G;
+                out[((qrow0 + qi) * n_heads + h * G + g) * HD + c] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+            }
         }
     } else {  // split-KV partial: unnormalised accumulator, running max (natural log domain), sum
         const int nsp = gridDim.z, sp = blockIdx.z;

@@ -79,16 +79,20 @@ __global__ void embed_rows(const T* __restrict__ emb, const int32_t* __restrict_
 // out[r] = x[r] * rsqrt(mean(x^2) + eps) * w; one warp per row.  Optionally
 // also: head[r] = dot(out[r], hw) (value / reward head), and a copy of out[r]
 // into a per-slot hidden cache at [slot][t] (for the PPO head update).
+// With part != nullptr the row is first completed by the split-K partial sums
+// of the preceding decode GEMM (gemm_dec DEC_PARTIAL): x[r] += sum_s part[s][r]
+// in split order (deterministic), and the updated residual is written back.
 template <class T>
-__global__ void rmsnorm_rows(const float* __restrict__ x, const float* __restrict__ w, T* out,
+__global__ void rmsnorm_rows(float* __restrict__ x, const float* __restrict__ w, T* out,
                              int rows, int d, float eps, const float* head_w, float* head_out,
                              T* cache, const int32_t* slot, const int32_t* tidx, int cache_rows,
-                             int t_lo, int t_hi) {
+                             int t_lo, int t_hi, const float* __restrict__ part, int n_part,
+                             size_t part_stride) {
     pdl_trigger();
     pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= rows) return;
-    const float* xr = x + static_cast<size_t>(warp) * d;
+    float* xr = x + static_cast<size_t>(warp) * d;
     // all of the row's float4 loads are issued before the reduction (one
     // memory round trip); d <= 32 * 4 * kMaxV4
     constexpr int kMaxV4 = 28;
@@ -98,7 +102,29 @@ __global__ void rmsnorm_rows(const float* __restrict__ x, const float* __restric
 #pragma unroll
     for (int i = 0; i < kMaxV4; ++i) {
         const int c = lane + 32 * i;
-        v[i] = c < nv ? __ldg(reinterpret_cast<const float4*>(xr) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[i] = c < nv ? reinterpret_cast<const float4*>(xr)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (part) {
+        for (int sp = 0; sp < n_part; ++sp) {
+            const float4* pr = reinterpret_cast<const float4*>(part + sp * part_stride +
+                                                               static_cast<size_t>(warp) * d);
+#pragma unroll
+            for (int i = 0; i < kMaxV4; ++i) {
+                const int c = lane + 32 * i;
+                if (c < nv) {
+                    const float4 a = pr[c];
+                    v[i].x += a.x;
+                    v[i].y += a.y;
+                    v[i].z += a.z;
+                    v[i].w += a.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxV4; ++i) {
+            const int c = lane + 32 * i;
+            if (c < nv) reinterpret_cast<float4*>(xr)[c] = v[i];
+        }
     }
 #pragma unroll
     for (int i = 0; i < kMaxV4; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
@@ -140,12 +166,117 @@ __global__ void rmsnorm_rows(const float* __restrict__ x, const float* __restric
     }
 }
 
+// Decode-path RMSNorm that first completes the residual row with the
+// split-K partials of the preceding decode GEMM: x[r] += sum_s part[s][r]
+// (split order, deterministic) and writes x back; then the same outputs as
+// rmsnorm_rows (normed row, optional head dot and hidden-cache copy).  One
+// 256-thread CTA per row, one float4 column per thread per pass, the split
+// loads of a column issued together; gamma is fetched before the PDL wait.
+template <class T>
+__global__ void __launch_bounds__(256)
+    residual_rmsnorm(float* __restrict__ x, const float* __restrict__ w, T* out, int rows, int d,
+                     float eps, const float* __restrict__ part, int n_part, size_t part_stride,
+                     const float* head_w, float* head_out, T* cache, const int32_t* slot,
+                     const int32_t* tidx, int cache_rows, int t_lo, int t_hi) {
+    constexpr int kCols = 4;  // float4 columns per thread: d <= 256 * 4 * 4
+    const int r = blockIdx.x, tid = threadIdx.x, nv = d >> 2;
+    float4 g[kCols], hw[kCols];
+#pragma unroll
+    for (int i = 0; i < kCols; ++i) {
+        const int c = tid + 256 * i;
+        g[i] = c < nv ? __ldg(reinterpret_cast<const float4*>(w) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        hw[i] = (head_w && c < nv) ? __ldg(reinterpret_cast<const float4*>(head_w) + c)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    pdl_trigger();
+    pdl_wait();
+    if (r >= rows) return;
+    float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(r) * d);
+    float4 v[kCols];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < kCols; ++i) {
+        const int c = tid + 256 * i;
+        if (c >= nv) continue;
+        float4 a = xr[c];
+        const float4* pc = reinterpret_cast<const float4*>(part) + static_cast<size_t>(r) * nv + c;
+        const size_t ps = part_stride >> 2;
+        int sp = 0;
+        for (; sp + 4 <= n_part; sp += 4) {
+            const float4 p0 = pc[sp * ps], p1 = pc[(sp + 1) * ps], p2 = pc[(sp + 2) * ps],
+                         p3 = pc[(sp + 3) * ps];
+            a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+            a.x += p1.x; a.y += p1.y; a.z += p1.z; a.w += p1.w;
+            a.x += p2.x; a.y += p2.y; a.z += p2.z; a.w += p2.w;
+            a.x += p3.x; a.y += p3.y; a.z += p3.z; a.w += p3.w;
+        }
+        for (; sp < n_part; ++sp) {
+            const float4 p0 = pc[sp * ps];
+            a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+        }
+        if (n_part > 0) xr[c] = a;
+        v[i] = a;
+        ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+    }
+    __shared__ float red[8], red2[8];
+    ss = warp_sum(ss);
+    if ((tid & 31) == 0) red[tid >> 5] = ss;
+    __syncthreads();
+    ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss += red[i];
+    const float inv = rsqrtf(ss / d + eps);
+    T* orow = out ? out + static_cast<size_t>(r) * d : nullptr;
+    T* crow = nullptr;
+    if (cache) {
+        const int t = tidx[r];
+        if (t >= t_lo && t <= t_hi) crow = cache + (static_cast<size_t>(slot[r]) * cache_rows + t) * d;
+    }
+    float hd = 0.f;
+#pragma unroll
+    for (int i = 0; i < kCols; ++i) {
+        const int c = tid + 256 * i;
+        if (c >= nv) continue;
+        const float y[4] = {v[i].x * inv * g[i].x, v[i].y * inv * g[i].y, v[i].z * inv * g[i].z,
+                            v[i].w * inv * g[i].w};
+        T t4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) t4[k] = fromf<T>(y[k]);
+        if (orow) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) orow[4 * c + k] = t4[k];
+        }
+        if (crow) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) crow[4 * c + k] = t4[k];
+        }
+        if (head_w)
+            hd += tof(t4[0]) * hw[i].x + tof(t4[1]) * hw[i].y + tof(t4[2]) * hw[i].z + tof(t4[3]) * hw[i].w;
+    }
+    if (head_w) {
+        hd = warp_sum(hd);
+        if ((tid & 31) == 0) red2[tid >> 5] = hd;
+        __syncthreads();
+        if (tid == 0) {
+            float t = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t += red2[i];
+            head_out[r] = t;
+        }
+    }
+}
+
 // ------------------------------------------------- RoPE + paged KV append
 // qkv row layout: [q (H*hd) | k (KV*hd) | v (KV*hd)], rotate-half RoPE.
+// With part != nullptr the qkv row is assembled from the decode GEMM's
+// split-K partials plus the q/k/v bias (rounded to T, exactly as the unsplit
+// GEMM's bias epilogue stores it) into shared memory first.
 template <class T>
 __global__ void rope_append(const T* __restrict__ qkv, T* q_out, KvView kv, int layer,
                             const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
-                            int rows, int n_heads, float theta) {
+                            int rows, int n_heads, float theta, const float* __restrict__ part,
+                            int n_part, size_t part_stride, const float* __restrict__ bias) {
+    extern __shared__ uint8_t rope_smem[];
     pdl_trigger();
     pdl_wait();
     const int r = blockIdx.x;
@@ -154,6 +285,35 @@ __global__ void rope_append(const T* __restrict__ qkv, T* q_out, KvView kv, int 
     const int H = n_heads, KV = kv.kv_heads;
     const int width = (H + 2 * KV) * hd;
     const T* src = qkv + static_cast<size_t>(r) * width;
+    if (part) {  // width % 4 == 0; float4 columns, split loads issued 4 at a time
+        T* row = reinterpret_cast<T*>(rope_smem);
+        const int nv = width >> 2;
+        const size_t ps = part_stride >> 2;
+        for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+            const float4* pc = reinterpret_cast<const float4*>(part) + static_cast<size_t>(r) * nv + c;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+            int sp = 0;
+            for (; sp + 4 <= n_part; sp += 4) {
+                const float4 p0 = pc[sp * ps], p1 = pc[(sp + 1) * ps], p2 = pc[(sp + 2) * ps],
+                             p3 = pc[(sp + 3) * ps];
+                a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+                a.x += p1.x; a.y += p1.y; a.z += p1.z; a.w += p1.w;
+                a.x += p2.x; a.y += p2.y; a.z += p2.z; a.w += p2.w;
+                a.x += p3.x; a.y += p3.y; a.z += p3.z; a.w += p3.w;
+            }
+            for (; sp < n_part; ++sp) {
+                const float4 p0 = pc[sp * ps];
+                a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+            }
+            const float4 b = bias ? reinterpret_cast<const float4*>(bias)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            row[4 * c] = fromf<T>(a.x + b.x);
+            row[4 * c + 1] = fromf<T>(a.y + b.y);
+            row[4 * c + 2] = fromf<T>(a.z + b.z);
+            row[4 * c + 3] = fromf<T>(a.w + b.w);
+        }
+        __syncthreads();
+        src = row;
+    }
     const int p = pos[r], s = slot[r];
     T* kc = static_cast<T*>(kv.k);
     T* vc = static_cast<T*>(kv.v);

@@ -92,6 +92,47 @@ def test_gemm_swiglu_epilogue():
     assert (y.float() - ref).abs().max().item() < 2e-2 * max(1, ref.abs().max().item())
 
 
+# decode GEMM (swap-AB tcgen05, gemm_dec.cuh): partial sums over splits, SwiGLU, store+bias
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 1152, 896), (40, 896, 896), (64, 896, 4864),
+                                   (129, 384, 256), (256, 896, 4864), (282, 1152, 896),
+                                   (298, 896, 4864), (512, 256, 128)])
+def test_gemm_dec_partials_vs_torch(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 11 + N)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    ws_floats = 16 << 20
+    ws = torch.full((ws_floats,), float("nan"), device="cuda")
+    sp = C.c_int32(0)
+    st = _lib().oppo_k_gemm_dec(M, N, K, _ptr(x), _ptr(w), None, None, 0, _ptr(ws), ws_floats,
+                                C.byref(sp), _stream())
+    assert st == 0, _lib().oppo_last_error_global()
+    assert 1 <= sp.value <= K // 64
+    y = ws[: sp.value * M * N].view(sp.value, M, N).sum(0)  # every partial written (no NaN left)
+    ref = x.double() @ w.double().T
+    rel = ((y.double() - ref).abs().max() / ref.abs().max()).item()
+    assert rel < 1e-4, rel
+
+
+@pytest.mark.parametrize("M", [3, 64, 200, 282])
+def test_gemm_dec_swiglu_and_store(M):
+    F, K = 384, 896
+    g = torch.Generator(device="cuda").manual_seed(M)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(2 * F, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(2 * F, device="cuda", generator=g)
+    y = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    assert _lib().oppo_k_gemm_dec(M, 2 * F, K, _ptr(x), _ptr(w), None, _ptr(y), 1, None, 0, None,
+                                  _stream()) == 0
+    z = x.float() @ w.float().T
+    ref = torch.nn.functional.silu(z[:, 0::2]) * z[:, 1::2]
+    assert (y.float() - ref).abs().max().item() < 2e-2 * max(1, ref.abs().max().item())
+    y2 = torch.empty(M, 2 * F, device="cuda", dtype=torch.bfloat16)
+    assert _lib().oppo_k_gemm_dec(M, 2 * F, K, _ptr(x), _ptr(w), _ptr(b), _ptr(y2), 2, None, 0, None,
+                                  _stream()) == 0
+    ref2 = z + b
+    assert (y2.float() - ref2).abs().max().item() < 2e-2 * max(1, ref2.abs().max().item())
+
+
 # ------------------------------------------------------------------ PPO
 def _ragged(case_list, key):
     return np.concatenate([np.asarray(c[key], dtype=np.float64) for c in case_list])
