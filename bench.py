@@ -144,6 +144,7 @@ def run_arm(eng, wl, cfg, seed, steps, warmup, rank, world, dist):
             int(st.n_tokens) * 4 + len(ids) * 4
         wall = time.perf_counter() - t0
         return dict(samples=len(ids), step_us=led.step_us, update_us=st.update_us, wall_s=wall,
+                    loop_us=led.decode_loop_us, loop_bytes=led.decode_weight_bytes + led.decode_kv_bytes,
                     decode_us=led.decode_us, score_us=led.score_us, iters=led.decode_iters,
                     decode_tokens=led.decode_tokens, prefill_tokens=led.prefill_tokens,
                     launches=led.kernel_launches, h2d=h2d, d2h=d2h, tokens=int(st.n_tokens),
@@ -179,22 +180,50 @@ def make_cfg(wl, baseline=False):
     return S.baseline(cfg) if baseline else cfg
 
 
-def kernel_roofline(hbm_peak):
-    """Dominant decode kernel class alone: the gate|up projection GEMM of the
-    0.5B actor at the step's full decode batch (M=282 sequences), swept over 24
-    distinct layer weights so they stream from HBM (24 x 17.4 MB > 126 MB L2)."""
-    from paper_2509_25762_b200._lib import lib
-    M, N, K = 282, 2 * 4864, 896
-    us = C.c_float()
-    st = lib().oppo_k_gemm_bench(M, N, K, 24, 240, 2, C.byref(us))
-    if st != 0:
+def decode_roofline(recs, hbm_peak, peak_src):
+    """The dominant unit of the step: one actor decode iteration (a CUDA graph
+    of ~200 launches: 24 layers x {RMSNorm, qkv GEMM, RoPE/KV append, paged
+    attention, O GEMM, RMSNorm, gate|up GEMM, down GEMM} + lm_head/sampling),
+    timed live with CUDA events on the actor stream over the timed steps'
+    decode loops.  Algorithmic bytes per iteration (SURVEY 8d B_dec): the
+    actor's weights once (non-embedding + lm_head, 0.988 GB) + per active row
+    the KV positions it reads and the row it appends (12,288 B per position)."""
+    loop_us = sum(r["loop_us"] for r in recs)
+    loop_b = sum(r["loop_bytes"] for r in recs)
+    iters = sum(r["iters"] for r in recs)
+    if loop_us <= 0 or iters <= 0:
         return None
-    algo = N * K * 2 + M * K * 2 + M * (N // 2) * 2  # weights + activations in + SwiGLU out
+    ach = loop_b / (loop_us * 1e-6) / 1e9
+    out = {"kernel": "actor decode iteration (CUDA graph: 24 layers + lm_head/sampling)",
+           "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+           "frac": round(ach / hbm_peak, 4), "traffic": None,
+           "algorithmic_bytes_per_launch": round(loop_b / iters),
+           "avg_launch_us": round(loop_us / iters, 2),
+           "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
+           "timing": "CUDA events on the actor stream around each step's decode loop"}
+    try:  # DRAM bytes of one decode iteration from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "r01_decode_iter_traffic.json")) as f:
+            t = json.load(f)
+        out["traffic"] = t["dram_bytes_per_iteration"]
+        out["traffic_source"] = t["source"]
+    except Exception:
+        pass
+    return out
+
+
+def gemm_microbench(hbm_peak):
+    """Secondary: the decode gate|up GEMM alone at M=64 rows (the step's median
+    batch), 24 distinct weight copies so weights stream from HBM."""
+    from paper_2509_25762_b200._lib import lib
+    M, N, K = 64, 2 * 4864, 896
+    us = C.c_float()
+    if lib().oppo_k_gemm_bench(M, N, K, 24, 240, 17, C.byref(us)) != 0:
+        return None
+    algo = N * K * 2 + M * K * 2 + M * (N // 2) * 2
     ach = algo / (us.value * 1e-6) / 1e9
-    return {"kernel": "gemm_bf16_tc (tcgen05+TMA) decode gate|up, M=282 N=9728 K=896",
-            "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(ach / hbm_peak, 4), "traffic": None,
-            "algorithmic_bytes_per_launch": algo, "avg_launch_us": round(us.value, 3)}
+    return {"kernel": "gemm_dec (swap-AB tcgen05+TMA) gate|up+SwiGLU, M=64 N=9728 K=896",
+            "achieved": round(ach, 1), "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
+            "avg_launch_us": round(us.value, 3)}
 
 
 def cpu_baseline(wl, budget_s=12.0):
@@ -313,9 +342,8 @@ def ours(args):
         "tokens_per_step": int(np.mean([r["tokens"] for r in rec])),
         "prefill_tokens_per_step": int(np.mean([r["prefill_tokens"] for r in rec])),
     }
-    line["roofline"] = kernel_roofline(hbm)
-    if line["roofline"]:
-        line["roofline"]["peak_source"] = peak_src + " (MEASURED_PEAKS.json hbm_gbs, burst)"
+    line["roofline"] = decode_roofline(rec, hbm, peak_src)
+    line["kernels"] = {"decode_gemm_gate_up": gemm_microbench(hbm)}
     line["cpu_baseline"] = cpu_baseline(wl) if not args.no_cpu else None
     line["clocks"] = clocks.summary()
     line["gpu_launches"] = int(sum(r["launches"] for r in rec))
