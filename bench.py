@@ -286,7 +286,7 @@ def ours(args):
                          max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
                          max_response_len=wl["cap"], page_size=64, device=local,
                          carry=cfg.carry_granularity, train_heads=1, sample_seed=2 + rank,
-                         weight_seed=1)
+                         weight_seed=1, scorer_sms=args.scorer_sms if not base else 0)
             recs, wall = run_arm(eng, wl, cfg, 7, args.steps, args.warmup, rank, world, dist)
             eng.close()
             torch.cuda.empty_cache()
@@ -319,7 +319,9 @@ def ours(args):
                    "global_batch": wl["batch"] * world, "parallelism": f"dp{world}",
                    "params_per_model": param_count(SHAPES[wl["actor"]]),
                    "l2": "working set > L2 (4 models x ~1 GB bf16 weights + paged KV)",
-                   "value_def": "samples / device time of (generation + scoring + PPO update)"},
+                   "value_def": "samples / device time of (generation + scoring + PPO update)",
+                   "sm_partition": f"scorers {args.scorer_sms} SMs | actor rest (green contexts)"
+                                   if args.scorer_sms else "shared (stream priorities)"},
         "gen_score_samples_per_s": round(o["samples"] / o["gen_s"], 2),
     }
     if "sequential" in res:
@@ -404,6 +406,8 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg1"])
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scorer-sms", type=int, default=64,
+                    help="fixed SM partition for the scorer stream in the overlapped arm (0: shared)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference(args)

@@ -302,7 +302,8 @@ typedef struct oppo_engine_cfg {
     int32_t world;
     int32_t use_graphs;       /* capture the decode iteration in a CUDA graph */
     int32_t train_heads;      /* PPO update trains lm_head (actor) + value head (critic) */
-    int32_t _pad;
+    int32_t scorer_sms;       /* fixed SM partition: SMs for the scorer stream (green
+                                 contexts, multiple of 8), the rest run the actor; 0 = shared */
     void* nccl_comm;          /* ncclComm_t or NULL (single GPU)       */
 } oppo_engine_cfg;
 

@@ -165,6 +165,64 @@ struct EngineExtra {
 };
 std::unordered_map<const Engine*, EngineExtra> g_extra;
 
+int env_int(const char* k, int dflt) {
+    const char* v = std::getenv(k);
+    return v ? std::atoi(v) : dflt;
+}
+
+template <class F>
+F driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+        throw Error(OPPO_ERR_CUDA, std::string(name) + " unavailable");
+    return reinterpret_cast<F>(p);
+}
+
+#define OPPO_CU_CHECK(x)                                                                    \
+    do {                                                                                    \
+        const CUresult r_ = (x);                                                            \
+        if (r_ != CUDA_SUCCESS)                                                             \
+            throw Error(OPPO_ERR_CUDA, std::string(#x) + " failed (" + std::to_string(r_) + ")"); \
+    } while (0)
+
+// Fixed SM partition (north_star: "concurrent streams with a fixed SM
+// partition"): two green contexts on the device, `scorer_sms` SMs (rounded up
+// to the architecture's granularity of 8) for the reward/critic/reference
+// prefill and the rest for the actor's decode.  Each stream is created inside
+// its green context, so kernels launched on it only run on its SMs; memory is
+// shared with the primary context.
+void make_sm_partition(Engine& e, int scorer_sms, int prio_hi, int prio_lo) {
+    using GetDev = CUresult (*)(CUdevice*, int);
+    using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+    using Split = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*,
+                               unsigned int, unsigned int);
+    using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+    using GCreate = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+    using GStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
+    CUdevice dev;
+    OPPO_CU_CHECK(driver_fn<GetDev>("cuDeviceGet")(&dev, e.cfg.device));
+    CUdevResource all{}, grp{}, rest{};
+    OPPO_CU_CHECK(driver_fn<GetRes>("cuDeviceGetDevResource")(dev, &all, CU_DEV_RESOURCE_TYPE_SM));
+    unsigned int n = 1;
+    OPPO_CU_CHECK(driver_fn<Split>("cuDevSmResourceSplitByCount")(&grp, &n, &all, &rest, 0,
+                                                                  static_cast<unsigned>(scorer_sms)));
+    if (n != 1 || rest.sm.smCount == 0) config_error("SM partition: scorer_sms leaves no actor SMs");
+    CUdevResourceDesc ds, da;
+    OPPO_CU_CHECK(driver_fn<GenDesc>("cuDevResourceGenerateDesc")(&ds, &grp, 1));
+    OPPO_CU_CHECK(driver_fn<GenDesc>("cuDevResourceGenerateDesc")(&da, &rest, 1));
+    OPPO_CU_CHECK(driver_fn<GCreate>("cuGreenCtxCreate")(&e.gctx_scorer, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+    OPPO_CU_CHECK(driver_fn<GCreate>("cuGreenCtxCreate")(&e.gctx_actor, da, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+    CUstream a, s;
+    OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&a, e.gctx_actor, CU_STREAM_NON_BLOCKING, prio_hi));
+    OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&s, e.gctx_scorer, CU_STREAM_NON_BLOCKING, prio_lo));
+    e.sa = reinterpret_cast<cudaStream_t>(a);
+    e.ss = reinterpret_cast<cudaStream_t>(s);
+    e.sms_actor = static_cast<int>(rest.sm.smCount);
+    e.sms_scorer = static_cast<int>(grp.sm.smCount);
+}
+
 // --------------------------------------------------------------- weights
 template <class T>
 void init_tensor(T* p, int64_t n, uint64_t seed, uint64_t id, float std_, cudaStream_t st) {
@@ -373,7 +431,7 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
                               : (!std::is_same_v<T, __nv_bfloat16> || !e.attn_cluster) ? 16
                               : hd == 32 ? attn_merge_splits<32>()
                               : hd == 64 ? attn_merge_splits<64>() : attn_merge_splits<128>();
-        splits = std::max(1, std::min(cdiv(per_sm * e.num_sms, base), max_split));
+        splits = std::max(1, std::min(cdiv(per_sm * w.sms, base), max_split));
         while (splits > 1 && static_cast<size_t>(R) * H * splits > w.attn_ws_rows) --splits;
     }
     (void)max_ctx;
@@ -540,8 +598,15 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         OPPO_CUDA_CHECK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, cfg.device));
         int lo = 0, hi = 0;
         OPPO_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
-        OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
+        OPPO_CUDA_CHECK(cudaFree(nullptr));  // make the primary context current
+        e->sms_actor = e->sms_scorer = e->num_sms;
+        const int split = cfg.scorer_sms > 0 ? cfg.scorer_sms : env_int("OPPO_SCORER_SMS", 0);
+        if (split > 0) {
+            make_sm_partition(*e, split, hi, lo);  // fixed SM split: scorers | actor
+        } else {
+            OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
+            OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
+        }
         for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
 
@@ -609,10 +674,8 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
             alloc_work<__nv_bfloat16>(*e, e->wa, std::max(e->S + 16, 32), false);
             alloc_work<__nv_bfloat16>(*e, e->ws, e->prefill_rows, true);
         }
-        auto env_int = [](const char* k, int dflt) {
-            const char* v = std::getenv(k);
-            return v ? std::atoi(v) : dflt;
-        };
+        e->wa.sms = e->sms_actor;
+        e->ws.sms = e->sms_scorer;
         e->attn_cluster = env_int("OPPO_ATTN_CLUSTER", 1) != 0;
         e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
         e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
@@ -668,6 +731,12 @@ void engine_free(Engine* e) {
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     if (e->sa) cudaStreamDestroy(e->sa);
     if (e->ss) cudaStreamDestroy(e->ss);
+    try {
+        using GDestroy = CUresult (*)(CUgreenCtx);
+        if (e->gctx_actor) driver_fn<GDestroy>("cuGreenCtxDestroy")(e->gctx_actor);
+        if (e->gctx_scorer) driver_fn<GDestroy>("cuGreenCtxDestroy")(e->gctx_scorer);
+    } catch (...) {
+    }
     delete e;
 }
 
@@ -681,9 +750,19 @@ void open_step(Engine& e) {
     e.launches = 0;
 }
 
+// The admission prefill and the PPO update run on the actor stream but use the
+// (prefill-sized) scorer workspace: size their grids for the actor partition.
+struct ActorSms {
+    Work& w;
+    int saved;
+    explicit ActorSms(Engine& e) : w(e.ws), saved(e.ws.sms) { w.sms = e.sms_actor; }
+    ~ActorSms() { w.sms = saved; }
+};
+
 template <class T>
 void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* prompts) {
     open_step(e);
+    ActorSms actor_sms(e);
     std::vector<int32_t> slots, lens;
     std::vector<int64_t> ids;
     std::vector<int32_t> pt_rows;  // page-table rows, S x max_pages layout subset
@@ -1290,6 +1369,7 @@ template <class T>
 void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hparams& hp,
                      oppo_ppo_stats& st_out) {
     cudaStream_t st = e.sa;
+    ActorSms actor_sms(e);
     cudaEvent_t t0, t1;
     OPPO_CUDA_CHECK(cudaEventCreate(&t0));
     OPPO_CUDA_CHECK(cudaEventCreate(&t1));

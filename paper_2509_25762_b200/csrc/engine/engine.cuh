@@ -57,6 +57,7 @@ struct Model {
 // Activation workspace of one stream (actor decode or scorer prefill).
 struct Work {
     int max_rows = 0;
+    int sms = 148;  // SMs of the partition this workspace's stream runs on (grid sizing)
     RowMeta meta{};
     float* x = nullptr;      // residual [R, dmax] fp32
     void* h = nullptr;       // normed   [R, dmax]
@@ -112,6 +113,8 @@ struct Engine {
     int dtype = OPPO_DTYPE_BF16;
     size_t esz = 2;
     int num_sms = 148;
+    int sms_actor = 148, sms_scorer = 148;  // fixed SM partition (green contexts) or the whole GPU
+    CUgreenCtx gctx_actor = nullptr, gctx_scorer = nullptr;
     Model models[N_MODELS];
 
     int S = 0, Pmax = 0, Lmax = 0, page_size = 64, max_pages = 0, n_pages = 0;

@@ -209,12 +209,12 @@ int gemm_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int 
                  const void* wt, int N, int ldw, int mode, void* y, int ldy, const float* bias) {
     e.launches += 1;
     return gemm_dec_impl(&e, st, x, M, K, ldx, wt, N, ldw, mode, y, ldy, bias, w.gemm_ws,
-                         w.gemm_ws_floats, e.num_sms, e.pdl);
+                         w.gemm_ws_floats, w.sms, e.pdl);
 }
 
 void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
               const void* wt, int N, int ldw, const EpiParams& ep) {
-    gemm_impl(&e, &w, st, x, M, K, ldx, wt, N, ldw, ep, e.dtype, e.num_sms, w.gemm_ws,
+    gemm_impl(&e, &w, st, x, M, K, ldx, wt, N, ldw, ep, e.dtype, w.sms, w.gemm_ws,
               w.gemm_ws_floats, w.gemm_cnt, w.gemm_cnt_n);
     e.launches += 1;
 }

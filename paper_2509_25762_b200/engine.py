@@ -45,7 +45,7 @@ class Engine:
     def __init__(self, actor="tiny", reward=None, critic=None, ref=None, dtype=abi.DTYPE_BF16,
                  max_slots=16, max_prompt_len=8, max_response_len=64, page_size=64, kv_pages=0,
                  weight_seed=1, sample_seed=2, carry=abi.CARRY_CHUNK, train_heads=0, device=0,
-                 nccl_comm=None, rank=0, world=1, use_graphs=1):
+                 nccl_comm=None, rank=0, world=1, use_graphs=1, scorer_sms=0):
         cfg = abi.EngineCfg()
         cfg.actor = dims(actor)
         cfg.reward = dims(reward or actor)
@@ -64,6 +64,7 @@ class Engine:
         cfg.rank, cfg.world = rank, world
         cfg.train_heads = train_heads
         cfg.use_graphs = use_graphs
+        cfg.scorer_sms = scorer_sms
         cfg.nccl_comm = nccl_comm
         self.cfg = cfg
         self.h = C.c_void_p()
