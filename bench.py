@@ -97,72 +97,51 @@ def host_prompts(ids, P, V, seed):
 
 
 def run_arm(eng, wl, cfg, seed, steps, warmup, rank, world, dist):
-    """Python-side driver loop over the C ABI (driver.cpp:103-195), host prompts
-    copied in at admission and step results read back every step."""
-    from paper_2509_25762_b200 import abi
-    from paper_2509_25762_b200 import scheduler as S
+    """The data-parallel step loop (paper_2509_25762_b200.dp.run_rank, i.e.
+    driver.cpp:103-195 per rank) through the C ABI: host prompts copied in at
+    admission, step results read back every step.  Returns the timed steps."""
+    from paper_2509_25762_b200 import dp
     import torch
 
-    B = cfg.batch_size
-    lengths = S.sample_lengths(cfg.lengths, seed ^ rank, 50000)
-    ctl = S.DeltaController(cfg.controller, cfg.window, cfg.delta_min, cfg.delta_max,
-                            cfg.delta_inc, cfg.delta_dec)
-    hp = cfg.ppo
-    entries, next_id, delta = [], 0, cfg.delta_init
     V = eng.cfg.actor.vocab
     P = cfg.prompt_len
-    recs = []
+    ex = dp.GpuExecutor(eng, prompt_fn=lambda ids: host_prompts(ids, P, V, 1234))
+    marks = {}
 
-    def one_step(step):
-        nonlocal entries, next_id, delta
-        t0 = time.perf_counter()
-        fresh = []
-        while len(entries) + len(fresh) < B + delta:
-            fresh.append(S.seq_array([dict(id=next_id, prompt_len=P, target_len=lengths[next_id],
-                                           admitted_at=step, arrival_step=step)])[0])
-            next_id += 1
-        h2d = 0
-        if fresh:
-            pr = host_prompts([f.id for f in fresh], P, V, 1234 + rank)
-            eng.admit(fresh, prompts=pr)
-            h2d += sum(p.nbytes for p in pr) + len(fresh) * C.sizeof(abi.SeqState)
-        entries = entries + fresh
-        active = [e for e in entries if not e.scored]
-        pre = len(entries) - len(active)
-        need = B - pre
-        outs, led = [], abi.Ledger()
-        if active and need > 0:
-            outs, led = eng.run_step(active, cfg.chunk_size, cfg.schedule_mode, need)
-            h2d += len(active) * C.sizeof(abi.SeqState)
-        batch, entries, _ = S.select_finished(entries, outs, B)
-        ids = [b.id for b in batch]
-        st = eng.ppo_update(ids, hp) if ids else abi.PpoStats()
-        eng.release(ids)
-        ctl.observe(st.mean_reward)
-        delta, _ = ctl.update(delta)
-        d2h = len(outs) * C.sizeof(abi.SeqOutcome) + C.sizeof(abi.PpoStats) + \
-            int(st.n_tokens) * 4 + len(ids) * 4
-        wall = time.perf_counter() - t0
-        return dict(samples=len(ids), step_us=led.step_us, update_us=st.update_us, wall_s=wall,
-                    loop_us=led.decode_loop_us, loop_bytes=led.decode_weight_bytes + led.decode_kv_bytes,
-                    decode_us=led.decode_us, score_us=led.score_us, iters=led.decode_iters,
-                    decode_tokens=led.decode_tokens, prefill_tokens=led.prefill_tokens,
-                    launches=led.kernel_launches, h2d=h2d, d2h=d2h, tokens=int(st.n_tokens),
-                    reward=st.mean_reward, obj=st.ppo_objective)
+    def on_step(rec):
+        if rec["step"] == warmup - 1 or (warmup == 0 and rec["step"] == 0 and "t0" not in marks):
+            if warmup > 0:
+                if dist:
+                    dist.barrier()
+                torch.cuda.synchronize()
+            marks["t0"] = time.perf_counter()
 
-    for s in range(warmup):
-        one_step(s)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for s in range(warmup, warmup + steps):
-        recs.append(one_step(s))
+    if warmup == 0:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        marks["t0"] = time.perf_counter()
+    recs = dp.run_rank(cfg, seed, rank, world, ex, steps=warmup + steps, on_step=on_step)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    wall = time.perf_counter() - t0
-    return recs, wall
+    wall = time.perf_counter() - marks["t0"]
+    out = []
+    for r in recs[warmup:]:
+        led, st = r["ledger"], r["stats"] or abi_stats()
+        out.append(dict(samples=len(r["ids"]), step_us=led.step_us, update_us=st.update_us,
+                        wall_s=r["wall_s"], loop_us=led.decode_loop_us,
+                        loop_bytes=led.decode_weight_bytes + led.decode_kv_bytes,
+                        decode_us=led.decode_us, score_us=led.score_us, iters=led.decode_iters,
+                        decode_tokens=led.decode_tokens, prefill_tokens=led.prefill_tokens,
+                        launches=led.kernel_launches, h2d=r["h2d"], d2h=r["d2h"] + int(st.n_tokens) * 4,
+                        tokens=int(st.n_tokens), reward=r["mean_reward"], obj=st.ppo_objective))
+    return out, wall
+
+
+def abi_stats():
+    from paper_2509_25762_b200 import abi
+    return abi.PpoStats()
 
 
 def make_cfg(wl, baseline=False):
@@ -272,7 +251,8 @@ def ours(args):
         dist = td
     torch.cuda.set_device(local)
     from paper_2509_25762_b200 import abi
-    from paper_2509_25762_b200.engine import Engine, param_count, SHAPES
+    from paper_2509_25762_b200.engine import Engine, param_count, SHAPES, nccl_comm_from_torch
+    comm = nccl_comm_from_torch(rank, world, local) if world > 1 else None
 
     wl = TINY if args.workload == "cfg1" else CFG2
     hbm, tflops, peak_src = peaks()
@@ -286,7 +266,8 @@ def ours(args):
                          max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
                          max_response_len=wl["cap"], page_size=64, device=local,
                          carry=cfg.carry_granularity, train_heads=1, sample_seed=2 + rank,
-                         weight_seed=1, scorer_sms=args.scorer_sms if not base else 0)
+                         weight_seed=1, scorer_sms=args.scorer_sms if not base else 0,
+                         nccl_comm=comm, rank=rank, world=world)
             recs, wall = run_arm(eng, wl, cfg, 7, args.steps, args.warmup, rank, world, dist)
             eng.close()
             torch.cuda.empty_cache()

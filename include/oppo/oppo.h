@@ -358,6 +358,17 @@ oppo_status oppo_read_rollout(oppo_engine* e, int64_t id, int32_t* tokens, float
 oppo_status oppo_run_seed(oppo_engine* e, const oppo_run_config* cfg, uint64_t seed,
                           oppo_step_record* records, int32_t* n_records, int64_t* sel_ids);
 
+/* Data-parallel plumbing: one NCCL communicator over the GPUs of
+ * the box; pass it as oppo_engine_cfg.nccl_comm with rank/world.  The engine
+ * then allreduces the whitening / reward statistics and the trained heads'
+ * gradients inside oppo_ppo_update.  Rank 0 creates the id and ships it to
+ * the other ranks (e.g. torch.distributed broadcast). */
+#define OPPO_NCCL_ID_BYTES 128
+oppo_status oppo_nccl_unique_id(uint8_t* out /* OPPO_NCCL_ID_BYTES */);
+oppo_status oppo_nccl_comm_create(const uint8_t* id, int32_t world, int32_t rank, int32_t device,
+                                  void** comm);
+oppo_status oppo_nccl_comm_destroy(void* comm);
+
 /* Prompt tokens of an admitted sequence (synthetic stream or caller-provided). */
 oppo_status oppo_read_prompt(oppo_engine* e, int64_t id, int32_t* out, int32_t cap, int32_t* len);
 

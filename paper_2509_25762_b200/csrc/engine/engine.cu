@@ -26,6 +26,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <nccl.h>
+
 #include "engine.cuh"
 #include "host/driver.hpp"
 #include "kernels/ppo.cuh"
@@ -405,6 +407,49 @@ void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
     }
 }
 
+// Decode attention with RoPE + KV append fused (attn_dec.cuh), bf16.  The
+// qkv row comes from the decode GEMM's partials (n_part > 0) or a bf16 row.
+template <int HD>
+void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
+                        const float* part, int n_part, const float* bias) {
+    using Cf = AttnDecCfg<HD>;
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cf::SMEM));
+    });
+    const auto& d = m.dims;
+    const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
+    const int base = R * d.n_kv_heads;
+    int nsp = std::max(1, std::min(cdiv(2 * w.sms, base), Cf::MAX_SPLIT));
+    if (e.attn_max_split > 0) nsp = std::min(nsp, e.attn_max_split);
+    const dim3 grid(R, d.n_kv_heads, nsp);
+    auto* out = static_cast<__nv_bfloat16*>(w.attn);
+    const auto* qkv = static_cast<const __nv_bfloat16*>(w.qkv);
+    const size_t pstride = static_cast<size_t>(R) * m.qkv_width();
+    if (nsp > 1)
+        launch_cluster_z(e.pdl, nsp, attn_dec<HD>, grid, dim3(128), Cf::SMEM, st, part, n_part, pstride, bias,
+                         qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta);
+    else
+        launch(e.pdl, attn_dec<HD>, grid, dim3(128), Cf::SMEM, st, part, n_part, pstride, bias, qkv, out, kv,
+               layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta);
+    e.launches += 1;
+}
+
+bool attn_dec_supported(const oppo_model_dims& d) {
+    const int G = d.n_heads / d.n_kv_heads;
+    return G <= 16 && (d.head_dim == 32 || d.head_dim == 64 || d.head_dim == 128);
+}
+
+void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
+                     const float* part, int n_part, const float* bias) {
+    switch (m.dims.head_dim) {
+    case 32: attn_dec_launch_hd<32>(e, m, w, st, layer, R, part, n_part, bias); break;
+    case 64: attn_dec_launch_hd<64>(e, m, w, st, layer, R, part, n_part, bias); break;
+    default: attn_dec_launch_hd<128>(e, m, w, st, layer, R, part, n_part, bias); break;
+    }
+}
+
 template <class T>
 struct Final {
     bool write_h = true;
@@ -461,6 +506,7 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         // OPPO_DEBUG_SKIP (perf diagnosis only; results are garbage): bit 1
         // attention, 2 RoPE/KV append, 4 norms, 8 projection GEMMs
         const int skip = e.debug_skip;
+        const bool fused_attn = e.attn_fused && attn_dec_supported(d);
         for (int l = 0; l < d.n_layers; ++l) {
             const auto& L = m.layers[l];
             if (!(skip & 4)) launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, L.ln1,
@@ -480,10 +526,15 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
                 ep.scale = 1.f;
                 gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
             }
-            if (!(skip & 2)) launch(e.pdl, rope_append<T>, dim3(R), dim3(128), sq ? rope_smem : 0, st,
-                   static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l, w.meta.slot, w.meta.pos, R,
-                   H, kRopeTheta, sq ? part : nullptr, sq, static_cast<size_t>(R) * m.qkv_width(), L.bqkv);
-            if (!(skip & 1)) attn_mma_launch(e, m, w, st, l, R, decode, splits, qblocks, n_qblocks);
+            if (fused_attn) {  // RoPE + KV append + attention in one launch
+                if (!(skip & 1)) attn_dec_launch(e, m, w, st, l, R, sq ? part : nullptr, sq, L.bqkv);
+            } else {
+                if (!(skip & 2)) launch(e.pdl, rope_append<T>, dim3(R), dim3(128), sq ? rope_smem : 0, st,
+                       static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l, w.meta.slot, w.meta.pos, R,
+                       H, kRopeTheta, sq ? part : nullptr, sq, static_cast<size_t>(R) * m.qkv_width(), L.bqkv);
+                if (!(skip & 1)) attn_mma_launch(e, m, w, st, l, R, decode, splits, qblocks, n_qblocks);
+                e.launches += 2;  // rope + attention
+            }
             np = (skip & 8) ? 0 : residual(w.attn, m.q_width(), L.wo);
             if (!(skip & 4)) launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, L.ln2,
                    static_cast<T*>(w.h), R, D, kRmsEps, part, np, static_cast<size_t>(R) * D, nullptr,
@@ -500,7 +551,7 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
                 gemm_run(e, w, st, w.h, R, D, D, L.wgu, 2 * d.d_ff, D, ep);
             }
             np = (skip & 8) ? 0 : residual(w.ff, d.d_ff, L.wdown);
-            e.launches += 4;
+            e.launches += 2;  // the two norms (GEMMs / attention count themselves)
         }
         launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, m.final_norm,
                fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, part, np,
@@ -680,6 +731,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
         e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
         e->debug_skip = env_int("OPPO_DEBUG_SKIP", 0);
+        e->attn_fused = env_int("OPPO_ATTN_FUSED", 1) != 0;
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
         e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 128);
@@ -726,7 +778,8 @@ void engine_free(Engine* e) {
         if (m.lm_master) cudaFree(m.lm_master);
     }
     for (void* p : {static_cast<void*>(e->d_hf_actor), static_cast<void*>(e->d_hf_critic),
-                    static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf})
+                    static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf,
+                    static_cast<void*>(e->g_lm)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     if (e->sa) cudaStreamDestroy(e->sa);
@@ -1365,6 +1418,31 @@ __global__ void sq_err_sum(const float* v, const float* r, int n, double* out) {
     }
 }
 
+__global__ void sum_floats(const float* x, int n, double* out) {
+    double s = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    s = warp_sum_d(s);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += sh[i];  // fixed order
+        *out = t;
+    }
+}
+__global__ void add_into(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+
+#define OPPO_NCCL_CHECK(x)                                                                  \
+    do {                                                                                    \
+        const ncclResult_t r_ = (x);                                                        \
+        if (r_ != ncclSuccess)                                                              \
+            throw ::oppo::Error(OPPO_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
 template <class T>
 void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hparams& hp,
                      oppo_ppo_stats& st_out) {
@@ -1432,14 +1510,35 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     gae_scan<float><<<cdiv(n * 32, 128), 128, 0, st>>>(n, d_off, d_rew, d_vals,
                                                       static_cast<float>(hp.gamma),
                                                       static_cast<float>(hp.lambda), d_adv, d_ret);
-    // K9 whitening statistics (+ NCCL allreduce across ranks in DP runs)
-    const int mb = std::min(1024, cdiv(N, 256));
+    // K9 whitening statistics.  Data-parallel runs allreduce
+    // {sum adv, sum adv^2, n_tokens, sum reward, n_samples} in one fp64 NCCL
+    // call: whitening uses the global moments, the token mean of the
+    // objective / gradients the global token count, and every rank's Delta
+    // controller the global mean reward.
+    const bool dp = e.nccl != nullptr && e.cfg.world > 1;
+    const int mb = std::min(1024, std::max(1, cdiv(N, 256)));
     double* stats = nullptr;
-    if (hp.whiten) {
+    double n_glob = N, score_glob = 0, samples_glob = n;
+    if (hp.whiten || dp) {
         moments<float><<<mb, 256, 0, st>>>(d_adv, N, d_part);
         moments_final<<<1, 32, 0, st>>>(d_part, mb, static_cast<double>(N), d_stats);
-        stats = d_stats;
+        if (hp.whiten) stats = d_stats;
     }
+    if (dp) {
+        sum_floats<<<1, 256, 0, st>>>(d_score, n, d_stats + 3);
+        const double nn = n;
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(d_stats + 6, &nn, 8, cudaMemcpyHostToDevice, st));
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(d_stats + 4, d_stats + 6, 8, cudaMemcpyDeviceToDevice, st));
+        OPPO_NCCL_CHECK(ncclAllReduce(d_stats, d_stats, 5, ncclDouble, ncclSum,
+                                      static_cast<ncclComm_t>(e.nccl), st));
+        double g[5];
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(g, d_stats, 5 * 8, cudaMemcpyDeviceToHost, st));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
+        n_glob = g[2];
+        score_glob = g[3];
+        samples_glob = g[4];
+    }
+    const float inv_n_glob = 1.0f / static_cast<float>(std::max(1.0, n_glob));
     // current-policy log-probs of the sampled tokens from the cached actor hidden states
     const int nt = gemm_logit_tiles(e.dtype, V);
     Work& w = e.ws;
@@ -1459,7 +1558,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     // K10 clipped objective and d obj / d logp
     const int cb = std::min(1024, cdiv(N, 256));
     ppo_clip<float><<<cb, 256, 0, st>>>(N, d_new, d_old, d_adv, static_cast<float>(hp.clip_epsilon),
-                                        stats, 1e-8, d_dobj, d_part, 1.0f / std::max(1, N));
+                                        stats, 1e-8, d_dobj, d_part, inv_n_glob);
     sum_partials<<<1, 32, 0, st>>>(d_part, cb, d_stats + 4);
     // K11 head update: lm_head += lr * dObj/dW  (gradient ascent, ppo.cpp:288-290)
     if (e.cfg.train_heads && hp.learning_rate > 0) {
@@ -1468,6 +1567,15 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
             e.g_buf = dalloc(static_cast<size_t>(V) * gc * sizeof(T));
             e.ht_buf = dalloc(static_cast<size_t>(std::max(Da, Dc)) * gc * sizeof(T));
             e.vgrad = static_cast<float*>(dalloc(std::max(Da, Dc) * 4));
+        }
+        // DP: accumulate lr * dObj/dW into a gradient buffer, allreduce it, then
+        // apply; single GPU: accumulate straight into the fp32 master
+        const size_t nw = static_cast<size_t>(V) * Da;
+        float* gdst = actor.lm_master;
+        if (dp) {
+            if (!e.g_lm) e.g_lm = static_cast<float*>(dalloc(nw * 4));
+            OPPO_CUDA_CHECK(cudaMemsetAsync(e.g_lm, 0, nw * 4, st));
+            gdst = e.g_lm;
         }
         for (int c0 = 0; c0 < N; c0 += gc) {
             const int cn = std::min(gc, N - c0);
@@ -1485,16 +1593,24 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
                 d_hf + static_cast<size_t>(c0) * Da, cn, Da, cp, static_cast<T*>(e.ht_buf));
             EpiParams eg{};
             eg.mode = EPI_ADD_F32;
-            eg.y = actor.lm_master;
+            eg.y = gdst;
             eg.ldy = Da;
             eg.scale = static_cast<float>(hp.learning_rate);
             gemm_run(e, w, st, e.g_buf, V, cp, cp, e.ht_buf, Da, cp, eg);
         }
-        const size_t nn = static_cast<size_t>(V) * Da;
+        if (dp) {  // gradient allreduce (sum: every rank's dObj already carries 1/N_global)
+            OPPO_NCCL_CHECK(ncclAllReduce(e.g_lm, e.g_lm, nw, ncclFloat, ncclSum,
+                                          static_cast<ncclComm_t>(e.nccl), st));
+            add_into<<<cdiv(static_cast<int64_t>(nw), 256), 256, 0, st>>>(actor.lm_master, e.g_lm,
+                                                                        static_cast<int64_t>(nw));
+        }
+        const size_t nn = nw;
         convert<float, T><<<cdiv(nn, 256), 256, 0, st>>>(actor.lm_master, static_cast<T*>(actor.lm_head), nn);
         // critic value head: w -= vlr * (1/N) sum (V - R) h
-        value_head_grad<T><<<cdiv(Dc, 128), 128, 0, st>>>(d_hc, Dc, N, d_vtok, d_ret, e.vgrad,
-                                                          1.0f / std::max(1, N));
+        value_head_grad<T><<<cdiv(Dc, 128), 128, 0, st>>>(d_hc, Dc, N, d_vtok, d_ret, e.vgrad, inv_n_glob);
+        if (dp)
+            OPPO_NCCL_CHECK(ncclAllReduce(e.vgrad, e.vgrad, Dc, ncclFloat, ncclSum,
+                                          static_cast<ncclComm_t>(e.nccl), st));
         head_sgd<<<cdiv(Dc, 128), 128, 0, st>>>(critic.head, e.vgrad, Dc,
                                                 static_cast<float>(hp.value_learning_rate));
     }
@@ -1516,6 +1632,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     for (float x : score) sr += x;
     for (float x : kl) sk += x;
     st_out.mean_reward = n ? sr / n : 0.0;
+    if (dp) st_out.mean_reward = samples_glob > 0 ? score_glob / samples_glob : 0.0;  // global mean
     st_out.kl_mean = N ? sk / N : 0.0;
     st_out.ppo_objective = N ? hs[4] / N : 0.0;
     st_out.value_loss = N ? 0.5 * hs[5] / N : 0.0;
@@ -1835,6 +1952,41 @@ oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
         oppo_set_global_error(x.what());
         return x.code;
     }
+}
+
+oppo_status oppo_nccl_unique_id(uint8_t* out) {
+    try {
+        static_assert(sizeof(ncclUniqueId) == OPPO_NCCL_ID_BYTES, "ncclUniqueId size");
+        ncclUniqueId id;
+        OPPO_NCCL_CHECK(ncclGetUniqueId(&id));
+        std::memcpy(out, &id, sizeof(id));
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
+
+oppo_status oppo_nccl_comm_create(const uint8_t* id, int32_t world, int32_t rank, int32_t device,
+                                  void** comm) {
+    try {
+        if (world < 1 || rank < 0 || rank >= world) oppo::config_error("rank/world out of range");
+        OPPO_CUDA_CHECK(cudaSetDevice(device));
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        ncclComm_t c;
+        OPPO_NCCL_CHECK(ncclCommInitRank(&c, world, uid, rank));
+        *comm = c;
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
+
+oppo_status oppo_nccl_comm_destroy(void* comm) {
+    if (comm) ncclCommDestroy(static_cast<ncclComm_t>(comm));
+    return OPPO_OK;
 }
 
 // Decode GEMM (gemm_dec.cuh) alone: mode 0 partials (d_ws [splits][M][N] fp32,

@@ -18,6 +18,7 @@
 #include "engine/launch.cuh"
 #include "kernels/model.cuh"
 #include "kernels/attn_mma.cuh"
+#include "kernels/attn_dec.cuh"
 #include "oppo/oppo.h"
 
 namespace oppo {
@@ -150,7 +151,8 @@ struct Engine {
     bool attn_cluster = true;  // split-KV merge in DSMEM (else workspace + combine kernel)
     int attn_per_sm = 4;       // target decode attention CTAs per SM
     int attn_max_split = 0;
-    int debug_skip = 0;        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
+    int debug_skip = 0;
+    bool attn_fused = true;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
     int dec_qkv_max = 96;      // largest batch for which qkv uses the swap-AB decode GEMM
     int dec_gu_max = 64;       // ... gate|up
     int dec_res_max = 128;     // ... O and down (down always: K >= 2048)
@@ -173,6 +175,7 @@ struct Engine {
     void* ht_buf = nullptr;  // transposed hidden [d, chunk]
     int g_chunk = 4096;
     float* vgrad = nullptr;
+    float* g_lm = nullptr;   // DP: lm_head gradient buffer (allreduced)
     void* nccl = nullptr;
 };
 

@@ -166,3 +166,21 @@ class Engine:
         self._check(lib().oppo_run_seed(self.h, C.byref(cfg), seed, recs, C.byref(n), sel))
         b = cfg.batch_size
         return list(recs[:n.value]), [list(sel[i * b:(i + 1) * b]) for i in range(n.value)]
+
+
+NCCL_ID_BYTES = 128
+
+
+def nccl_comm_from_torch(rank, world, device):
+    """One NCCL communicator for the engine (oppo_engine_cfg.nccl_comm): rank 0
+    makes the id, torch.distributed (already initialised) broadcasts it."""
+    import torch.distributed as dist
+    buf = (C.c_uint8 * NCCL_ID_BYTES)()
+    if rank == 0:
+        check(lib().oppo_nccl_unique_id(buf))
+    obj = [bytes(buf) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    C.memmove(buf, obj[0], NCCL_ID_BYTES)
+    comm = C.c_void_p()
+    check(lib().oppo_nccl_comm_create(buf, world, rank, device, C.byref(comm)))
+    return comm.value
