@@ -450,6 +450,109 @@ void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
     }
 }
 
+// ------------------------------------------------ persistent decode kernel
+bool mega_supported(const Engine& e, const oppo_model_dims& d) {
+    const int G = d.n_heads / d.n_kv_heads;
+    return e.dtype == OPPO_DTYPE_BF16 && G <= 16 && (d.head_dim == 64 || d.head_dim == 128) &&
+           d.d_model % 64 == 0 && d.d_model <= 3584 && (d.n_heads * d.head_dim) % 64 == 0 &&
+           d.d_ff % 64 == 0;
+}
+
+void mega_setup(Engine& e) {
+    Model& m = e.models[ACTOR];
+    const auto& d = m.dims;
+    std::vector<mega::LayerP> lp(d.n_layers);
+    const int qkvw = m.qkv_width(), qw = m.q_width();
+    for (int l = 0; l < d.n_layers; ++l) {
+        const auto& L = m.layers[l];
+        lp[l].w[mega::W_QKV] = make_tma_2d(L.wqkv, qkvw, d.d_model, d.d_model, 128);
+        lp[l].w[mega::W_O] = make_tma_2d(L.wo, d.d_model, qw, qw, 128);
+        lp[l].w[mega::W_GU] = make_tma_2d(L.wgu, 2 * d.d_ff, d.d_model, d.d_model, 128);
+        lp[l].w[mega::W_DN] = make_tma_2d(L.wdown, d.d_model, d.d_ff, d.d_ff, 128);
+        lp[l].bqkv = L.bqkv;
+        lp[l].ln1 = L.ln1;
+        lp[l].ln2 = L.ln2;
+    }
+    e.d_mega_layers = static_cast<mega::LayerP*>(dalloc(lp.size() * sizeof(mega::LayerP)));
+    OPPO_CUDA_CHECK(cudaMemcpy(e.d_mega_layers, lp.data(), lp.size() * sizeof(mega::LayerP),
+                               cudaMemcpyHostToDevice));
+    e.d_mega_bar = static_cast<unsigned*>(dalloc(64));
+    OPPO_CUDA_CHECK(cudaMemset(e.d_mega_bar, 0, 64));
+    const size_t rows = static_cast<size_t>(e.S + 16) * d.n_kv_heads;
+    const size_t slot = static_cast<size_t>(16) * d.head_dim + 32;
+    e.d_mega_aws = static_cast<float*>(dalloc(rows * 4 * slot * 4));
+    e.d_mega_acnt = static_cast<int*>(dalloc(rows * 4));
+    OPPO_CUDA_CHECK(cudaMemset(e.d_mega_acnt, 0, rows * 4));
+}
+
+// One decode iteration's transformer stack as one persistent kernel; returns
+// the split count of the down-projection partials left for the final norm.
+template <int HD>
+int mega_launch_hd(Engine& e, Model& m, Work& w, cudaStream_t st, int R) {
+    const auto& d = m.dims;
+    mega::Args a{};
+    a.M = R;
+    a.Mp = (R + 15) / 16 * 16;
+    a.D = d.d_model;
+    a.H = d.n_heads;
+    a.KV = d.n_kv_heads;
+    a.HD = d.head_dim;
+    a.F = d.d_ff;
+    a.L = d.n_layers;
+    a.qkvw = m.qkv_width();
+    a.qw = m.q_width();
+    a.x = w.x;
+    a.h = static_cast<__nv_bfloat16*>(w.h);
+    a.attn = static_cast<__nv_bfloat16*>(w.attn);
+    a.ff = static_cast<__nv_bfloat16*>(w.ff);
+    a.ws = w.gemm_ws;
+    a.aws = e.d_mega_aws;
+    a.acnt = e.d_mega_acnt;
+    a.bar = e.d_mega_bar;
+    a.layers = e.d_mega_layers;
+    a.kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
+    a.slot = w.meta.slot;
+    a.pos = w.meta.pos;
+    const int G = w.sms;  // one CTA per SM of the actor partition
+    const int Ns[4] = {a.qkvw, a.D, 2 * a.F, a.D}, Ks[4] = {a.D, a.qw, a.D, a.F};
+    for (int g = 0; g < 4; ++g) {
+        const int tiles = (Ns[g] + 127) / 128, kbt = Ks[g] / 64;
+        int sp = g == mega::W_GU ? 1 : std::max(1, std::min(kbt, G / tiles));
+        while (sp > 1 && static_cast<size_t>(sp) * R * Ns[g] > w.gemm_ws_floats) --sp;
+        a.kbps[g] = (kbt + sp - 1) / sp;
+        a.sp[g] = (kbt + a.kbps[g] - 1) / a.kbps[g];
+    }
+    a.att_sp = std::max(1, std::min(4, G / std::max(1, R * a.KV)));
+    a.stage_bytes = dec::kWBytes + a.Mp * 128;
+    const int attn_smem = AttnDecCfg<HD>::SMEM;
+    const int budget = 227 * 1024 - 1024 - attn_smem - 512;
+    a.stages = std::max(1, std::min(8, budget / a.stage_bytes));
+    a.attn_off = a.stages * a.stage_bytes;
+    int cols = 32;
+    while (cols < a.Mp) cols *= 2;
+    a.tmem_cols = cols;
+    a.first_np = 0;
+    a.eps = kRmsEps;
+    a.theta = kRopeTheta;
+    const int smem = 1024 + a.attn_off + attn_smem + 512;
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(mega::decode_layers<HD>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    });
+    CUtensorMap s1, s2, s3;
+    const CUtensorMap& xh = cached_map_pub(&e, w.h, R, a.D, a.D, a.Mp, s1);
+    const CUtensorMap& xa = cached_map_pub(&e, w.attn, R, a.qw, a.qw, a.Mp, s2);
+    const CUtensorMap& xf = cached_map_pub(&e, w.ff, R, a.F, a.F, a.Mp, s3);
+    launch(e.pdl, mega::decode_layers<HD>, dim3(G), dim3(128), smem, st, xh, xa, xf, a);
+    e.launches += 1;
+    return a.sp[mega::W_DN];
+}
+
+int mega_launch(Engine& e, Model& m, Work& w, cudaStream_t st, int R) {
+    return m.dims.head_dim == 64 ? mega_launch_hd<64>(e, m, w, st, R) : mega_launch_hd<128>(e, m, w, st, R);
+}
+
 template <class T>
 struct Final {
     bool write_h = true;
@@ -484,6 +587,16 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
     // by the consumer kernels (RoPE/KV append, RMSNorm residual add)
     const bool dec_gemm = std::is_same_v<T, __nv_bfloat16> && decode && R <= 512 && D <= 4096 &&
                           D % 64 == 0 && m.q_width() % 64 == 0 && d.d_ff % 64 == 0;
+    if (dec_gemm && e.d_mega_layers && &m == &e.models[ACTOR] && R <= e.mega_max_rows) {
+        const int np = mega_launch(e, m, w, st, R);
+        launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, m.final_norm,
+               fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, w.gemm_ws, np,
+               static_cast<size_t>(R) * D, fin.head, w.head_out, fin.cache, w.meta.slot, w.meta.t,
+               e.tok_stride, fin.t_lo, fin.t_hi);
+        e.launches += 2;
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     if (dec_gemm) {
         const size_t rope_smem = static_cast<size_t>(m.qkv_width()) * sizeof(T);
         const float* part = w.gemm_ws;
@@ -654,9 +767,11 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         const int split = cfg.scorer_sms > 0 ? cfg.scorer_sms : env_int("OPPO_SCORER_SMS", 0);
         if (split > 0) {
             make_sm_partition(*e, split, hi, lo);  // fixed SM split: scorers | actor
+            OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->su, cudaStreamNonBlocking, hi));
         } else {
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
+            e->su = e->sa;
         }
         for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
@@ -727,6 +842,8 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         e->wa.sms = e->sms_actor;
         e->ws.sms = e->sms_scorer;
+        e->mega_max_rows = env_int("OPPO_MEGA_MAX_ROWS", 256);
+        if (e->mega_max_rows > 0 && mega_supported(*e, cfg.actor)) mega_setup(*e);
         e->attn_cluster = env_int("OPPO_ATTN_CLUSTER", 1) != 0;
         e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
         e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
@@ -779,9 +896,12 @@ void engine_free(Engine* e) {
     }
     for (void* p : {static_cast<void*>(e->d_hf_actor), static_cast<void*>(e->d_hf_critic),
                     static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf,
-                    static_cast<void*>(e->g_lm)})
+                    static_cast<void*>(e->g_lm), static_cast<void*>(e->d_mega_layers),
+                    static_cast<void*>(e->d_mega_bar), static_cast<void*>(e->d_mega_aws),
+                    static_cast<void*>(e->d_mega_acnt)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
+    if (e->su && e->su != e->sa) cudaStreamDestroy(e->su);
     if (e->sa) cudaStreamDestroy(e->sa);
     if (e->ss) cudaStreamDestroy(e->ss);
     try {
@@ -803,12 +923,13 @@ void open_step(Engine& e) {
     e.launches = 0;
 }
 
-// The admission prefill and the PPO update run on the actor stream but use the
-// (prefill-sized) scorer workspace: size their grids for the actor partition.
+// The admission prefill and the PPO update run between decode loops on the
+// whole-GPU stream su with the (prefill-sized) scorer workspace: size their
+// grids for all SMs.
 struct ActorSms {
     Work& w;
     int saved;
-    explicit ActorSms(Engine& e) : w(e.ws), saved(e.ws.sms) { w.sms = e.sms_actor; }
+    explicit ActorSms(Engine& e) : w(e.ws), saved(e.ws.sms) { w.sms = e.num_sms; }
     ~ActorSms() { w.sms = saved; }
 };
 
@@ -879,8 +1000,8 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
         rows_total += np;
     }
     const size_t o_segs = A.push_vec(segs), o_qbs = A.push_vec(qbs);
-    A.upload(e.sa);
-    cudaStream_t st = e.sa;
+    A.upload(e.su);
+    cudaStream_t st = e.su;  // admission prefill: whole GPU (host-synchronised below)
     for (int i = 0; i < n; ++i)
         OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_page_table + static_cast<size_t>(slots[i]) * e.max_pages,
                                         A.at<int32_t>(o_rows) + static_cast<size_t>(i) * e.max_pages,
@@ -1446,7 +1567,7 @@ __global__ void add_into(float* __restrict__ dst, const float* __restrict__ src,
 template <class T>
 void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hparams& hp,
                      oppo_ppo_stats& st_out) {
-    cudaStream_t st = e.sa;
+    cudaStream_t st = e.su;  // the update runs between steps: whole GPU
     ActorSms actor_sms(e);
     cudaEvent_t t0, t1;
     OPPO_CUDA_CHECK(cudaEventCreate(&t0));

@@ -19,6 +19,7 @@
 #include "kernels/model.cuh"
 #include "kernels/attn_mma.cuh"
 #include "kernels/attn_dec.cuh"
+#include "kernels/decode_mega.cuh"
 #include "oppo/oppo.h"
 
 namespace oppo {
@@ -141,6 +142,7 @@ struct Engine {
     int prefill_rows = 8192;
     int qblock = 32;  // queries per prefill attention block (bf16: rows = queries x G <= 64)
     cudaStream_t sa = nullptr, ss = nullptr;
+    cudaStream_t su = nullptr;  // admission prefill + PPO update: whole GPU (== sa without a partition)
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr,
                 ev_loop0 = nullptr;
@@ -152,7 +154,13 @@ struct Engine {
     int attn_per_sm = 4;       // target decode attention CTAs per SM
     int attn_max_split = 0;
     int debug_skip = 0;
-    bool attn_fused = true;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
+    bool attn_fused = true;
+    // persistent decode kernel (decode_mega.cuh) for batches <= mega_max_rows
+    int mega_max_rows = 256;
+    mega::LayerP* d_mega_layers = nullptr;
+    unsigned* d_mega_bar = nullptr;
+    float* d_mega_aws = nullptr;
+    int* d_mega_acnt = nullptr;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
     int dec_qkv_max = 96;      // largest batch for which qkv uses the swap-AB decode GEMM
     int dec_gu_max = 64;       // ... gate|up
     int dec_res_max = 128;     // ... O and down (down always: K >= 2048)
@@ -193,6 +201,8 @@ int gemm_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int 
 int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int ldx, const void* wt,
                   int N, int ldw, int mode, void* y, int ldy, const float* bias, float* ws,
                   size_t ws_floats, int num_sms, bool pdl);
+const CUtensorMap& cached_map_pub(Engine* e, const void* ptr, int rows, int cols, int ld, int box_rows,
+                                  CUtensorMap& scratch);
 CUtensorMap make_tma_2d(const void* ptr, int rows, int cols, int ld, int box_rows);
 int gemm_logit_tiles(int dtype, int N);  // partial tiles per row of an EPI_LOGITS GEMM
 void gemm_with_params(int dtype, int M, int N, int K, const void* x, const void* w,

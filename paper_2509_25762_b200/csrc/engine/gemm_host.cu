@@ -71,6 +71,11 @@ static const CUtensorMap& cached_map(Engine* e, const void* ptr, int rows, int c
     return it->second;
 }
 
+const CUtensorMap& cached_map_pub(Engine* e, const void* ptr, int rows, int cols, int ld, int box_rows,
+                                  CUtensorMap& scratch) {
+    return cached_map(e, ptr, rows, cols, ld, box_rows, scratch);
+}
+
 int gemm_logit_tiles(int, int N) { return (N + kSampleBlock - 1) / kSampleBlock; }
 
 // x: [M, K] (ld ldx), w: [N, K] (ld ldw).  bf16: 128-token tiles (A operand,
