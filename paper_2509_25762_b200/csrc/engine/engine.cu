@@ -476,6 +476,7 @@ void mega_setup(Engine& e) {
     e.d_mega_layers = static_cast<mega::LayerP*>(dalloc(lp.size() * sizeof(mega::LayerP)));
     OPPO_CUDA_CHECK(cudaMemcpy(e.d_mega_layers, lp.data(), lp.size() * sizeof(mega::LayerP),
                                cudaMemcpyHostToDevice));
+    if (e.mega_trace) e.mega_trace_buf = static_cast<unsigned long long*>(dalloc(8 * (7 * d.n_layers + 2)));
     e.d_mega_bar = static_cast<unsigned*>(dalloc(64));
     OPPO_CUDA_CHECK(cudaMemset(e.d_mega_bar, 0, 64));
     const size_t rows = static_cast<size_t>(e.S + 16) * d.n_kv_heads;
@@ -514,31 +515,45 @@ int mega_launch_hd(Engine& e, Model& m, Work& w, cudaStream_t st, int R) {
     a.slot = w.meta.slot;
     a.pos = w.meta.pos;
     const int G = w.sms;  // one CTA per SM of the actor partition
-    const int Ns[4] = {a.qkvw, a.D, 2 * a.F, a.D}, Ks[4] = {a.D, a.qw, a.D, a.F};
-    for (int g = 0; g < 4; ++g) {
-        const int tiles = (Ns[g] + 127) / 128, kbt = Ks[g] / 64;
-        int sp = g == mega::W_GU ? 1 : std::max(1, std::min(kbt, G / tiles));
-        while (sp > 1 && static_cast<size_t>(sp) * R * Ns[g] > w.gemm_ws_floats) --sp;
-        a.kbps[g] = (kbt + sp - 1) / sp;
-        a.sp[g] = (kbt + a.kbps[g] - 1) / a.kbps[g];
-    }
-    a.att_sp = std::max(1, std::min(4, G / std::max(1, R * a.KV)));
     a.stage_bytes = dec::kWBytes + a.Mp * 128;
     const int attn_smem = AttnDecCfg<HD>::SMEM;
-    const int budget = 227 * 1024 - 1024 - attn_smem - 512;
+    const int budget = 225 * 1024 - 1024 - attn_smem - 512;  // + static smem < the 227 KB opt-in
     a.stages = std::max(1, std::min(8, budget / a.stage_bytes));
+    // K split per GEMM.  qkv and O: one pipeline's worth of k blocks per item,
+    // so an item's weights are entirely prefetched during the preceding
+    // attention / norm phase and the consumer folds few partials.  down: split
+    // across the grid (its weights stream right after the gate|up barrier).
+    // gate|up: unsplit (SwiGLU needs the full sum).  OPPO_MEGA_KBPS_* override.
+    const int Ns[4] = {a.qkvw, a.D, 2 * a.F, a.D}, Ks[4] = {a.D, a.qw, a.D, a.F};
+    const char* env_k[4] = {"OPPO_MEGA_KBPS_QKV", "OPPO_MEGA_KBPS_O", "OPPO_MEGA_KBPS_GU", "OPPO_MEGA_KBPS_DN"};
+    for (int g = 0; g < 4; ++g) {
+        const int tiles = (Ns[g] + 127) / 128, kbt = Ks[g] / 64;
+        int kbps;
+        if (g == mega::W_GU) kbps = kbt;
+        else if (g == mega::W_DN) kbps = (kbt + std::max(1, G / tiles) - 1) / std::max(1, G / tiles);
+        else kbps = std::min(kbt, a.stages);
+        kbps = std::max(1, std::min(kbt, env_int(env_k[g], kbps)));
+        while (static_cast<size_t>((kbt + kbps - 1) / kbps) * R * Ns[g] > w.gemm_ws_floats) ++kbps;
+        a.kbps[g] = kbps;
+        a.sp[g] = (kbt + kbps - 1) / kbps;
+    }
+    a.att_sp = std::max(1, std::min(4, env_int("OPPO_MEGA_ATT_SP", 1)));
     a.attn_off = a.stages * a.stage_bytes;
     int cols = 32;
     while (cols < a.Mp) cols *= 2;
     a.tmem_cols = cols;
     a.first_np = 0;
+    a.trace = nullptr;
+    if (e.mega_trace) a.trace = e.mega_trace_buf;
+    a.barriers_only = e.debug_skip == 255;
+    a.bar_ra = env_int("OPPO_MEGA_BAR_RA", 1);
     a.eps = kRmsEps;
     a.theta = kRopeTheta;
     const int smem = 1024 + a.attn_off + attn_smem + 512;
     static std::once_flag attr;
     std::call_once(attr, [] {
         OPPO_CUDA_CHECK(cudaFuncSetAttribute(mega::decode_layers<HD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
     });
     CUtensorMap s1, s2, s3;
     const CUtensorMap& xh = cached_map_pub(&e, w.h, R, a.D, a.D, a.Mp, s1);
@@ -842,7 +857,10 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         e->wa.sms = e->sms_actor;
         e->ws.sms = e->sms_scorer;
-        e->mega_max_rows = env_int("OPPO_MEGA_MAX_ROWS", 256);
+        // persistent decode kernel: experimental, off by default (measured slower
+        // than the PDL-chained kernels: 2 us per grid barrier x 168, profiles/)
+        e->mega_max_rows = env_int("OPPO_MEGA_MAX_ROWS", 0);
+        e->mega_trace = env_int("OPPO_MEGA_TRACE", 0) != 0;
         if (e->mega_max_rows > 0 && mega_supported(*e, cfg.actor)) mega_setup(*e);
         e->attn_cluster = env_int("OPPO_ATTN_CLUSTER", 1) != 0;
         e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
@@ -1447,6 +1465,17 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     OPPO_CUDA_CHECK(cudaGetLastError());
     e.step_open = false;
 
+    if (e.mega_trace && e.mega_trace_buf) {  // phase times of the last decode iteration
+        const int L = e.models[ACTOR].dims.n_layers;
+        std::vector<unsigned long long> t(7 * L + 1);
+        OPPO_CUDA_CHECK(cudaMemcpy(t.data(), e.mega_trace_buf, t.size() * 8, cudaMemcpyDeviceToHost));
+        double ph[7] = {0};
+        for (int l = 0; l < L; ++l)
+            for (int k = 0; k < 7; ++k) ph[k] += (t[l * 7 + k + 1] - t[l * 7 + k]) * 1e-3;
+        std::fprintf(stderr, "[oppo] mega phases (us, sum over %d layers): norm1 %.1f qkv %.1f attn %.1f o %.1f "
+                     "norm2 %.1f gu %.1f down %.1f total %.1f\n", L, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5],
+                     ph[6], (t[7 * L] - t[0]) * 1e-3);
+    }
     out = plan.outcomes;
     ledger = plan.ledger;
     float ms = 0;

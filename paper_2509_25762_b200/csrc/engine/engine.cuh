@@ -160,7 +160,9 @@ struct Engine {
     mega::LayerP* d_mega_layers = nullptr;
     unsigned* d_mega_bar = nullptr;
     float* d_mega_aws = nullptr;
-    int* d_mega_acnt = nullptr;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
+    int* d_mega_acnt = nullptr;
+    bool mega_trace = false;
+    unsigned long long* mega_trace_buf = nullptr;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
     int dec_qkv_max = 96;      // largest batch for which qkv uses the swap-AB decode GEMM
     int dec_gu_max = 64;       // ... gate|up
     int dec_res_max = 128;     // ... O and down (down always: K >= 2048)

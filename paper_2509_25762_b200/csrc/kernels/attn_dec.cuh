@@ -76,16 +76,16 @@ __global__ void __launch_bounds__(128)
         if (part) {  // split loads issued 4 at a time (one memory round trip per 4 splits)
             float a = 0.f;
             const float* p = part + static_cast<size_t>(r) * width + col;
-            int sp = 0;
-            for (; sp + 4 <= n_part; sp += 4) {
-                const float p0 = p[sp * part_stride], p1 = p[(sp + 1) * part_stride],
-                            p2 = p[(sp + 2) * part_stride], p3 = p[(sp + 3) * part_stride];
-                a += p0;
-                a += p1;
-                a += p2;
-                a += p3;
+            for (int s0 = 0; s0 < n_part; s0 += 8) {  // 8 split loads in flight, split order
+                float pv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) pv[k] = s0 + k < n_part ? __ldcg(p + (s0 + k) * part_stride) : 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (s0 + k >= n_part) break;
+                    a += pv[k];
+                }
             }
-            for (; sp < n_part; ++sp) a += p[sp * part_stride];
             v = tof(fromf<__nv_bfloat16>(a + (bias ? bias[col] : 0.f)));
         } else {
             v = tof(qkv[static_cast<size_t>(r) * width + col]);

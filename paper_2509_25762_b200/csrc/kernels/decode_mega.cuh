@@ -66,6 +66,9 @@ struct Args {
     int stages, stage_bytes, attn_off, tmem_cols;
     int first_np;          // split-K partials pending in ws from before the kernel
     float eps, theta;
+    unsigned long long* trace;  // optional: %globaltimer after every barrier (CTA 0)
+    int barriers_only;          // perf diagnosis: skip all phase work (results garbage)
+    int bar_ra;                 // 1: release/acquire barrier (grid_sync_ra)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -73,6 +76,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // --------------------------------------------------------------- barrier
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -91,6 +100,34 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
+}
+
+// Same barrier with release/acquire atomics instead of full fences: the
+// arrival is an atom.add.release.gpu (orders this CTA's prior writes), the
+// wait an ld.acquire.gpu poll of the generation word.
+__device__ __forceinline__ void grid_sync_ra(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g, old;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+        } else {
+            unsigned cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+            } while (cur == g);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> later TMA reads
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void sync_all(const Args& a) {
+    if (a.bar_ra) grid_sync_ra(a.bar);
+    else grid_sync(a.bar);
 }
 
 // ------------------------------------------------------------ GEMM phase
@@ -273,17 +310,16 @@ static __device__ void norm_phase(const Args& a, const Smem& sm, const float* ga
             if (c >= nv) continue;
             float4 acc = xr[c];
             const float4* pc = reinterpret_cast<const float4*>(a.ws) + static_cast<size_t>(r) * nv + c;
-            int s = 0;
-            for (; s + 4 <= np; s += 4) {
-                const float4 p0 = pc[s * ps], p1 = pc[(s + 1) * ps], p2 = pc[(s + 2) * ps], p3 = pc[(s + 3) * ps];
-                acc.x += p0.x; acc.y += p0.y; acc.z += p0.z; acc.w += p0.w;
-                acc.x += p1.x; acc.y += p1.y; acc.z += p1.z; acc.w += p1.w;
-                acc.x += p2.x; acc.y += p2.y; acc.z += p2.z; acc.w += p2.w;
-                acc.x += p3.x; acc.y += p3.y; acc.z += p3.z; acc.w += p3.w;
-            }
-            for (; s < np; ++s) {
-                const float4 p0 = pc[s * ps];
-                acc.x += p0.x; acc.y += p0.y; acc.z += p0.z; acc.w += p0.w;
+            for (int s0 = 0; s0 < np; s0 += 8) {  // 8 split loads in flight, summed in split order
+                float4 pv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    pv[k] = s0 + k < np ? __ldcg(pc + (s0 + k) * ps) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (s0 + k >= np) break;
+                    acc.x += pv[k].x; acc.y += pv[k].y; acc.z += pv[k].z; acc.w += pv[k].w;
+                }
             }
             if (np > 0) xr[c] = acc;
             v[i] = acc;
@@ -338,16 +374,16 @@ __device__ void attn_phase(const Args& a, const Smem& sm, int layer, int np_qkv)
             const int col = gi < G ? (h * G + gi) * HD + d : gi == G ? (H + h) * HD + d : (H + KV + h) * HD + d;
             const float* pp = a.ws + static_cast<size_t>(r) * width + col;
             float acc = 0.f;
-            int s = 0;
-            for (; s + 4 <= np_qkv; s += 4) {
-                const float p0 = pp[s * pstride], p1 = pp[(s + 1) * pstride], p2 = pp[(s + 2) * pstride],
-                            p3 = pp[(s + 3) * pstride];
-                acc += p0;
-                acc += p1;
-                acc += p2;
-                acc += p3;
+            for (int s0 = 0; s0 < np_qkv; s0 += 8) {  // 8 split loads in flight, split order
+                float pv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) pv[k] = s0 + k < np_qkv ? __ldcg(pp + (s0 + k) * pstride) : 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (s0 + k >= np_qkv) break;
+                    acc += pv[k];
+                }
             }
-            for (; s < np_qkv; ++s) acc += pp[s * pstride];
             fq[gi * HD + d] = tof(fromf<__nv_bfloat16>(acc + bias[col]));
         }
         __syncthreads();
@@ -608,23 +644,41 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0 && lane == 0) prefetch_w(a, sm, p, 0, W_QKV, blockIdx.x);  // before the PDL wait
     pdl_wait();
     int np = a.first_np;
-    for (int l = 0; l < a.L; ++l) {
+    int tix = 1;
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[0] = gtimer();
+    if (a.barriers_only) {
+        int tix = 1;
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[0] = gtimer();
+        for (int k = 0; k < 7 * a.L; ++k) {
+            sync_all(a);
+            if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
+        }
+        np = 0;
+    }
+    for (int l = 0; l < (a.barriers_only ? 0 : a.L); ++l) {
         const LayerP& L = a.layers[l];
         norm_phase(a, sm, L.ln1, np, a.D);
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
         gemm_phase(a, sm, p, tmem, l, W_QKV, &xm_h, DEC_PARTIAL, l, W_O);
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
         attn_phase<HD>(a, sm, l, a.sp[W_QKV]);
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
         gemm_phase(a, sm, p, tmem, l, W_O, &xm_attn, DEC_PARTIAL, l, W_GU);
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
         norm_phase(a, sm, L.ln2, a.sp[W_O], a.D);
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
         gemm_phase(a, sm, p, tmem, l, W_GU, &xm_h, DEC_SWIGLU, l, W_DN);
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
         gemm_phase(a, sm, p, tmem, l, W_DN, &xm_ff, DEC_PARTIAL, l + 1, W_QKV);
         np = a.sp[W_DN];
-        grid_sync(a.bar);
+        sync_all(a);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[tix++] = gtimer();
     }
     pdl_trigger();
     asm volatile("tcgen05.fence::before_thread_sync;");

@@ -201,18 +201,16 @@ __global__ void __launch_bounds__(256)
         float4 a = xr[c];
         const float4* pc = reinterpret_cast<const float4*>(part) + static_cast<size_t>(r) * nv + c;
         const size_t ps = part_stride >> 2;
-        int sp = 0;
-        for (; sp + 4 <= n_part; sp += 4) {
-            const float4 p0 = pc[sp * ps], p1 = pc[(sp + 1) * ps], p2 = pc[(sp + 2) * ps],
-                         p3 = pc[(sp + 3) * ps];
-            a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
-            a.x += p1.x; a.y += p1.y; a.z += p1.z; a.w += p1.w;
-            a.x += p2.x; a.y += p2.y; a.z += p2.z; a.w += p2.w;
-            a.x += p3.x; a.y += p3.y; a.z += p3.z; a.w += p3.w;
-        }
-        for (; sp < n_part; ++sp) {
-            const float4 p0 = pc[sp * ps];
-            a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+        for (int s0 = 0; s0 < n_part; s0 += 8) {  // 8 split loads in flight, summed in split order
+            float4 pv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                pv[k] = s0 + k < n_part ? __ldcg(pc + (s0 + k) * ps) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (s0 + k >= n_part) break;
+                a.x += pv[k].x; a.y += pv[k].y; a.z += pv[k].z; a.w += pv[k].w;
+            }
         }
         if (n_part > 0) xr[c] = a;
         v[i] = a;
