@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "engine.cuh"
@@ -82,6 +83,21 @@ int gemm_logit_tiles(int, int N) { return (N + kSampleBlock - 1) / kSampleBlock;
 // zero-filled past M by TMA) x BN-row weight tiles; BN = 256 for prefill and
 // the lm_head, 64/128 for decode so the grid covers the SMs; split-K when the
 // tile count is still under half the SMs.
+// experimental, off: the 256x256 tile serialises its epilogue with the
+// mainloop at one CTA per SM and measured slower (249 vs 182 us, gate|up at
+// 8192 rows) than two 128x256 CTAs per SM
+static const bool g_tc256 = [] {
+    const char* v = std::getenv("OPPO_TC256");
+    return v && std::atoi(v) != 0;
+}();
+
+// experimental, off: measured 2x slower than the unsplit kernel (cluster
+// co-scheduling of two ~130 KB-smem CTAs costs more than the halved stream)
+static const bool g_dec_pair = [] {
+    const char* v = std::getenv("OPPO_DEC_PAIR");
+    return v && std::atoi(v) != 0;
+}();
+
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
                       const void* wt, int N, int ldw, const EpiParams& ep_in, int dtype,
                       int num_sms, float* ws, size_t ws_floats, int* cnt, int cnt_n) {
@@ -96,6 +112,26 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         if (ldx != K || ldw != K) throw Error(OPPO_ERR_INTERNAL, "SIMT GEMM needs packed rows");
         launch(e && e->pdl, gemm_simt<float>, dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock),
                dim3(128), 0, st, static_cast<const float*>(x), static_cast<const float*>(wt), sh, ep);
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    // Token-rich prefill GEMMs (>= 8 token tiles, not the logits epilogue, the
+    // output wide enough to fill the SMs): 256x256 tiles, one CTA per SM.
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && g_tc256 &&
+        ((M + 255) / 256) * ((N + 255) / 256) >= num_sms) {
+        static std::once_flag attr256;
+        std::call_once(attr256, [] {
+            OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc256,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 tc::Cfg256::SMEM));
+        });
+        sh.splits = 1;
+        sh.kb_per_split = (K + 63) / 64;
+        CUtensorMap s1, s2;
+        const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
+        const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 256, s2);
+        launch(e && e->pdl, tc::gemm_bf16_tc256, dim3((M + 255) / 256, (N + 255) / 256), dim3(128),
+               tc::Cfg256::SMEM, st, mx, mw, sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
@@ -185,8 +221,14 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
             }
         }
     }
+    // SwiGLU: K split over a CTA pair (DSMEM reduce) doubles the CTAs that
+    // stream the weights (gate|up has only N/128 weight tiles)
+    const bool pair = mode == DEC_SWIGLU && s.nbox == 1 && kb_total >= 4 && g_dec_pair &&
+                      tiles * 2 <= 2 * num_sms;
+    if (pair) splits = 2;
     s.kb_per_split = (kb_total + splits - 1) / splits;
     splits = (kb_total + s.kb_per_split - 1) / s.kb_per_split;
+    s.pair = pair ? 1 : 0;
     s.stages = std::max(1, std::min(s.kb_per_split, std::min(8, (200 * 1024) / stage)));
     int cols = 32;
     while (cols < (s.nbox == 2 ? 512 : s.box_rows)) cols *= 2;
@@ -205,7 +247,10 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
     CUtensorMap s1, s2;
     const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 128, s1);
     const CUtensorMap& mx = cached_map(e, x, M, K, ldx, s.box_rows, s2);
-    launch(pdl, dec::gemm_dec, dim3(tiles, splits), dim3(128), smem, st, mw, mx, s);
+    if (pair)
+        launch_cluster(pdl, dim3(1, 2, 1), dec::gemm_dec, dim3(tiles, 2), dim3(128), smem, st, mw, mx, s);
+    else
+        launch(pdl, dec::gemm_dec, dim3(tiles, splits), dim3(128), smem, st, mw, mx, s);
     OPPO_CUDA_CHECK(cudaGetLastError());
     return mode == DEC_PARTIAL ? splits : 1;
 }

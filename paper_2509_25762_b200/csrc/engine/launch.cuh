@@ -24,6 +24,27 @@ inline void launch(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, si
     OPPO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
+// Same, with a thread-block cluster of the given shape.
+template <typename... KArgs, typename... Args>
+inline void launch_cluster(bool pdl, dim3 cl, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                           size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl.x;
+    at[0].val.clusterDim.y = cl.y;
+    at[0].val.clusterDim.z = cl.z;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 2 : 1;
+    OPPO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // Same, with a thread-block cluster of (1, 1, cz) CTAs (cz > 1).
 template <typename... KArgs, typename... Args>
 inline void launch_cluster_z(bool pdl, int cz, void (*kernel)(KArgs...), dim3 grid, dim3 block,

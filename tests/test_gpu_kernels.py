@@ -92,6 +92,25 @@ def test_gemm_swiglu_epilogue():
     assert (y.float() - ref).abs().max().item() < 2e-2 * max(1, ref.abs().max().item())
 
 
+@pytest.mark.parametrize("M,N,K,epi", [(4096, 9728, 896, EPI_SWIGLU), (8192, 4864, 896, EPI_STORE),
+                                       (2304, 5120, 4864, EPI_STORE)])
+def test_gemm_prefill_256x256_tile_vs_torch(M, N, K, epi, monkeypatch):
+    """Token-rich GEMMs: the default path (128x256 tiles) and, where enabled
+    (OPPO_TC256=1, read at library load), the 256x256-tile kernel."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.03).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g) if epi == EPI_STORE else None
+    y = torch.empty(M, N // 2 if epi == EPI_SWIGLU else N, device="cuda", dtype=torch.bfloat16)
+    st = _lib().oppo_k_gemm(1, M, N, K, _ptr(x), _ptr(w), _ptr(b) if b is not None else None, _ptr(y),
+                            epi, _stream())
+    assert st == 0, _lib().oppo_last_error_global()
+    z = x.float() @ w.float().T
+    ref = torch.nn.functional.silu(z[:, 0::2]) * z[:, 1::2] if epi == EPI_SWIGLU else z + b
+    err = (y.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
 # decode GEMM (swap-AB tcgen05, gemm_dec.cuh): partial sums over splits, SwiGLU, store+bias
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 1152, 896), (40, 896, 896), (64, 896, 4864),
                                    (129, 384, 256), (256, 896, 4864), (282, 1152, 896),

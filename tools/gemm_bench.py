@@ -13,6 +13,9 @@ SHAPES = [("qkv", 1152, 896, 24, 0), ("o", 896, 896, 24, 1), ("gate|up", 9728, 8
           ("down", 896, 4864, 24, 1), ("lm_head", 151936, 896, 3, 3)]
 if os.environ.get("DEC", "1") == "1":  # decode GEMM (gemm_dec): 16 partials, 17 SwiGLU
     SHAPES = [(n, N, K, c, {0: 16, 1: 16, 2: 17}.get(e, e)) for n, N, K, c, e in SHAPES]
+if os.environ.get("PREFILL") == "1":  # scorer prefill pass shapes (token-tiled kernels)
+    SHAPES = [("qkv", 1152, 896, 4, 0), ("o", 896, 896, 4, 1), ("gate|up", 9728, 896, 4, 2),
+              ("down", 896, 4864, 4, 1)]
 Ms = [int(x) for x in os.environ.get("MS", "16,64,128,282").split(",")]
 tot = {}
 for M in Ms:
