@@ -42,6 +42,7 @@ def ref():
             "ref_tuner_replay": (i32, [P(i32), i32, i32, P(i32), P(dbl), i32, P(i32)]),
             "ref_run_seed": (i32, [P(abi.RunConfig), u64, P(abi.StepRecord), P(i32), P(i32)]),
             "ref_run_seeds_parallel": (i32, [P(abi.RunConfig), P(u64), i32, P(i64)]),
+            "ref_write_outputs": (i32, [P(abi.RunConfig), P(u64), i32, C.c_char_p]),
             "ref_trace_seed": (i32, [P(abi.RunConfig), u64, P(abi.StepRecord), P(i32), P(i64),
                                      P(abi.SeqState), i32, P(i32)]),
             "ref_compute_gae": (i32, [P(dbl), P(dbl), i32, dbl, dbl, P(dbl)]),
@@ -111,6 +112,12 @@ def run_seed(cfg, seed):
     n, comp = C.c_int32(), C.c_int32()
     rcheck(ref().ref_run_seed(C.byref(cfg), seed, recs, C.byref(n), C.byref(comp)))
     return list(recs[:n.value]), bool(comp.value)
+
+
+def write_outputs(cfg, seeds, out_dir):
+    """rlpipe::run_experiment_in_memory + write_outputs into out_dir."""
+    arr = (C.c_uint64 * len(seeds))(*seeds)
+    rcheck(ref().ref_write_outputs(C.byref(cfg), arr, len(seeds), str(out_dir).encode()))
 
 
 def trace_seed(cfg, seed, buf_cap=0):

@@ -11,6 +11,7 @@
 // (driver.cpp:103-195) that records selected ids, validated in the tests
 // against rlpipe::run_seed's own StepRecords.
 #include <algorithm>
+#include <filesystem>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -307,6 +308,18 @@ int ref_run_seed(const oppo_run_config* cfg, uint64_t seed, oppo_step_record* re
         for (size_t i = 0; i < run.steps.size(); ++i) fill_record(recs[i], run.steps[i]);
         *n_recs = static_cast<int>(run.steps.size());
         *complete = run.complete;
+    });
+}
+
+// rlpipe::run_experiment_in_memory + write_outputs (driver.cpp:228-350):
+// steps_<seed>.csv, tuner_<seed>.csv and summary.json of the reference, for
+// the run-output compatibility tests.
+int ref_write_outputs(const oppo_run_config* cfg, const uint64_t* seeds, int n_seeds, const char* dir) {
+    return guard([&] {
+        RunConfig config = to_ref(*cfg);
+        config.seeds.assign(seeds, seeds + n_seeds);
+        const auto exp = run_experiment_in_memory(config);
+        write_outputs(exp, std::filesystem::path(dir));
     });
 }
 

@@ -295,3 +295,40 @@ def test_persistent_decode_kernel_vs_oracle_and_multi_kernel_path():
         agree = a["tokens"][:n] == b["tokens"][:n]
         k = int(np.argmin(agree)) if not agree.all() else n
         assert np.max(np.abs(a["old_lp"][:k] - b["old_lp"][:k]), initial=0.0) < 0.05
+
+
+def test_gpu_tuner_on_measured_step_time_replays(tmp_path):
+    """the chunk-size tuner (chunking.cpp:61-107) fed the GPU's
+    measured step time.  Replaying the recorded (candidate, step_us) pairs
+    through the tuner reproduces every chunk size the run used after its
+    exploration steps; the run's outputs are written in the reference's
+    formats (steps/tuner CSV, summary.json)."""
+    from paper_2509_25762_b200 import outputs
+    cfg = S.default_config(mode=abi.RUN_TUNE, steps=14, batch_size=8, prompt_len=8, delta_init=2,
+                           delta_max=4, controller=abi.DELTA_FIXED, proxy_kind=0, chunk_size=16,
+                           tune_chunks=1, chunk_candidates=[8, 16, 32], retune_period=7,
+                           lengths_kind=abi.LEN_LOGNORMAL, lengths_mu_log=3.5,
+                           lengths_sigma_log=0.6, lengths_cap=64, latency_decode_per_token=1,
+                           latency_prefill_per_token=0, latency_reward_residual=0,
+                           latency_placement=1)
+    eng = Engine("tiny", dtype=abi.DTYPE_BF16, max_slots=16, max_prompt_len=8,
+                 max_response_len=64, sample_seed=SAMPLE_SEED)
+    recs, _ = eng.run_seed(cfg, 3)
+    eng.close()
+    assert len(recs) == cfg.steps and all(r.step_us > 0 for r in recs)
+    rows = outputs.tuner_rows(cfg, recs, measure="us")
+    assert [c for _, c, _, _ in rows] == [8, 16, 32, 8, 16, 32]  # ascending exploration per period
+    chosen_after = {}
+    for step, _, _, ch in rows:
+        chosen_after[step] = ch
+    current, by_step = 8, {}
+    for r in recs:
+        if r.step in chosen_after:
+            current = chosen_after[r.step]
+        elif r.step % cfg.retune_period >= 3:
+            by_step[r.step] = current
+    assert by_step and all(recs[s].chunk_size == c for s, c in by_step.items())
+    run = dict(seed=3, records=recs, complete=True, error="")
+    outputs.write_outputs(cfg, [run], [run], tmp_path)
+    assert (tmp_path / "steps_3.csv").read_text().startswith("step,wall_ticks,finished")
+    assert (tmp_path / "tuner_3.csv").exists() and (tmp_path / "steps_3_us.csv").exists()
