@@ -332,3 +332,28 @@ def test_gpu_tuner_on_measured_step_time_replays(tmp_path):
     outputs.write_outputs(cfg, [run], [run], tmp_path)
     assert (tmp_path / "steps_3.csv").read_text().startswith("step,wall_ticks,finished")
     assert (tmp_path / "tuner_3.csv").exists() and (tmp_path / "steps_3_us.csv").exists()
+
+
+def test_7b_actor_15b_scorers_width_bf16_vs_oracle():
+    """BASELINE configs 3-5 pair a wide actor with smaller scorers: a 7B-width
+    actor (d=3584, 28 q / 4 kv heads, head_dim 128, SwiGLU 18944, untied
+    lm_head) with 1.5B-width reward / critic / reference (d=1536, 12 / 2
+    heads, SwiGLU 8960), 2 layers each, 1024-token vocabulary: decode (head_dim
+    128, G=7 tensor-core attention, decode GEMMs at d=3584) and the scorers'
+    chunked prefill against the fp64 oracle."""
+    actor = dict(n_layers=2, d_model=3584, n_heads=28, n_kv_heads=4, head_dim=128, d_ff=18944,
+                 vocab=1024, tied=0)
+    scorer = dict(n_layers=2, d_model=1536, n_heads=12, n_kv_heads=2, head_dim=128, d_ff=8960,
+                  vocab=1024, tied=1)
+    P, C = 16, 16
+    lens = [30, 45, 12, 38]
+    eng = Engine(actor, scorer, scorer, scorer, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P,
+                 max_response_len=48, sample_seed=SAMPLE_SEED)
+    st = fresh_states(len(lens), P, lens)
+    eng.admit(st)
+    eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+    orc = oracles(eng)
+    for s in st[:3]:
+        check_rollout(eng, orc, s["id"], P, tol_lp=0.2, tol_val=0.25, margin_tol=0.2,
+                      strict_tokens=False)
+    eng.close()
