@@ -292,3 +292,80 @@ void gemm_with_params(int dtype, int M, int N, int K, const void* x, const void*
 }
 
 }  // namespace oppo
+
+// ------------------------------------------------------------------------
+// TMA streaming probe (perf diagnosis, tools/tma_probe.py): each CTA streams
+// `tiles` boxes of [box_rows x 64] bf16 from a row-major matrix through a ring
+// of `stages` shared-memory buffers with mbarrier completion, no compute.
+namespace oppo {
+namespace probe {
+__global__ void __launch_bounds__(32) tma_stream(const __grid_constant__ CUtensorMap map, int rows, int kb_total,
+                                                 int per_cta, int stages, int box_bytes, unsigned* sink) {
+    extern __shared__ uint8_t sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + stages * box_bytes);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) tc::mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    const int row_tiles = rows / (box_bytes / 128);
+    uint32_t phase = 0;
+    int issued = 0, done = 0;
+    const int first = blockIdx.x * per_cta;
+    auto issue = [&](int t) {
+        const int s = t % stages;
+        const int g = first + t;
+        const int rt = g % row_tiles, kb = (g / row_tiles) % kb_total;
+        tc::mbar_expect_tx(&full[s], box_bytes);
+        tc::tma_load_2d(sm + s * box_bytes, &map, &full[s], kb * 64, rt * (box_bytes / 128));
+    };
+    for (; issued < stages && issued < per_cta; ++issued) issue(issued);
+    for (; done < per_cta; ++done) {
+        const int s = done % stages;
+        tc::mbar_wait(&full[s], (done / stages) & 1);
+        if (issued < per_cta) issue(issued++);
+    }
+    (void)phase;
+    if (blockIdx.x == 0) *sink = sm[7];
+}
+}  // namespace probe
+}  // namespace oppo
+
+extern "C" oppo_status oppo_k_tma_probe(int32_t ctas, int32_t stages, int32_t box_rows, int32_t per_cta,
+                                        float* us, float* gbs) {
+    try {
+        const int K = 4096, rows = 16384;  // 128 MB bf16 matrix (> L2)
+        void* buf = nullptr;
+        unsigned* sink = nullptr;
+        OPPO_CUDA_CHECK(cudaMalloc(&buf, static_cast<size_t>(rows) * K * 2));
+        OPPO_CUDA_CHECK(cudaMalloc(&sink, 64));
+        OPPO_CUDA_CHECK(cudaMemset(buf, 0, static_cast<size_t>(rows) * K * 2));
+        const CUtensorMap m = oppo::make_tma_2d(buf, rows, K, K, box_rows);
+        const int box_bytes = box_rows * 128;
+        const int smem = stages * box_bytes + 1024 + 256;
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(oppo::probe::tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        for (int w = 0; w < 2; ++w)
+            oppo::probe::tma_stream<<<ctas, 32, smem>>>(m, rows, K / 64, per_cta, stages, box_bytes, sink);
+        cudaEventRecord(a);
+        const int reps = 5;
+        for (int r = 0; r < reps; ++r)
+            oppo::probe::tma_stream<<<ctas, 32, smem>>>(m, rows, K / 64, per_cta, stages, box_bytes, sink);
+        cudaEventRecord(b);
+        OPPO_CUDA_CHECK(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        *us = ms * 1e3f / reps;
+        *gbs = static_cast<float>(static_cast<double>(ctas) * per_cta * box_bytes / (*us * 1e-6) / 1e9);
+        cudaFree(buf);
+        cudaFree(sink);
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
