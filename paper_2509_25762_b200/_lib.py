@@ -8,7 +8,8 @@ import os
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboppo.so")
+# OPPO_LIB: an alternative build of the same library (A/B perf comparisons)
+LIB_PATH = os.environ.get("OPPO_LIB") or os.path.join(_HERE, "liboppo.so")
 
 _lib = None
 

@@ -421,18 +421,25 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     const auto& d = m.dims;
     const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
     const int base = R * d.n_kv_heads;
+    // split-KV clusters measured slower than one CTA per (row, KV head) with
+    // 4 warps over the context (cluster co-scheduling); OPPO_ATTN_MAX_SPLIT > 1
+    // re-enables them for very long contexts at tiny batches
     int nsp = std::max(1, std::min(cdiv(2 * w.sms, base), Cf::MAX_SPLIT));
-    if (e.attn_max_split > 0) nsp = std::min(nsp, e.attn_max_split);
+    nsp = std::min(nsp, e.attn_max_split > 0 ? e.attn_max_split : 1);
     const dim3 grid(R, d.n_kv_heads, nsp);
     auto* out = static_cast<__nv_bfloat16*>(w.attn);
     const auto* qkv = static_cast<const __nv_bfloat16*>(w.qkv);
     const size_t pstride = static_cast<size_t>(R) * m.qkv_width();
+    // early K/V tile loads help while the grid is under one wave (latency);
+    // with several waves they only add memory traffic to the critical fold
+    const int early = base * nsp <= 2 * w.sms ? 1 : 0;
+    const int smem = early ? Cf::SMEM : Cf::SMEM_ALIAS;
     if (nsp > 1)
-        launch_cluster_z(e.pdl, nsp, attn_dec<HD>, grid, dim3(128), Cf::SMEM, st, part, n_part, pstride, bias,
-                         qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta);
+        launch_cluster_z(e.pdl, nsp, attn_dec<HD>, grid, dim3(128), smem, st, part, n_part, pstride, bias,
+                         qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
     else
-        launch(e.pdl, attn_dec<HD>, grid, dim3(128), Cf::SMEM, st, part, n_part, pstride, bias, qkv, out, kv,
-               layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta);
+        launch(e.pdl, attn_dec<HD>, grid, dim3(128), smem, st, part, n_part, pstride, bias, qkv, out, kv,
+               layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
     e.launches += 1;
 }
 

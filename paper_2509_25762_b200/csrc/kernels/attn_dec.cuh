@@ -33,9 +33,11 @@ struct AttnDecCfg {
     static constexpr int WARP_BYTES = 2 * 2 * TP * LDS * 2;  // K,V double buffer
     static constexpr int SLOT = 16 * HD + 32;                // merge partial (floats)
     static constexpr int QBYTES = 16 * LDS * 2;
-    // the fp32 q/k/v staging of phase 1 aliases the K/V buffers (free until the tiles load)
-    static constexpr int SMEM = 4 * WARP_BYTES + QBYTES;
-    static_assert(4 * WARP_BYTES >= 18 * HD * 4, "q/k/v staging must fit the K/V buffers");
+    // fp32 q/k/v staging of phase 1 (own region: the first K/V tiles load meanwhile)
+    static constexpr int FQ_BYTES = 18 * HD * 4;
+    static constexpr int SMEM = 4 * WARP_BYTES + QBYTES + FQ_BYTES;  // early-tile launch
+    static constexpr int SMEM_ALIAS = 4 * WARP_BYTES + QBYTES;       // staging aliases K/V
+    static_assert(4 * WARP_BYTES >= FQ_BYTES, "q/k/v staging must fit the K/V buffers");
     // CTAs of a split-KV cluster whose 4 x nsp partials fit rank 0's K/V buffers
     static constexpr int MAX_SPLIT = (4 * WARP_BYTES) / (4 * SLOT * 4) > 8 ? 8
                                                                             : (4 * WARP_BYTES) / (4 * SLOT * 4);
@@ -46,14 +48,16 @@ __global__ void __launch_bounds__(128)
     attn_dec(const float* __restrict__ part, int n_part, size_t part_stride,
              const float* __restrict__ bias, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* out,
              KvView kv, int layer, int n_heads, const int32_t* __restrict__ slot_r,
-             const int32_t* __restrict__ pos_r, int rows, float theta) {
+             const int32_t* __restrict__ pos_r, int rows, float theta, int early_tiles) {
     using namespace am;
     using Cf = AttnDecCfg<HD>;
     constexpr int TP = Cf::TP, LDS = Cf::LDS, NT = TP / 8, DT = HD / 8;
     extern __shared__ __align__(128) uint8_t adsm[];
     uint8_t* kvbuf = adsm;                                                     // 4 warps x K/V x 2
     auto sQ = reinterpret_cast<__nv_bfloat16(*)[LDS]>(adsm + 4 * Cf::WARP_BYTES);  // [16][LDS]
-    float* fq = reinterpret_cast<float*>(adsm);  // [G+2][HD] fp32 staging (aliases kvbuf)
+    // [G+2][HD] fp32 staging: its own region when the first tiles load early,
+    // else aliased onto the (still idle) K/V buffers (smaller launch footprint)
+    float* fq = reinterpret_cast<float*>(early_tiles ? adsm + 4 * Cf::WARP_BYTES + Cf::QBYTES : adsm);
     pdl_trigger();
     pdl_wait();
     const int r = blockIdx.x;
@@ -65,6 +69,31 @@ __global__ void __launch_bounds__(128)
     const int slen = (ctx + nsp - 1) / nsp;
     const int p_begin = min(ctx, z * slen), p_end = min(ctx, p_begin + slen);
     const bool owner = pos >= p_begin && pos < p_end;  // this CTA appends the new k, v
+
+    // K/V tiles of positions before the new token do not depend on this
+    // iteration: each warp issues its first tile now, so the loads overlap the
+    // qkv fold / RoPE / append below (a tile holding `pos` waits for the append)
+    const int lane_ = tid & 31;
+    auto sK = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES);
+    auto sV = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES + 2 * TP * LDS * 2);
+    const __nv_bfloat16* kc = static_cast<const __nv_bfloat16*>(kv.k);
+    const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(kv.v);
+    auto load_tile = [&](int buf, int t0) {
+        constexpr int CHUNKS = TP * HD / 8;  // 16-byte chunks per tensor
+#pragma unroll
+        for (int c = lane_; c < CHUNKS; c += 32) {
+            const int p = c / (HD / 8), e = (c % (HD / 8)) * 8;
+            const int ps = t0 + p;
+            const bool valid = ps < p_end;
+            const size_t base = valid ? kv_index<__nv_bfloat16>(kv, layer, slot, ps, h) + e : 0;
+            cp_async16(&sK[buf][p][e], kc + base, valid);
+            cp_async16(&sV[buf][p][e], vc + base, valid);
+        }
+        cp_async_commit();
+    };
+    const int first = p_begin + warp * TP;
+    const bool early = early_tiles && first < p_end && first + TP <= pos;
+    if (early) load_tile(0, first);
 
     // ---- 1. q (G heads), k, v of this KV group: fold partials, bias, bf16 round
     const int width = (H + 2 * KV) * HD;
@@ -132,31 +161,13 @@ __global__ void __launch_bounds__(128)
         qf[kk][2] = *reinterpret_cast<const uint32_t*>(&sQ[row0][c + 8]);
         qf[kk][3] = *reinterpret_cast<const uint32_t*>(&sQ[row1][c + 8]);
     }
-    auto sK = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES);
-    auto sV = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES + 2 * TP * LDS * 2);
     const float scale = rsqrtf(static_cast<float>(HD)) * 1.4426950408889634f;  // exp2 domain
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
     float o[DT][4];
 #pragma unroll
     for (int d = 0; d < DT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
-    const __nv_bfloat16* kc = static_cast<const __nv_bfloat16*>(kv.k);
-    const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(kv.v);
-    auto load_tile = [&](int buf, int t0) {
-        constexpr int CHUNKS = TP * HD / 8;  // 16-byte chunks per tensor
-#pragma unroll
-        for (int c = lane; c < CHUNKS; c += 32) {
-            const int p = c / (HD / 8), e = (c % (HD / 8)) * 8;
-            const int ps = t0 + p;
-            const bool valid = ps < p_end;
-            const size_t base = valid ? kv_index<__nv_bfloat16>(kv, layer, slot, ps, h) + e : 0;
-            cp_async16(&sK[buf][p][e], kc + base, valid);
-            cp_async16(&sV[buf][p][e], vc + base, valid);
-        }
-        cp_async_commit();
-    };
     int buf = 0;
-    const int first = p_begin + warp * TP;
-    if (first < p_end) load_tile(0, first);
+    if (!early && first < p_end) load_tile(0, first);
     for (int t0 = first; t0 < p_end; t0 += 4 * TP) {
         if (t0 + 4 * TP < p_end) {
             load_tile(buf ^ 1, t0 + 4 * TP);
