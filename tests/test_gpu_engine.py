@@ -254,8 +254,8 @@ def test_gqa_05b_width_bf16_vs_oracle():
     eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
     orc = oracles(eng)
     for s in st:
-        check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.1, margin_tol=0.2,
-                      strict_tokens=False)
+        check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.2, margin_tol=0.2,
+                      strict_tokens=False)  # bf16 reward/value heads at d=896: ~0.1 absolute
     eng.close()
 
 
