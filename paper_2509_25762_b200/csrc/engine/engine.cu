@@ -876,7 +876,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_fused = env_int("OPPO_ATTN_FUSED", 1) != 0;
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
-        e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 128);
+        e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 192);
         e->nccl = cfg.nccl_comm;
         e->pdl = cfg.use_graphs != 0 && env_int("OPPO_PDL", 1) != 0;
         OPPO_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -165,7 +165,7 @@ struct Engine {
     unsigned long long* mega_trace_buf = nullptr;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
     int dec_qkv_max = 96;      // largest batch for which qkv uses the swap-AB decode GEMM
     int dec_gu_max = 64;       // ... gate|up
-    int dec_res_max = 128;     // ... O and down (down always: K >= 2048)
+    int dec_res_max = 192;     // ... O and down (down always: K >= 2048)
 
     std::map<TmaKey, CUtensorMap> tma_cache;
     std::mutex tma_mu;  // guards tma_cache (decode and scorer launches come from two threads)

@@ -98,6 +98,12 @@ static const bool g_dec_pair = [] {
     return v && std::atoi(v) != 0;
 }();
 
+// cost-model latency (ns) of one fold round trip in the consuming kernel
+static const double g_fold_ns = [] {
+    const char* v = std::getenv("OPPO_DEC_FOLD_NS");
+    return v ? std::atof(v) : 400.0;  // measured: -8% decode iteration at 16 rows, neutral above
+}();
+
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
                       const void* wt, int N, int ldw, const EpiParams& ep_in, int dtype,
                       int num_sms, float* ws, size_t ws_floats, int* cnt, int cnt_n) {
@@ -213,8 +219,9 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
             const int se = (kb_total + kbps - 1) / kbps;
             if (static_cast<size_t>(se) * M * N > ws_floats) break;
             const int waves = (tiles * se + num_sms - 1) / num_sms;
+            // + the consumer's fold: one dependent L2 round trip per 8 splits
             const double t = waves * (kbps * static_cast<double>(stage) / 60.0) +
-                             se * static_cast<double>(M) * N * 8.0 / 8000.0;
+                             se * static_cast<double>(M) * N * 8.0 / 8000.0 + ((se + 7) / 8) * g_fold_ns;
             if (t < best - 1e-9) {
                 best = t;
                 splits = se;
