@@ -238,6 +238,40 @@ def cpu_baseline(wl, budget_s=12.0):
         return {"value": None, "error": str(ex)[:200]}
 
 
+def neural_port_baseline(wl, tokens=8):
+    """The same neural workload on the host: the C oracle's fp64 forward
+    (oracle/oppo_oracle.c, single thread) of the 0.5B-shaped model over a
+    bounded sample of `tokens` tokens, projected to samples/s for this
+    workload: each sample needs its prompt + mean response through the actor
+    (decode with a KV cache costs one forward pass of the sequence) and the
+    three scorers.  Weight values do not change the timing (zeros)."""
+    try:
+        from oracle import oracle as O
+        from paper_2509_25762_b200.engine import SHAPES
+        d = dict(SHAPES[wl["actor"]])
+        L, D, F, V = d["n_layers"], d["d_model"], d["d_ff"], d["vocab"]
+        qkv = (d["n_heads"] + 2 * d["n_kv_heads"]) * d["head_dim"]
+        q = d["n_heads"] * d["head_dim"]
+        z = np.zeros
+        w = {"embed": z((V, D), np.float32), "lm_head": z((V, D), np.float32),
+             "final_norm": z(D, np.float32), "ln1": [z(D, np.float32)] * L,
+             "wqkv": [z((qkv, D), np.float32)] * L, "bqkv": [z(qkv, np.float32)] * L,
+             "wo": [z((D, q), np.float32)] * L, "ln2": [z(D, np.float32)] * L,
+             "wgu": [z((2 * F, D), np.float32)] * L, "wdown": [z((D, F), np.float32)] * L}
+        g = O.GptOracle(d, w)
+        t = time.perf_counter()
+        g.forward(np.arange(tokens, dtype=np.int32) % V)
+        per_tok = (time.perf_counter() - t) / tokens
+        mean_len = float(np.exp(wl["mu"] + wl["sigma"] ** 2 / 2))  # lognormal mean (cap ignored)
+        per_sample = 4 * (wl["prompt_len"] + min(mean_len, wl["cap"])) * per_tok
+        return {"value": round(1.0 / per_sample, 6), "unit": "samples/s", "cores": 1, "kind": "port",
+                "sample": f"oracle_gpt_forward (fp64, scalar C) of the {wl['actor']} model over {tokens} "
+                          f"tokens: {per_tok * 1e3:.1f} ms/token, projected x4 models x "
+                          f"{wl['prompt_len']}+{min(mean_len, wl['cap']):.0f} tokens per sample"}
+    except Exception as ex:
+        return {"value": None, "error": str(ex)[:200]}
+
+
 def ours(args):
     import torch
     rank = int(os.environ.get("RANK", 0))
@@ -328,6 +362,10 @@ def ours(args):
     line["roofline"] = decode_roofline(rec, hbm, peak_src)
     line["kernels"] = {"decode_gemm_gate_up": gemm_microbench(hbm)}
     line["cpu_baseline"] = cpu_baseline(wl) if not args.no_cpu else None
+    if line["cpu_baseline"] is not None and not args.no_cpu:
+        # the reference's CPU path runs its toy tabular policy; the same neural
+        # workload on the host cores, for scale (reported, not the target)
+        line["cpu_baseline"]["neural_port"] = neural_port_baseline(wl)
     line["clocks"] = clocks.summary()
     line["gpu_launches"] = int(sum(r["launches"] for r in rec))
     print(json.dumps(line), flush=True)
