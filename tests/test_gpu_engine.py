@@ -357,3 +357,51 @@ def test_7b_actor_15b_scorers_width_bf16_vs_oracle():
         check_rollout(eng, orc, s["id"], P, tol_lp=0.2, tol_val=0.25, margin_tol=0.2,
                       strict_tokens=False)
     eng.close()
+
+
+def test_edge_cases_single_token_prompts_and_responses_vs_oracle():
+    """Edge cases of the step executor (fp32, strict token parity): one-token
+    prompts (no admission prefill; decode starts from the prompt token),
+    one- and two-token responses (a sequence that finishes on the first
+    iteration and whose only chunk carries the prompt), and mixed prompt
+    lengths in one batch."""
+    P_max, C = 8, 4
+    eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=8, max_prompt_len=P_max,
+                 max_response_len=32, sample_seed=SAMPLE_SEED)
+    states = [dict(id=0, prompt_len=1, target_len=1), dict(id=1, prompt_len=1, target_len=9),
+              dict(id=2, prompt_len=8, target_len=2), dict(id=3, prompt_len=5, target_len=17)]
+    eng.admit(states)
+    outs, led = eng.run_step(states, C, abi.MODE_STREAMED, len(states))
+    plan, _ = S.plan_step(states, C, abi.MODE_STREAMED, len(states))
+    assert [o.as_tuple() for o in outs] == [o.as_tuple() for o in plan]
+    orc = oracles(eng)
+    for s in states:
+        check_rollout(eng, orc, s["id"], s["prompt_len"], tol_lp=1e-3, tol_val=1e-3, margin_tol=1e-3)
+    eng.close()
+
+
+def test_engine_input_errors_map_to_reference_exceptions():
+    """Invalid runtime input raises InputError (rlpipe::InputError,
+    errors.hpp:15-18), invalid configuration ConfigError; the engine stays
+    usable after an input error."""
+    from paper_2509_25762_b200._lib import ConfigError, InputError
+    eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=2, max_prompt_len=8, max_response_len=16,
+                 sample_seed=SAMPLE_SEED)
+    with pytest.raises(InputError):
+        eng.admit([dict(id=0, prompt_len=8, target_len=17)])  # beyond max_response_len
+    with pytest.raises(InputError):
+        eng.admit([dict(id=0, prompt_len=9, target_len=4)])  # beyond max_prompt_len
+    eng.admit([dict(id=0, prompt_len=8, target_len=4)])
+    with pytest.raises(InputError):
+        eng.admit([dict(id=0, prompt_len=8, target_len=4)])  # duplicate id
+    with pytest.raises(InputError):
+        eng.run_step([dict(id=5, prompt_len=8, target_len=4)], 4, abi.MODE_STREAMED, 1)  # not admitted
+    eng.admit([dict(id=1, prompt_len=8, target_len=4)])
+    with pytest.raises(InputError):
+        eng.admit([dict(id=2, prompt_len=8, target_len=4)])  # no free slot
+    st = [dict(id=0, prompt_len=8, target_len=4), dict(id=1, prompt_len=8, target_len=4)]
+    outs, _ = eng.run_step(st, 4, abi.MODE_STREAMED, 2)  # still usable
+    assert all(o.score_ready >= 0 for o in outs)
+    eng.close()
+    with pytest.raises(ConfigError):
+        Engine("tiny", dtype=7)
