@@ -283,6 +283,14 @@ typedef struct oppo_model_dims {
 
 enum { OPPO_DTYPE_F32 = 0, OPPO_DTYPE_BF16 = 1 };
 
+/* Host-provided sum-allreduce used instead of NCCL when nccl_comm is NULL and
+ * world > 1 (e.g. a gloo process group in tests, or another transport):
+ * reduce `count` elements (dtype 0 f32, 1 f64) of the DEVICE buffer in place
+ * across ranks; work already enqueued on `stream` must be visible first.
+ * Returns 0 on success. */
+typedef int32_t (*oppo_allreduce_fn)(void* ctx, void* device_buf, int64_t count, int32_t dtype,
+                                     void* stream);
+
 typedef struct oppo_engine_cfg {
     oppo_model_dims actor;
     oppo_model_dims reward;
@@ -305,6 +313,8 @@ typedef struct oppo_engine_cfg {
     int32_t scorer_sms;       /* fixed SM partition: SMs for the scorer stream (green
                                  contexts, multiple of 8), the rest run the actor; 0 = shared */
     void* nccl_comm;          /* ncclComm_t or NULL (single GPU)       */
+    oppo_allreduce_fn allreduce; /* used when nccl_comm is NULL and world > 1 */
+    void* allreduce_ctx;
 } oppo_engine_cfg;
 
 typedef struct oppo_engine oppo_engine;

@@ -114,7 +114,8 @@ class EngineCfg(C.Structure):
                 ("max_response_len", C.c_int32), ("page_size", C.c_int32),
                 ("kv_pages", C.c_int32), ("carry_granularity", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("use_graphs", C.c_int32),
-                ("train_heads", C.c_int32), ("scorer_sms", C.c_int32), ("nccl_comm", C.c_void_p)]
+                ("train_heads", C.c_int32), ("scorer_sms", C.c_int32), ("nccl_comm", C.c_void_p),
+                ("allreduce", C.c_void_p), ("allreduce_ctx", C.c_void_p)]
 
 
 class PpoStats(C.Structure):

@@ -1600,6 +1600,19 @@ __global__ void add_into(float* __restrict__ dst, const float* __restrict__ src,
             throw ::oppo::Error(OPPO_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
     } while (0)
 
+// Sum-allreduce of a device buffer across the data-parallel ranks: NCCL when
+// the engine has a communicator, else the host-provided callback.
+void dp_allreduce(Engine& e, void* buf, int64_t count, bool f64, cudaStream_t st) {
+    if (e.nccl) {
+        OPPO_NCCL_CHECK(ncclAllReduce(buf, buf, static_cast<size_t>(count), f64 ? ncclDouble : ncclFloat,
+                                      ncclSum, static_cast<ncclComm_t>(e.nccl), st));
+        return;
+    }
+    if (!e.cfg.allreduce) internal_error("data-parallel update without a communicator");
+    if (e.cfg.allreduce(e.cfg.allreduce_ctx, buf, count, f64 ? 1 : 0, st) != 0)
+        throw Error(OPPO_ERR_NCCL, "host allreduce callback failed");
+}
+
 template <class T>
 void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hparams& hp,
                      oppo_ppo_stats& st_out) {
@@ -1672,7 +1685,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     // call: whitening uses the global moments, the token mean of the
     // objective / gradients the global token count, and every rank's Delta
     // controller the global mean reward.
-    const bool dp = e.nccl != nullptr && e.cfg.world > 1;
+    const bool dp = e.cfg.world > 1 && (e.nccl != nullptr || e.cfg.allreduce != nullptr);
     const int mb = std::min(1024, std::max(1, cdiv(N, 256)));
     double* stats = nullptr;
     double n_glob = N, score_glob = 0, samples_glob = n;
@@ -1686,8 +1699,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         const double nn = n;
         OPPO_CUDA_CHECK(cudaMemcpyAsync(d_stats + 6, &nn, 8, cudaMemcpyHostToDevice, st));
         OPPO_CUDA_CHECK(cudaMemcpyAsync(d_stats + 4, d_stats + 6, 8, cudaMemcpyDeviceToDevice, st));
-        OPPO_NCCL_CHECK(ncclAllReduce(d_stats, d_stats, 5, ncclDouble, ncclSum,
-                                      static_cast<ncclComm_t>(e.nccl), st));
+        dp_allreduce(e, d_stats, 5, true, st);
         double g[5];
         OPPO_CUDA_CHECK(cudaMemcpyAsync(g, d_stats, 5 * 8, cudaMemcpyDeviceToHost, st));
         OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -1756,8 +1768,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
             gemm_run(e, w, st, e.g_buf, V, cp, cp, e.ht_buf, Da, cp, eg);
         }
         if (dp) {  // gradient allreduce (sum: every rank's dObj already carries 1/N_global)
-            OPPO_NCCL_CHECK(ncclAllReduce(e.g_lm, e.g_lm, nw, ncclFloat, ncclSum,
-                                          static_cast<ncclComm_t>(e.nccl), st));
+            dp_allreduce(e, e.g_lm, static_cast<int64_t>(nw), false, st);
             add_into<<<cdiv(static_cast<int64_t>(nw), 256), 256, 0, st>>>(actor.lm_master, e.g_lm,
                                                                         static_cast<int64_t>(nw));
         }
@@ -1766,8 +1777,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         // critic value head: w -= vlr * (1/N) sum (V - R) h
         value_head_grad<T><<<cdiv(Dc, 128), 128, 0, st>>>(d_hc, Dc, N, d_vtok, d_ret, e.vgrad, inv_n_glob);
         if (dp)
-            OPPO_NCCL_CHECK(ncclAllReduce(e.vgrad, e.vgrad, Dc, ncclFloat, ncclSum,
-                                          static_cast<ncclComm_t>(e.nccl), st));
+            dp_allreduce(e, e.vgrad, Dc, false, st);
         head_sgd<<<cdiv(Dc, 128), 128, 0, st>>>(critic.head, e.vgrad, Dc,
                                                 static_cast<float>(hp.value_learning_rate));
     }

@@ -45,7 +45,7 @@ class Engine:
     def __init__(self, actor="tiny", reward=None, critic=None, ref=None, dtype=abi.DTYPE_BF16,
                  max_slots=16, max_prompt_len=8, max_response_len=64, page_size=64, kv_pages=0,
                  weight_seed=1, sample_seed=2, carry=abi.CARRY_CHUNK, train_heads=0, device=0,
-                 nccl_comm=None, rank=0, world=1, use_graphs=1, scorer_sms=0):
+                 nccl_comm=None, rank=0, world=1, use_graphs=1, scorer_sms=0, allreduce=None):
         cfg = abi.EngineCfg()
         cfg.actor = dims(actor)
         cfg.reward = dims(reward or actor)
@@ -66,6 +66,16 @@ class Engine:
         cfg.use_graphs = use_graphs
         cfg.scorer_sms = scorer_sms
         cfg.nccl_comm = nccl_comm
+        self._allreduce = None
+        if allreduce is not None:  # host sum-allreduce (count, f64) over a device buffer
+            def _cb(ctx, buf, count, dtype, stream):
+                try:
+                    allreduce(buf, count, bool(dtype), stream)
+                    return 0
+                except Exception:  # reported to the engine as a failed collective
+                    return 1
+            self._allreduce = ALLREDUCE_FN(_cb)
+            cfg.allreduce = C.cast(self._allreduce, C.c_void_p)
         self.cfg = cfg
         self.h = C.c_void_p()
         check(lib().oppo_engine_create(C.byref(cfg), C.byref(self.h)))
@@ -169,6 +179,38 @@ class Engine:
 
 
 NCCL_ID_BYTES = 128
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+
+
+def gloo_device_allreduce():
+    """A host allreduce for oppo_engine_cfg.allreduce over the default
+    torch.distributed (gloo) group: device -> host, all_reduce(SUM), host ->
+    device (for CPU-transport tests of the data-parallel update)."""
+    import torch
+    import torch.distributed as dist
+    cudart = C.CDLL("libcudart.so.12") if _have("libcudart.so.12") else C.CDLL("libcudart.so")
+    cudart.cudaStreamSynchronize.argtypes = [C.c_void_p]
+    cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+
+    def fn(buf, count, f64, stream):
+        t = torch.empty(count, dtype=torch.float64 if f64 else torch.float32)
+        nbytes = count * (8 if f64 else 4)
+        assert cudart.cudaStreamSynchronize(stream) == 0
+        assert cudart.cudaMemcpy(t.data_ptr(), buf, nbytes, 2) == 0  # device -> host
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        assert cudart.cudaMemcpy(buf, t.data_ptr(), nbytes, 1) == 0  # host -> device
+        # a pageable host->device cudaMemcpy may return before its DMA lands, and
+        # the engine's stream is non-blocking: wait for the copy explicitly
+        assert cudart.cudaDeviceSynchronize() == 0
+    return fn
+
+
+def _have(name):
+    try:
+        C.CDLL(name)
+        return True
+    except OSError:
+        return False
 
 
 def nccl_comm_from_torch(rank, world, device):
