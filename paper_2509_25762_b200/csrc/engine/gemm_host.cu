@@ -104,6 +104,16 @@ static const double g_fold_ns = [] {
     return v ? std::atof(v) : 400.0;  // measured: -8% decode iteration at 16 rows, neutral above
 }();
 
+// CTA-pair 256x256 prefill tiles: correct in isolation (tests) and measured
+// down 91 -> 83 us, gate|up 182 -> 180 us at 8192 rows (the operand stream is
+// the limit, ~6 TB/s L2 -> SM), but the full overlapped step hung once with
+// it enabled (clusters inside the scorer green context + PDL chains): off by
+// default, OPPO_TC2SM=1 opts in
+static const bool g_tc2sm = [] {
+    const char* v = std::getenv("OPPO_TC2SM");
+    return v && std::atoi(v) != 0;
+}();
+
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
                       const void* wt, int N, int ldw, const EpiParams& ep_in, int dtype,
                       int num_sms, float* ws, size_t ws_floats, int* cnt, int cnt_n) {
@@ -138,6 +148,25 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 256, s2);
         launch(e && e->pdl, tc::gemm_bf16_tc256, dim3((M + 255) / 256, (N + 255) / 256), dim3(128),
                tc::Cfg256::SMEM, st, mx, mw, sh, ep);
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    // Token-rich prefill GEMMs: CTA-pair 256x256 tiles (cta_group::2)
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && g_tc2sm) {
+        static std::once_flag attr2;
+        std::call_once(attr2, [] {
+            OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 tc::Cfg2Sm::SMEM));
+        });
+        sh.splits = 1;
+        sh.kb_per_split = (K + 63) / 64;
+        CUtensorMap s1, s2;
+        const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
+        const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 128, s2);
+        const int mt2 = (m_tiles + 1) / 2 * 2;  // whole CTA pairs (OOB rows zero-filled)
+        launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm, dim3(mt2, (N + 255) / 256), dim3(128),
+                       tc::Cfg2Sm::SMEM, st, mx, mw, sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
