@@ -874,6 +874,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
         e->debug_skip = env_int("OPPO_DEBUG_SKIP", 0);
         e->attn_fused = env_int("OPPO_ATTN_FUSED", 1) != 0;
+        e->lmhead_dec_max = env_int("OPPO_LMHEAD_DEC_MAX", 32);  // measured crossover ~40 rows
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
         e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 192);
@@ -1253,7 +1254,10 @@ void decode_iteration(Engine& e, int M, cudaStream_t st) {
     ep.targets = nullptr;
     ep.keys = w.meta.key;
     const int D = m.dims.d_model;
-    gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
+    if (std::is_same_v<T, __nv_bfloat16> && M <= e.lmhead_dec_max && D % 64 == 0 && m.dims.vocab % 128 == 0)
+        lmhead_dec_run(e, w, st, w.h, M, D, m.lm_head, m.dims.vocab, w.partials, w.meta.key);
+    else
+        gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
     launch(e.pdl, logits_combine, dim3(cdiv(M, 4)), dim3(128), 0, st, w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, M, w.meta.key,
                                                nullptr, w.meta.slot, w.meta.t, e.d_tok, e.d_old_lp,
                                                e.tok_stride, nullptr, nullptr, e.d_iter);

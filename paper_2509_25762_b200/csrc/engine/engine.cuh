@@ -155,6 +155,7 @@ struct Engine {
     int attn_max_split = 0;
     int debug_skip = 0;
     bool attn_fused = true;
+    int lmhead_dec_max = 32;   // decode lm_head through lmhead_dec.cuh up to this batch (0: off)
     // persistent decode kernel (decode_mega.cuh) for batches <= mega_max_rows
     int mega_max_rows = 256;
     mega::LayerP* d_mega_layers = nullptr;
@@ -205,6 +206,8 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
                   size_t ws_floats, int num_sms, bool pdl);
 const CUtensorMap& cached_map_pub(Engine* e, const void* ptr, int rows, int cols, int ld, int box_rows,
                                   CUtensorMap& scratch);
+void lmhead_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, const void* wt,
+                    int V, float4* partials, const uint64_t* keys);
 CUtensorMap make_tma_2d(const void* ptr, int rows, int cols, int ld, int box_rows);
 int gemm_logit_tiles(int dtype, int N);  // partial tiles per row of an EPI_LOGITS GEMM
 void gemm_with_params(int dtype, int M, int N, int K, const void* x, const void* w,

@@ -9,6 +9,7 @@
 #include "engine.cuh"
 #include "kernels/gemm.cuh"
 #include "kernels/gemm_dec.cuh"
+#include "kernels/lmhead_dec.cuh"
 
 namespace oppo {
 
@@ -289,6 +290,37 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
         launch(pdl, dec::gemm_dec, dim3(tiles, splits), dim3(128), smem, st, mw, mx, s);
     OPPO_CUDA_CHECK(cudaGetLastError());
     return mode == DEC_PARTIAL ? splits : 1;
+}
+
+// Decode lm_head + in-block sampling (lmhead_dec.cuh), <= 128 tokens.
+void lmhead_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, const void* wt,
+                    int V, float4* partials, const uint64_t* keys) {
+    lmh::Shape s{};
+    s.M = M;
+    s.Mp = (M + 15) / 16 * 16;
+    s.N = V;
+    s.K = K;
+    const int stage = lmh::kWBytes + s.Mp * 128;
+    s.stages = std::max(1, std::min(K / 64, (200 * 1024) / stage));
+    int cols = 32;
+    while (cols < 2 * s.Mp) cols *= 2;
+    s.tmem_cols = cols;
+    s.n_tiles = gemm_logit_tiles(OPPO_DTYPE_BF16, V);
+    s.partials = partials;
+    s.keys = keys;
+    const int smem = s.stages * stage + 1024 + 2048;
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(lmh::lmhead_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024));
+    });
+    CUtensorMap s1, s2;
+    const CUtensorMap& mw = cached_map(&e, wt, V, K, K, 256, s1);
+    const CUtensorMap& mx = cached_map(&e, x, M, K, K, s.Mp, s2);
+    launch(e.pdl, lmh::lmhead_dec, dim3((V + 255) / 256), dim3(128), smem, st, mw, mx, s);
+    OPPO_CUDA_CHECK(cudaGetLastError());
+    e.launches += 1;
+    (void)w;
 }
 
 int gemm_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
