@@ -409,13 +409,13 @@ void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
 
 // Decode attention with RoPE + KV append fused (attn_dec.cuh), bf16.  The
 // qkv row comes from the decode GEMM's partials (n_part > 0) or a bf16 row.
-template <int HD>
+template <int HD, int NW>
 void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
                         const float* part, int n_part, const float* bias) {
-    using Cf = AttnDecCfg<HD>;
+    using Cf = AttnDecCfg<HD, NW>;
     static std::once_flag attr;
     std::call_once(attr, [] {
-        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Cf::SMEM));
     });
     const auto& d = m.dims;
@@ -435,10 +435,10 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     const int early = base * nsp <= 2 * w.sms ? 1 : 0;
     const int smem = early ? Cf::SMEM : Cf::SMEM_ALIAS;
     if (nsp > 1)
-        launch_cluster_z(e.pdl, nsp, attn_dec<HD>, grid, dim3(128), smem, st, part, n_part, pstride, bias,
+        launch_cluster_z(e.pdl, nsp, attn_dec<HD, NW>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias,
                          qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
     else
-        launch(e.pdl, attn_dec<HD>, grid, dim3(128), smem, st, part, n_part, pstride, bias, qkv, out, kv,
+        launch(e.pdl, attn_dec<HD, NW>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias, qkv, out, kv,
                layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
     e.launches += 1;
 }
@@ -450,10 +450,20 @@ bool attn_dec_supported(const oppo_model_dims& d) {
 
 void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
                      const float* part, int n_part, const float* bias) {
+    // 8 warps x 16-position tiles (head_dim <= 64) while the grid is within one
+    // wave (measured -90 us per iteration at 16-128 rows), 4 warps x 32 above
+    const bool w8 = e.attn_warps == 8 ||
+                    (e.attn_warps == 0 && R * m.dims.n_kv_heads <= 2 * w.sms);
     switch (m.dims.head_dim) {
-    case 32: attn_dec_launch_hd<32>(e, m, w, st, layer, R, part, n_part, bias); break;
-    case 64: attn_dec_launch_hd<64>(e, m, w, st, layer, R, part, n_part, bias); break;
-    default: attn_dec_launch_hd<128>(e, m, w, st, layer, R, part, n_part, bias); break;
+    case 32:
+        if (w8) attn_dec_launch_hd<32, 8>(e, m, w, st, layer, R, part, n_part, bias);
+        else attn_dec_launch_hd<32, 4>(e, m, w, st, layer, R, part, n_part, bias);
+        break;
+    case 64:
+        if (w8) attn_dec_launch_hd<64, 8>(e, m, w, st, layer, R, part, n_part, bias);
+        else attn_dec_launch_hd<64, 4>(e, m, w, st, layer, R, part, n_part, bias);
+        break;
+    default: attn_dec_launch_hd<128, 4>(e, m, w, st, layer, R, part, n_part, bias); break;
     }
 }
 
@@ -875,6 +885,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->debug_skip = env_int("OPPO_DEBUG_SKIP", 0);
         e->attn_fused = env_int("OPPO_ATTN_FUSED", 1) != 0;
         e->lmhead_dec_max = env_int("OPPO_LMHEAD_DEC_MAX", 32);  // measured crossover ~40 rows
+        e->attn_warps = env_int("OPPO_ATTN_WARPS", 0);  // 0 auto, 4 or 8 forced
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
         e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 192);

@@ -155,6 +155,7 @@ struct Engine {
     int attn_max_split = 0;
     int debug_skip = 0;
     bool attn_fused = true;
+    int attn_warps = 0;        // decode attention warps per CTA (0 auto, 4 or 8)
     int lmhead_dec_max = 32;   // decode lm_head through lmhead_dec.cuh up to this batch (0: off)
     // persistent decode kernel (decode_mega.cuh) for batches <= mega_max_rows
     int mega_max_rows = 256;

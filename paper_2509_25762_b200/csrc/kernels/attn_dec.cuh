@@ -26,38 +26,42 @@
 
 namespace oppo {
 
-template <int HD>
+template <int HD, int NW = 4>
 struct AttnDecCfg {
-    static constexpr int TP = HD >= 128 ? 16 : 32;  // positions per warp tile
+    static constexpr int WARPS = NW;
+    static constexpr int THREADS = 32 * NW;
+    // positions per warp tile (8 warps: half-size tiles, same shared memory)
+    static constexpr int TP = (HD >= 128 || NW == 8) ? 16 : 32;
     static constexpr int LDS = HD + 8;              // padded smem row (elements)
     static constexpr int WARP_BYTES = 2 * 2 * TP * LDS * 2;  // K,V double buffer
     static constexpr int SLOT = 16 * HD + 32;                // merge partial (floats)
     static constexpr int QBYTES = 16 * LDS * 2;
     // fp32 q/k/v staging of phase 1 (own region: the first K/V tiles load meanwhile)
     static constexpr int FQ_BYTES = 18 * HD * 4;
-    static constexpr int SMEM = 4 * WARP_BYTES + QBYTES + FQ_BYTES;  // early-tile launch
-    static constexpr int SMEM_ALIAS = 4 * WARP_BYTES + QBYTES;       // staging aliases K/V
-    static_assert(4 * WARP_BYTES >= FQ_BYTES, "q/k/v staging must fit the K/V buffers");
+    static constexpr int SMEM = NW * WARP_BYTES + QBYTES + FQ_BYTES;  // early-tile launch
+    static constexpr int SMEM_ALIAS = NW * WARP_BYTES + QBYTES;       // staging aliases K/V
+    static_assert(NW * WARP_BYTES >= FQ_BYTES, "q/k/v staging must fit the K/V buffers");
+    static_assert(NW * WARP_BYTES >= NW * (16 * HD + 32) * 4, "warp partials must fit the K/V buffers");
     // CTAs of a split-KV cluster whose 4 x nsp partials fit rank 0's K/V buffers
-    static constexpr int MAX_SPLIT = (4 * WARP_BYTES) / (4 * SLOT * 4) > 8 ? 8
-                                                                            : (4 * WARP_BYTES) / (4 * SLOT * 4);
+    static constexpr int MAX_SPLIT = (NW * WARP_BYTES) / (NW * SLOT * 4) > 8 ? 8
+                                                                              : (NW * WARP_BYTES) / (NW * SLOT * 4);
 };
 
-template <int HD>
-__global__ void __launch_bounds__(128)
+template <int HD, int NW>
+__global__ void __launch_bounds__(32 * NW)
     attn_dec(const float* __restrict__ part, int n_part, size_t part_stride,
              const float* __restrict__ bias, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* out,
              KvView kv, int layer, int n_heads, const int32_t* __restrict__ slot_r,
              const int32_t* __restrict__ pos_r, int rows, float theta, int early_tiles) {
     using namespace am;
-    using Cf = AttnDecCfg<HD>;
-    constexpr int TP = Cf::TP, LDS = Cf::LDS, NT = TP / 8, DT = HD / 8;
+    using Cf = AttnDecCfg<HD, NW>;
+    constexpr int TP = Cf::TP, LDS = Cf::LDS, NT = TP / 8, DT = HD / 8, NTH = Cf::THREADS;
     extern __shared__ __align__(128) uint8_t adsm[];
     uint8_t* kvbuf = adsm;                                                     // 4 warps x K/V x 2
-    auto sQ = reinterpret_cast<__nv_bfloat16(*)[LDS]>(adsm + 4 * Cf::WARP_BYTES);  // [16][LDS]
+    auto sQ = reinterpret_cast<__nv_bfloat16(*)[LDS]>(adsm + NW * Cf::WARP_BYTES);  // [16][LDS]
     // [G+2][HD] fp32 staging: its own region when the first tiles load early,
     // else aliased onto the (still idle) K/V buffers (smaller launch footprint)
-    float* fq = reinterpret_cast<float*>(early_tiles ? adsm + 4 * Cf::WARP_BYTES + Cf::QBYTES : adsm);
+    float* fq = reinterpret_cast<float*>(early_tiles ? adsm + NW * Cf::WARP_BYTES + Cf::QBYTES : adsm);
     pdl_trigger();
     pdl_wait();
     const int r = blockIdx.x;
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(128)
     // ---- 1. q (G heads), k, v of this KV group: fold partials, bias, bf16 round
     const int width = (H + 2 * KV) * HD;
     const int nvals = (G + 2) * HD;
-    for (int i = tid; i < nvals; i += 128) {
+    for (int i = tid; i < nvals; i += NTH) {
         const int gi = i / HD, d = i % HD;
         const int col = gi < G ? (h * G + gi) * HD + d : gi == G ? (H + h) * HD + d : (H + KV + h) * HD + d;
         float v;
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     // RoPE on q heads and k (rotate-half), then q -> sQ (bf16), new k/v -> cache
     const int half = HD / 2;
-    for (int i = tid; i < (G + 1) * half; i += 128) {
+    for (int i = tid; i < (G + 1) * half; i += NTH) {
         const int gi = i / half, d = i % half;
         const float inv_freq = __powf(theta, -2.0f * d / HD);
         float sn, cs;
@@ -142,9 +146,9 @@ __global__ void __launch_bounds__(128)
     }
     if (owner) {
         __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(kv.v) + kv_index<__nv_bfloat16>(kv, layer, slot, pos, h);
-        for (int d = tid; d < HD; d += 128) vc[d] = fromf<__nv_bfloat16>(fq[(G + 1) * HD + d]);
+        for (int d = tid; d < HD; d += NTH) vc[d] = fromf<__nv_bfloat16>(fq[(G + 1) * HD + d]);
     }
-    for (int i = tid; i < (16 - G) * HD; i += 128) sQ[G + i / HD][i % HD] = fromf<__nv_bfloat16>(0.f);
+    for (int i = tid; i < (16 - G) * HD; i += NTH) sQ[G + i / HD][i % HD] = fromf<__nv_bfloat16>(0.f);
     __threadfence_block();
     __syncthreads();  // q in smem; the appended k/v visible to this CTA's tile loads
 
@@ -168,9 +172,9 @@ __global__ void __launch_bounds__(128)
     for (int d = 0; d < DT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     int buf = 0;
     if (!early && first < p_end) load_tile(0, first);
-    for (int t0 = first; t0 < p_end; t0 += 4 * TP) {
-        if (t0 + 4 * TP < p_end) {
-            load_tile(buf ^ 1, t0 + 4 * TP);
+    for (int t0 = first; t0 < p_end; t0 += NW * TP) {
+        if (t0 + NW * TP < p_end) {
+            load_tile(buf ^ 1, t0 + NW * TP);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(128)
         __syncthreads();
         dst = reinterpret_cast<float*>(kvbuf);
     }
-    dst += (z * 4 + warp) * Cf::SLOT;
+    dst += (z * NW + warp) * Cf::SLOT;
 #pragma unroll
     for (int d = 0; d < DT; ++d) {
         const int c = d * 8 + tig * 2;
@@ -279,8 +283,8 @@ __global__ void __launch_bounds__(128)
         __syncthreads();
     }
     const float* bufm = reinterpret_cast<const float*>(kvbuf);
-    const int np = 4 * nsp;
-    for (int e = tid; e < G * HD; e += 128) {
+    const int np = NW * nsp;
+    for (int e = tid; e < G * HD; e += NTH) {
         const int g = e / HD, c = e % HD;
         float mx = -INFINITY;
         for (int sp = 0; sp < np; ++sp) mx = fmaxf(mx, bufm[sp * Cf::SLOT + 16 * HD + g * 2]);
