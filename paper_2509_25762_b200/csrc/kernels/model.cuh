@@ -144,16 +144,21 @@ __global__ void rmsnorm_rows(float* __restrict__ x, const float* __restrict__ w,
         if (c >= nv) break;
         const float4 g = __ldg(reinterpret_cast<const float4*>(w) + c);
         float y[4] = {v[i].x * inv * g.x, v[i].y * inv * g.y, v[i].z * inv * g.z, v[i].w * inv * g.w};
-        T t4[4];
+        __align__(8) T t4[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) t4[k] = fromf<T>(y[k]);
-        if (orow) {
+        if constexpr (sizeof(T) == 2) {  // one 8-byte store per 4 values
+            if (orow) *reinterpret_cast<uint2*>(orow + 4 * c) = *reinterpret_cast<const uint2*>(t4);
+            if (crow) *reinterpret_cast<uint2*>(crow + 4 * c) = *reinterpret_cast<const uint2*>(t4);
+        } else {
+            if (orow) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) orow[4 * c + k] = t4[k];
-        }
-        if (crow) {
+                for (int k = 0; k < 4; ++k) orow[4 * c + k] = t4[k];
+            }
+            if (crow) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) crow[4 * c + k] = t4[k];
+                for (int k = 0; k < 4; ++k) crow[4 * c + k] = t4[k];
+            }
         }
         if (head_w) {
             const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w) + c);
@@ -315,11 +320,13 @@ __global__ void rope_append(const T* __restrict__ qkv, T* q_out, KvView kv, int 
     const int p = pos[r], s = slot[r];
     T* kc = static_cast<T*>(kv.k);
     T* vc = static_cast<T*>(kv.v);
-    for (int i = threadIdx.x; i < (H + KV) * half; i += blockDim.x) {
-        const int head = i / half, d = i % half;
-        const float inv_freq = __powf(theta, -2.0f * d / hd);
-        float sn, cs;
-        sincosf(p * inv_freq, &sn, &cs);
+    // a thread keeps one rotary frequency d for the whole row (blockDim is a
+    // multiple of hd/2): one sincos per thread instead of one per element
+    const int d = threadIdx.x % half, hstep = blockDim.x / half;
+    const float inv_freq = __powf(theta, -2.0f * d / hd);
+    float sn, cs;
+    sincosf(p * inv_freq, &sn, &cs);
+    for (int head = threadIdx.x / half; head < H + KV; head += hstep) {
         const float x1 = tof(src[head * hd + d]);
         const float x2 = tof(src[head * hd + d + half]);
         const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
