@@ -208,7 +208,10 @@ void make_sm_partition(Engine& e, int scorer_sms, int prio_hi, int prio_lo) {
     CUdevResource all{}, grp{}, rest{};
     OPPO_CU_CHECK(driver_fn<GetRes>("cuDeviceGetDevResource")(dev, &all, CU_DEV_RESOURCE_TYPE_SM));
     unsigned int n = 1;
-    OPPO_CU_CHECK(driver_fn<Split>("cuDevSmResourceSplitByCount")(&grp, &n, &all, &rest, 0,
+    // OPPO_SPLIT_FLAGS: CUdevSmResourceSplit_flags (cluster-friendly layout was
+    // tried for CTA-pair GEMMs inside the scorer partition; they hang there)
+    const unsigned flags = static_cast<unsigned>(env_int("OPPO_SPLIT_FLAGS", 0));
+    OPPO_CU_CHECK(driver_fn<Split>("cuDevSmResourceSplitByCount")(&grp, &n, &all, &rest, flags,
                                                                   static_cast<unsigned>(scorer_sms)));
     if (n != 1 || rest.sm.smCount == 0) config_error("SM partition: scorer_sms leaves no actor SMs");
     CUdevResourceDesc ds, da;

@@ -107,12 +107,12 @@ static const double g_fold_ns = [] {
 
 // CTA-pair 256x256 prefill tiles: correct in isolation (tests) and measured
 // down 91 -> 83 us, gate|up 182 -> 180 us at 8192 rows (the operand stream is
-// the limit, ~6 TB/s L2 -> SM), but the full overlapped step hung once with
-// it enabled (clusters inside the scorer green context + PDL chains): off by
-// default, OPPO_TC2SM=1 opts in
-static const bool g_tc2sm = [] {
+// the limit, ~6 TB/s L2 -> SM).  Launched on the whole-GPU update/admission
+// stream it runs fine (OPPO_TC2SM=3); inside the scorer's green-context
+// partition it hangs (OPPO_TC2SM=2, either SM-split layout).  Off by default.
+static const int g_tc2sm = [] {  // 0 off, 1 everywhere, 2 scorer stream only, 3 other streams only
     const char* v = std::getenv("OPPO_TC2SM");
-    return v && std::atoi(v) != 0;
+    return v ? std::atoi(v) : 0;
 }();
 
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
@@ -153,7 +153,9 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         return;
     }
     // Token-rich prefill GEMMs: CTA-pair 256x256 tiles (cta_group::2)
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && g_tc2sm) {
+    const bool scorer_stream = e && st == e->ss;
+    const bool use2 = g_tc2sm == 1 || (g_tc2sm == 2 && scorer_stream) || (g_tc2sm == 3 && !scorer_stream);
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && use2) {
         static std::once_flag attr2;
         std::call_once(attr2, [] {
             OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm,
