@@ -30,8 +30,13 @@ sys.path.insert(0, ROOT)
 METRIC = "PPO samples/sec per step (overlap vs sequential) at 1/2/4/8 B200; roofline %"
 CFG2 = dict(name="cfg2", actor="0.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
             sigma=1.0, cap=1024, chunk=64, delta=26)
+# BASELINE configs[2] shape on one GPU: 1.5B actor + 0.5B scorers (chunk 64, 10% overcommit)
+CFG3 = dict(name="cfg3", actor="1.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
+            sigma=1.0, cap=1024, chunk=64, delta=26)
+WORKLOADS = {}
 TINY = dict(name="cfg1", actor="tiny", scorer="tiny", batch=8, prompt_len=8, mu=3.5, sigma=0.6,
             cap=64, chunk=16, delta=2)
+WORKLOADS.update(cfg1=TINY, cfg2=CFG2, cfg3=CFG3)
 
 
 def peaks():
@@ -288,7 +293,7 @@ def ours(args):
     from paper_2509_25762_b200.engine import Engine, param_count, SHAPES, nccl_comm_from_torch
     comm = nccl_comm_from_torch(rank, world, local) if world > 1 else None
 
-    wl = TINY if args.workload == "cfg1" else CFG2
+    wl = WORKLOADS[args.workload]
     hbm, tflops, peak_src = peaks()
     res = {}
     arms = [("oppo", False)] + ([] if args.no_sequential else [("sequential", True)])
@@ -379,7 +384,7 @@ def reference(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    wl = TINY if args.workload == "cfg1" else CFG2
+    wl = WORKLOADS[args.workload]
     try:
         from oracle import ref as R
         from paper_2509_25762_b200 import scheduler as S
@@ -422,7 +427,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg1"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scorer-sms", type=int, default=64,
