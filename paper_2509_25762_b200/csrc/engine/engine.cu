@@ -456,7 +456,7 @@ void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
     // 8 warps x 16-position tiles (head_dim <= 64) while the grid is within one
     // wave (measured -90 us per iteration at 16-128 rows), 4 warps x 32 above
     const bool w8 = e.attn_warps == 8 ||
-                    (e.attn_warps == 0 && R * m.dims.n_kv_heads <= 2 * w.sms);
+                    (e.attn_warps == 0 && 10 * R * m.dims.n_kv_heads <= e.attn_w8_tenths * w.sms);
     switch (m.dims.head_dim) {
     case 32:
         if (w8) attn_dec_launch_hd<32, 8>(e, m, w, st, layer, R, part, n_part, bias);
@@ -889,6 +889,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_fused = env_int("OPPO_ATTN_FUSED", 1) != 0;
         e->lmhead_dec_max = env_int("OPPO_LMHEAD_DEC_MAX", 32);  // measured crossover ~40 rows
         e->attn_warps = env_int("OPPO_ATTN_WARPS", 0);  // 0 auto, 4 or 8 forced
+        e->attn_w8_tenths = env_int("OPPO_ATTN_W8_TENTHS", 20);  // auto: 8 warps up to 2.0 CTAs/SM
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
         e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 192);
