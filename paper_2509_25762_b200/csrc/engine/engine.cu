@@ -412,14 +412,16 @@ void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
 
 // Decode attention with RoPE + KV append fused (attn_dec.cuh), bf16.  The
 // qkv row comes from the decode GEMM's partials (n_part > 0) or a bf16 row.
-template <int HD, int NW>
+template <int HD, int NW, int TPO = 0>
 void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
                         const float* part, int n_part, const float* bias) {
-    using Cf = AttnDecCfg<HD, NW>;
+    using Cf = AttnDecCfg<HD, NW, TPO>;
     static std::once_flag attr;
     std::call_once(attr, [] {
-        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW, TPO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Cf::SMEM));
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW, TPO>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     });
     const auto& d = m.dims;
     const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
@@ -438,10 +440,10 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     const int early = base * nsp <= 2 * w.sms ? 1 : 0;
     const int smem = early ? Cf::SMEM : Cf::SMEM_ALIAS;
     if (nsp > 1)
-        launch_cluster_z(e.pdl, nsp, attn_dec<HD, NW>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias,
+        launch_cluster_z(e.pdl, nsp, attn_dec<HD, NW, TPO>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias,
                          qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
     else
-        launch(e.pdl, attn_dec<HD, NW>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias, qkv, out, kv,
+        launch(e.pdl, attn_dec<HD, NW, TPO>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias, qkv, out, kv,
                layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
     e.launches += 1;
 }
@@ -464,6 +466,8 @@ void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
         break;
     case 64:
         if (w8) attn_dec_launch_hd<64, 8>(e, m, w, st, layer, R, part, n_part, bias);
+        else if (e.attn_tp16 > 0 || (e.attn_tp16 < 0 && R * m.dims.n_kv_heads >= 5 * w.sms))
+            attn_dec_launch_hd<64, 4, 16>(e, m, w, st, layer, R, part, n_part, bias);
         else attn_dec_launch_hd<64, 4>(e, m, w, st, layer, R, part, n_part, bias);
         break;
     default: attn_dec_launch_hd<128, 4>(e, m, w, st, layer, R, part, n_part, bias); break;
@@ -709,21 +713,35 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
+    const bool rope_epi = std::is_same_v<T, __nv_bfloat16> && e.rope_epi && (hd == 64 || hd == 128);
     for (int l = 0; l < d.n_layers; ++l) {
         const auto& L = m.layers[l];
         launch(e.pdl, rmsnorm_rows<T>, dim3(nrm_blocks), dim3(128), 0, st, w.x, L.ln1, static_cast<T*>(w.h), R, D, kRmsEps,
                                                     nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, -1,
                                                     nullptr, 0, size_t(0));
         EpiParams ep{};
-        ep.mode = EPI_STORE;
-        ep.y = w.qkv;
-        ep.ldy = m.qkv_width();
         ep.bias = L.bqkv;
         ep.scale = 1.f;
-        gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
-        launch(e.pdl, rope_append<T>, dim3(R), dim3(128), 0, st, static_cast<const T*>(w.qkv), static_cast<T*>(w.q), kv, l,
-                                          w.meta.slot, w.meta.pos, R, H, kRopeTheta, nullptr, 0, size_t(0),
-                                          nullptr);
+        if (rope_epi) {  // RoPE + KV append in the projection's epilogue
+            ep.mode = EPI_ROPE_APPEND;
+            ep.q_out = w.q;
+            ep.kv = kv;
+            ep.layer = l;
+            ep.n_heads = H;
+            ep.theta = kRopeTheta;
+            ep.slot = w.meta.slot;
+            ep.pos = w.meta.pos;
+            gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
+            e.launches -= 1;  // counted below with the rope launch it replaces
+        } else {
+            ep.mode = EPI_STORE;
+            ep.y = w.qkv;
+            ep.ldy = m.qkv_width();
+            gemm_run(e, w, st, w.h, R, D, D, L.wqkv, m.qkv_width(), D, ep);
+            launch(e.pdl, rope_append<T>, dim3(R), dim3(128), 0, st, static_cast<const T*>(w.qkv),
+                   static_cast<T*>(w.q), kv, l, w.meta.slot, w.meta.pos, R, H, kRopeTheta, nullptr, 0,
+                   size_t(0), nullptr);
+        }
         if constexpr (std::is_same_v<T, __nv_bfloat16>) {
             attn_mma_launch(e, m, w, st, l, R, decode, splits, qblocks, n_qblocks);
         } else if (decode) {
@@ -891,6 +909,10 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_warps = env_int("OPPO_ATTN_WARPS", 0);  // 0 auto, 4 or 8 forced
         e->attn_w8_tenths = env_int("OPPO_ATTN_W8_TENTHS", 20);  // auto: 8 warps up to 2.0 CTAs/SM
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
+        e->rope_epi = env_int("OPPO_ROPE_EPI", 1) != 0;
+        // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
+        // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
+        e->attn_tp16 = env_int("OPPO_ATTN_TP16", -1);
         e->dec_gu_max = env_int("OPPO_DEC_GU_MAX", 64);
         e->dec_res_max = env_int("OPPO_DEC_RES_MAX", 192);
         e->nccl = cfg.nccl_comm;

@@ -156,6 +156,8 @@ struct Engine {
     int debug_skip = 0;
     bool attn_fused = true;
     int attn_warps = 0;        // decode attention warps per CTA (0 auto, 4 or 8)
+    int attn_tp16 = -1;         // 4-warp decode attention with 16-position tiles (hd 64): -1 auto, 0 off, 1 on
+    bool rope_epi = true;       // prefill: RoPE + KV append in the q|k|v GEMM epilogue
     int attn_w8_tenths = 20;   // auto rule: 8 warps while CTAs <= tenths/10 x SMs
     int lmhead_dec_max = 32;   // decode lm_head through lmhead_dec.cuh up to this batch (0: off)
     // persistent decode kernel (decode_mega.cuh) for batches <= mega_max_rows

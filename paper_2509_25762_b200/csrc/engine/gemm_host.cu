@@ -125,6 +125,9 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     ep.n_tiles = gemm_logit_tiles(dtype, N);
     GemmShape sh{M, N, K, 1, 0, nullptr, nullptr};
     const int m_tiles = (M + 127) / 128;
+    const bool rope = ep.mode == EPI_ROPE_APPEND;
+    if (rope && (dtype != OPPO_DTYPE_BF16 || (ep.kv.head_dim != 64 && ep.kv.head_dim != 128)))
+        throw Error(OPPO_ERR_INTERNAL, "rope-append epilogue: bf16, head_dim 64 or 128 only");
     if (dtype == OPPO_DTYPE_F32) {
         if (ldx != K || ldw != K) throw Error(OPPO_ERR_INTERNAL, "SIMT GEMM needs packed rows");
         launch(e && e->pdl, gemm_simt<float>, dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock),
@@ -134,7 +137,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     }
     // Token-rich prefill GEMMs (>= 8 token tiles, not the logits epilogue, the
     // output wide enough to fill the SMs): 256x256 tiles, one CTA per SM.
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && g_tc256 &&
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && g_tc256 &&
         ((M + 255) / 256) * ((N + 255) / 256) >= num_sms) {
         static std::once_flag attr256;
         std::call_once(attr256, [] {
@@ -155,7 +158,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // Token-rich prefill GEMMs: CTA-pair 256x256 tiles (cta_group::2)
     const bool scorer_stream = e && st == e->ss;
     const bool use2 = g_tc2sm == 1 || (g_tc2sm == 2 && scorer_stream) || (g_tc2sm == 3 && !scorer_stream);
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && use2) {
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && use2) {
         static std::once_flag attr2;
         std::call_once(attr2, [] {
             OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm,
@@ -196,6 +199,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
                 break;
             }
     }
+    if (rope && BN < ep.kv.head_dim) BN = ep.kv.head_dim;  // whole heads per tile
     const int n_tiles = (N + BN - 1) / BN;
     const int kb = (K + 63) / 64;
     const int tiles = n_tiles * m_tiles;

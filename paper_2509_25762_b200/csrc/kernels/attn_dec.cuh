@@ -26,12 +26,13 @@
 
 namespace oppo {
 
-template <int HD, int NW = 4>
+template <int HD, int NW = 4, int TPO = 0>
 struct AttnDecCfg {
     static constexpr int WARPS = NW;
     static constexpr int THREADS = 32 * NW;
-    // positions per warp tile (8 warps: half-size tiles, same shared memory)
-    static constexpr int TP = (HD >= 128 || NW == 8) ? 16 : 32;
+    // positions per warp tile (8 warps: half-size tiles, same shared memory;
+    // TPO = 16 with 4 warps: half the shared memory, more resident CTAs)
+    static constexpr int TP = TPO ? TPO : ((HD >= 128 || NW == 8) ? 16 : 32);
     static constexpr int LDS = HD + 8;              // padded smem row (elements)
     static constexpr int WARP_BYTES = 2 * 2 * TP * LDS * 2;  // K,V double buffer
     static constexpr int SLOT = 16 * HD + 32;                // merge partial (floats)
@@ -47,14 +48,14 @@ struct AttnDecCfg {
                                                                               : (NW * WARP_BYTES) / (NW * SLOT * 4);
 };
 
-template <int HD, int NW>
+template <int HD, int NW, int TPO = 0>
 __global__ void __launch_bounds__(32 * NW)
     attn_dec(const float* __restrict__ part, int n_part, size_t part_stride,
              const float* __restrict__ bias, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* out,
              KvView kv, int layer, int n_heads, const int32_t* __restrict__ slot_r,
              const int32_t* __restrict__ pos_r, int rows, float theta, int early_tiles) {
     using namespace am;
-    using Cf = AttnDecCfg<HD, NW>;
+    using Cf = AttnDecCfg<HD, NW, TPO>;
     constexpr int TP = Cf::TP, LDS = Cf::LDS, NT = TP / 8, DT = HD / 8, NTH = Cf::THREADS;
     extern __shared__ __align__(128) uint8_t adsm[];
     uint8_t* kvbuf = adsm;                                                     // 4 warps x K/V x 2

@@ -20,25 +20,6 @@ struct RowMeta {          // one row of a batch (decode or prefill)
     uint64_t* key;        // [R] sampling key (decode rows)
 };
 
-struct KvView {
-    void* k;              // pool base of layer 0
-    void* v;
-    int64_t layer_stride; // elements between layers
-    int32_t page_size;
-    int32_t kv_heads;
-    int32_t head_dim;
-    const int32_t* page_table;  // [slots][max_pages]
-    int32_t max_pages;
-};
-
-template <class T>
-__device__ __forceinline__ size_t kv_index(const KvView& kv, int layer, int slot, int pos, int h) {
-    const int page = kv.page_table[slot * kv.max_pages + pos / kv.page_size];
-    return static_cast<size_t>(layer) * kv.layer_stride +
-           ((static_cast<size_t>(page) * kv.kv_heads + h) * kv.page_size + pos % kv.page_size) *
-               kv.head_dim;
-}
-
 // --------------------------------------------------------------- weights
 // N(0, std) from the counter-based stream (seed, tensor id, index), Box-Muller.
 template <class T>

@@ -239,16 +239,27 @@ def test_ppo_update_vs_oracle_fp32():
     eng.close()
 
 
-def test_gqa_05b_width_bf16_vs_oracle():
+@pytest.mark.parametrize("attn_env", ["", "OPPO_ATTN_TP16=1", "OPPO_ATTN_WARPS=8", "OPPO_ATTN_WARPS=4"])
+def test_gqa_05b_width_bf16_vs_oracle(attn_env):
     """0.5B geometry (d=896, 14 q heads over 2 kv heads, head_dim 64, SwiGLU
     4864) at 2 layers / small vocabulary: tensor-core attention (decode and
-    chunked prefill, G=7 rows per KV head) and tcgen05 GEMMs vs fp64."""
+    chunked prefill, G=7 rows per KV head) and tcgen05 GEMMs vs fp64.  Every
+    decode-attention variant the launcher can pick by batch size (4 warps x 32
+    or 16 positions, 8 warps x 16) is forced once."""
+    import os
     shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
                  vocab=1024, tied=1)
     P, C = 16, 16
     lens = [40, 70, 23, 64]
-    eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=80,
-                 sample_seed=SAMPLE_SEED)
+    key, _, val = attn_env.partition("=")
+    if key:
+        os.environ[key] = val
+    try:
+        eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=80,
+                     sample_seed=SAMPLE_SEED)
+    finally:
+        if key:
+            os.environ.pop(key, None)
     st = fresh_states(len(lens), P, lens)
     eng.admit(st)
     eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
@@ -257,6 +268,49 @@ def test_gqa_05b_width_bf16_vs_oracle():
         check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.2, margin_tol=0.2,
                       strict_tokens=False)  # bf16 reward/value heads at d=896: ~0.1 absolute
     eng.close()
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_rope_append_epilogue_matches_separate_kernel(hd):
+    """Prefill q|k|v projection with RoPE + paged KV append in the GEMM
+    epilogue (EPI_ROPE_APPEND, the default) against EPI_STORE followed by the
+    rope_append kernel (OPPO_ROPE_EPI=0): same arithmetic, so at head_dim 64
+    (same tiles and K splits in both runs) every rollout output (tokens,
+    log-probs, reference log-probs, values, rewards) is bit-identical.  At
+    head_dim 128 the fused epilogue needs >= 128-wide tiles where the
+    unfused path picks 64-wide ones with another K split for small passes, so
+    the summation order differs: there the fused run is checked against the
+    fp64 oracle on every sequence."""
+    import os
+    H, KV = (14, 2) if hd == 64 else (12, 2)
+    shape = dict(n_layers=2, d_model=H * hd, n_heads=H, n_kv_heads=KV, head_dim=hd,
+                 d_ff=4864, vocab=1024, tied=1)
+    P, C = 40, 16  # multi-chunk prompts: prefill rows span pages and tiles
+    lens = [40, 70, 23, 64, 5, 33]
+    res = []
+    for flag in ("1", "0"):
+        os.environ["OPPO_ROPE_EPI"] = flag
+        try:
+            eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P,
+                         max_response_len=80, sample_seed=SAMPLE_SEED)
+        finally:
+            os.environ.pop("OPPO_ROPE_EPI", None)
+        st = fresh_states(len(lens), P, lens)
+        eng.admit(st)
+        eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+        res.append([eng.read_rollout(s["id"]) for s in st])
+        if flag == "1":
+            orc = oracles(eng)
+            for s in (st if hd == 128 else st[:3]):
+                check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.2, margin_tol=0.2,
+                              strict_tokens=False)
+        eng.close()
+        if hd == 128:
+            return
+    for a, b in zip(*res):
+        assert a["length"] == b["length"] and a["reward"] == b["reward"]
+        for k in ("tokens", "old_lp", "ref_lp", "values"):
+            assert np.array_equal(a[k], b[k]), k
 
 
 def test_persistent_decode_kernel_vs_oracle_and_multi_kernel_path():
