@@ -219,10 +219,12 @@ void make_sm_partition(Engine& e, int scorer_sms, int prio_hi, int prio_lo) {
     OPPO_CU_CHECK(driver_fn<GenDesc>("cuDevResourceGenerateDesc")(&da, &rest, 1));
     OPPO_CU_CHECK(driver_fn<GCreate>("cuGreenCtxCreate")(&e.gctx_scorer, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM));
     OPPO_CU_CHECK(driver_fn<GCreate>("cuGreenCtxCreate")(&e.gctx_actor, da, dev, CU_GREEN_CTX_DEFAULT_STREAM));
-    CUstream a, s;
+    CUstream a, a2, s;
     OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&a, e.gctx_actor, CU_STREAM_NON_BLOCKING, prio_hi));
+    OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&a2, e.gctx_actor, CU_STREAM_NON_BLOCKING, prio_hi));
     OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&s, e.gctx_scorer, CU_STREAM_NON_BLOCKING, prio_lo));
     e.sa = reinterpret_cast<cudaStream_t>(a);
+    e.sa2 = reinterpret_cast<cudaStream_t>(a2);
     e.ss = reinterpret_cast<cudaStream_t>(s);
     e.sms_actor = static_cast<int>(rest.sm.smCount);
     e.sms_scorer = static_cast<int>(grp.sm.smCount);
@@ -346,6 +348,18 @@ void alloc_work(Engine& e, Work& w, int rows, bool lm_rows) {
     w.attn_ws_rows = std::max<size_t>(R * hmax * 8, static_cast<size_t>(e.num_sms) * 64);
     w.attn_ws_o = static_cast<float*>(dalloc(w.attn_ws_rows * hdmax * 4));
     w.attn_ws_ml = static_cast<float*>(dalloc(w.attn_ws_rows * 2 * 4));
+}
+
+void free_work(Work& w) {
+    for (void* p : {static_cast<void*>(w.meta.slot), static_cast<void*>(w.meta.pos), static_cast<void*>(w.meta.tok),
+                    static_cast<void*>(w.meta.t), static_cast<void*>(w.meta.key), static_cast<void*>(w.x), w.h,
+                    w.qkv, w.q, w.attn, w.ff, static_cast<void*>(w.head_out), static_cast<void*>(w.partials),
+                    static_cast<void*>(w.tgt_logit), static_cast<void*>(w.lse), w.lm_in,
+                    static_cast<void*>(w.lm_tgt), static_cast<void*>(w.lm_slot), static_cast<void*>(w.lm_t),
+                    static_cast<void*>(w.gemm_ws), static_cast<void*>(w.gemm_cnt), static_cast<void*>(w.attn_ws_o),
+                    static_cast<void*>(w.attn_ws_ml)})
+        if (p) cudaFree(p);
+    w = Work{};
 }
 
 // --------------------------------------------------------------- forward
@@ -823,11 +837,14 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->su, cudaStreamNonBlocking, hi));
         } else {
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
+            OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa2, cudaStreamNonBlocking, hi));
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
             e->su = e->sa;
         }
         for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
+        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join})
+            OPPO_CUDA_CHECK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
 
         e->S = cfg.max_slots;
         e->Pmax = cfg.max_prompt_len;
@@ -895,6 +912,16 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         e->wa.sms = e->sms_actor;
         e->ws.sms = e->sms_scorer;
+        // two-branch decode iterations (bf16): the rows split in halves that run
+        // concurrently on sa / sa2, each half's launch latencies hidden behind
+        // the other's kernels (the weights are streamed twice)
+        e->dec_split_min = env_int("OPPO_DEC_SPLIT_MIN", 176);  // measured: wins from ~192 rows
+        if (e->dec_split_min > 0 && e->dtype == OPPO_DTYPE_BF16) {
+            alloc_work<__nv_bfloat16>(*e, e->wa2, std::max(e->S + 16, 32), false);
+            e->wa2.sms = e->sms_actor;
+        } else {
+            e->dec_split_min = 0;
+        }
         // persistent decode kernel: experimental, off by default (measured slower
         // than the PDL-chained kernels: 2 us per grid barrier x 168, profiles/)
         e->mega_max_rows = env_int("OPPO_MEGA_MAX_ROWS", 0);
@@ -964,7 +991,11 @@ void engine_free(Engine* e) {
                     static_cast<void*>(e->d_mega_acnt)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
+    for (Work* w : {&e->wa, &e->wa2, &e->ws}) free_work(*w);
+    for (cudaEvent_t ev : {e->ev_begin, e->ev_dec_end, e->ev_sc_end, e->ev_done, e->ev_loop0, e->ev_fork, e->ev_join})
+        if (ev) cudaEventDestroy(ev);
     if (e->su && e->su != e->sa) cudaStreamDestroy(e->su);
+    if (e->sa2) cudaStreamDestroy(e->sa2);
     if (e->sa) cudaStreamDestroy(e->sa);
     if (e->ss) cudaStreamDestroy(e->ss);
     try {
@@ -1271,13 +1302,12 @@ void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, in
     OPPO_CUDA_CHECK(cudaGetLastError());
 }
 
+// Rows [0, M) of one decode iteration through `w` (meta already filled):
+// forward, lm_head + in-block sampling, combine (token, log-prob -> buffers).
 template <class T>
-void decode_iteration(Engine& e, int M, cudaStream_t st) {
-    Work& w = e.wa;
+void decode_rows_forward(Engine& e, Work& w, int M, cudaStream_t st, int32_t* iter_inc) {
     Model& m = e.models[ACTOR];
     const int max_ctx = e.Pmax + e.Lmax;
-    launch(e.pdl, decode_rows, dim3(cdiv(M, 128)), dim3(128), 0, st, e.d_dseq, M, e.d_iter, e.d_prompt, e.Pmax, e.d_tok,
-                                              e.tok_stride, e.cfg.sample_seed, w.meta, e.S);
     Final<T> fin;
     fin.write_h = true;
     fin.cache = static_cast<T*>(e.d_hf_actor);
@@ -1297,8 +1327,40 @@ void decode_iteration(Engine& e, int M, cudaStream_t st) {
         gemm_run(e, w, st, w.h, M, D, D, m.lm_head, m.dims.vocab, D, ep);
     launch(e.pdl, logits_combine, dim3(cdiv(M, 4)), dim3(128), 0, st, w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, M, w.meta.key,
                                                nullptr, w.meta.slot, w.meta.t, e.d_tok, e.d_old_lp,
-                                               e.tok_stride, nullptr, nullptr, e.d_iter);
-    e.launches += 3;
+                                               e.tok_stride, nullptr, nullptr, iter_inc);
+    e.launches += 2;
+}
+
+template <class T>
+void decode_iteration(Engine& e, int M, cudaStream_t st) {
+    Work& w = e.wa;
+    launch(e.pdl, decode_rows, dim3(cdiv(M, 128)), dim3(128), 0, st, e.d_dseq, M, e.d_iter, e.d_prompt, e.Pmax, e.d_tok,
+                                              e.tok_stride, e.cfg.sample_seed, w.meta, e.S);
+    e.launches += 1;
+    if (e.dec_split_min > 0 && M >= e.dec_split_min && M >= 32) {
+        // two concurrent halves: rows [0, M1) on st through wa, [M1, M) on sa2
+        // through wa2 viewing wa's row metadata; the iteration counter is
+        // advanced by the second half only (both read it in decode_rows above)
+        const int M1 = (M / 2 + 15) / 16 * 16;
+        static const int pct = env_int("OPPO_DEC_SPLIT_SMS_PCT", 50);  // grid sizing per half (measured best)
+        Work wa_h = w;
+        wa_h.sms = std::max(8, w.sms * pct / 100);
+        Work wb = e.wa2;
+        wb.sms = wa_h.sms;
+        wb.meta.slot = w.meta.slot + M1;
+        wb.meta.pos = w.meta.pos + M1;
+        wb.meta.tok = w.meta.tok + M1;
+        wb.meta.t = w.meta.t + M1;
+        wb.meta.key = w.meta.key + M1;
+        OPPO_CUDA_CHECK(cudaEventRecord(e.ev_fork, st));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.sa2, e.ev_fork, 0));
+        decode_rows_forward<T>(e, wb, M - M1, e.sa2, e.d_iter);
+        decode_rows_forward<T>(e, wa_h, M1, st, nullptr);
+        OPPO_CUDA_CHECK(cudaEventRecord(e.ev_join, e.sa2));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(st, e.ev_join, 0));
+    } else {
+        decode_rows_forward<T>(e, w, M, st, e.d_iter);
+    }
 }
 
 // One decode iteration for batch size M: replay the captured graph (capture on

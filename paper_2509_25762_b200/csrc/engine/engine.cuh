@@ -139,6 +139,10 @@ struct Engine {
     void* d_ref_pending = nullptr;     // [S, d_ref]
 
     Work wa, ws;                        // actor decode / scorer prefill
+    Work wa2;                           // second decode branch (split iterations), rows view into wa.meta
+    cudaStream_t sa2 = nullptr;         // second decode branch stream (actor SMs)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int dec_split_min = 0;              // decode iterations of >= this many rows run as two concurrent halves
     int prefill_rows = 8192;
     int qblock = 32;  // queries per prefill attention block (bf16: rows = queries x G <= 64)
     cudaStream_t sa = nullptr, ss = nullptr;

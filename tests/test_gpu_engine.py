@@ -313,6 +313,36 @@ def test_rope_append_epilogue_matches_separate_kernel(hd):
             assert np.array_equal(a[k], b[k]), k
 
 
+def test_two_branch_decode_iterations_vs_oracle():
+    """Decode iterations split into two concurrent halves (OPPO_DEC_SPLIT_MIN:
+    rows [0, M1) on the actor stream, [M1, M) on a second stream, one CUDA
+    graph with a fork/join) at 40 active rows (bucket 48 -> 32 + 16), 0.5B
+    geometry: sampled tokens / log-probs / scorer outputs against the fp64
+    oracle, and every sequence reaches its target length (the iteration
+    counter advances once per iteration)."""
+    import os
+    shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                 vocab=1024, tied=1)
+    P, C = 16, 16
+    lens = [20 + (7 * i) % 40 for i in range(40)]
+    os.environ["OPPO_DEC_SPLIT_MIN"] = "32"
+    try:
+        eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=48, max_prompt_len=P,
+                     max_response_len=64, sample_seed=SAMPLE_SEED)
+    finally:
+        os.environ.pop("OPPO_DEC_SPLIT_MIN", None)
+    st = fresh_states(len(lens), P, lens)
+    eng.admit(st)
+    eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+    orc = oracles(eng)
+    for i in (0, 1, 17, 31, 32, 33, 39):  # both halves and the boundary
+        check_rollout(eng, orc, st[i]["id"], P, tol_lp=0.15, tol_val=0.2, margin_tol=0.2,
+                      strict_tokens=False)
+    for s_ in st:
+        assert eng.read_rollout(s_["id"])["length"] == s_["target_len"]
+    eng.close()
+
+
 def test_persistent_decode_kernel_vs_oracle_and_multi_kernel_path():
     """The persistent decode kernel (decode_mega.cuh, experimental, enabled by OPPO_MEGA_MAX_ROWS)
     at 40 rows, 0.5B geometry, 3 layers: sampled tokens / log-probs against the
