@@ -843,7 +843,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
-        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join})
+        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join, &e->ev_pre})
             OPPO_CUDA_CHECK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
 
         e->S = cfg.max_slots;
@@ -937,6 +937,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_w8_tenths = env_int("OPPO_ATTN_W8_TENTHS", 20);  // auto: 8 warps up to 2.0 CTAs/SM
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->rope_epi = env_int("OPPO_ROPE_EPI", 1) != 0;
+        e->pre_lp = env_int("OPPO_PRE_LP", 1) != 0;
         // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
         // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
         e->attn_tp16 = env_int("OPPO_ATTN_TP16", -1);
@@ -988,11 +989,14 @@ void engine_free(Engine* e) {
                     static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf,
                     static_cast<void*>(e->g_lm), static_cast<void*>(e->d_mega_layers),
                     static_cast<void*>(e->d_mega_bar), static_cast<void*>(e->d_mega_aws),
-                    static_cast<void*>(e->d_mega_acnt)})
+                    static_cast<void*>(e->d_mega_acnt), e->pre_hf, static_cast<void*>(e->pre_tok),
+                    static_cast<void*>(e->pre_new), static_cast<void*>(e->pre_lse), static_cast<void*>(e->pre_meta),
+                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     for (Work* w : {&e->wa, &e->wa2, &e->ws}) free_work(*w);
-    for (cudaEvent_t ev : {e->ev_begin, e->ev_dec_end, e->ev_sc_end, e->ev_done, e->ev_loop0, e->ev_fork, e->ev_join})
+    for (cudaEvent_t ev : {e->ev_begin, e->ev_dec_end, e->ev_sc_end, e->ev_done, e->ev_loop0, e->ev_fork, e->ev_join,
+                           e->ev_pre})
         if (ev) cudaEventDestroy(ev);
     if (e->su && e->su != e->sa) cudaStreamDestroy(e->su);
     if (e->sa2) cudaStreamDestroy(e->sa2);
@@ -1394,6 +1398,89 @@ void decode_iteration_graph(Engine& e, int M, cudaStream_t st) {
     e.launches += e.decode_graph_launches[M];
 }
 
+// ------------------------------------ policy log-probs of the finished sequences
+// meta = [n slots][n + 1 token offsets]
+template <class T>
+__global__ void pre_gather(const int32_t* __restrict__ meta, int n, const int32_t* __restrict__ tok,
+                           const T* __restrict__ cache, int stride, int d, int32_t* o_tok, T* o_hf) {
+    const int i = blockIdx.y;
+    const int s = meta[i], a = meta[n + i], L = meta[n + i + 1] - a;
+    for (int t = blockIdx.x; t < L; t += gridDim.x) {
+        const size_t src = static_cast<size_t>(s) * stride + t + 1;
+        if (threadIdx.x == 0) o_tok[a + t] = tok[src];
+        const T* h = cache + src * d;
+        T* dst = o_hf + static_cast<size_t>(a + t) * d;
+        for (int k = threadIdx.x; k < d; k += blockDim.x) dst[k] = h[k];
+    }
+}
+
+// log pi(token) and the log-sum-exp of every sampled token of the sequences
+// that finished this step, under the current lm_head, on stream `st` (the
+// actor's SMs, idle while the scorers finish the last wave).  Same kernels,
+// tiles and per-row arithmetic as the recompute in ppo_update_impl (a
+// LOGITS row never depends on the other rows of its tile), so the update
+// that reuses them is bit-identical to one that recomputes.
+template <class T>
+void precompute_policy_lp(Engine& e, const std::vector<int>& fslots, cudaStream_t st) {
+    e.pre_index.clear();
+    e.pre_version = -1;
+    const int n = static_cast<int>(fslots.size());
+    if (n == 0) return;
+    Model& actor = e.models[ACTOR];
+    const int Da = actor.dims.d_model, V = actor.dims.vocab;
+    std::vector<int32_t> meta(2 * n + 1);
+    int N = 0;
+    for (int i = 0; i < n; ++i) {
+        const auto& info = e.slots[fslots[i]];
+        meta[i] = fslots[i];
+        meta[n + i] = N;
+        e.pre_index[info.id] = {N, info.target_len};
+        N += info.target_len;
+    }
+    meta[2 * n] = N;
+    if (N == 0) return;
+    if (static_cast<size_t>(N) > e.pre_cap) {
+        for (void* p : {e.pre_hf, static_cast<void*>(e.pre_tok), static_cast<void*>(e.pre_new),
+                        static_cast<void*>(e.pre_lse)})
+            if (p) cudaFree(p);
+        e.pre_cap = static_cast<size_t>(N) * 5 / 4 + 64;
+        e.pre_hf = dalloc(e.pre_cap * Da * e.esz);
+        e.pre_tok = static_cast<int32_t*>(dalloc(e.pre_cap * 4));
+        e.pre_new = static_cast<float*>(dalloc(e.pre_cap * 4));
+        e.pre_lse = static_cast<float*>(dalloc(e.pre_cap * 4));
+    }
+    if (2 * n + 1 > e.pre_meta_cap) {
+        if (e.pre_meta) cudaFree(e.pre_meta);
+        e.pre_meta_cap = 2 * n + 65;
+        e.pre_meta = static_cast<int32_t*>(dalloc(static_cast<size_t>(e.pre_meta_cap) * 4));
+    }
+    const int nt = gemm_logit_tiles(e.dtype, V);
+    if (!e.pre_partials) {
+        e.pre_chunk = std::max(128, std::min(8192, static_cast<int>((static_cast<size_t>(64) << 20) / (nt * 16))));
+        e.pre_partials = static_cast<float4*>(dalloc(static_cast<size_t>(e.pre_chunk) * nt * 16));
+        e.pre_tgt = static_cast<float*>(dalloc(static_cast<size_t>(e.pre_chunk) * 4));
+    }
+    OPPO_CUDA_CHECK(cudaMemcpyAsync(e.pre_meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, st));
+    pre_gather<T><<<dim3(64, n), 128, 0, st>>>(e.pre_meta, n, e.d_tok, static_cast<const T*>(e.d_hf_actor),
+                                               e.tok_stride, Da, e.pre_tok, static_cast<T*>(e.pre_hf));
+    for (int c0 = 0; c0 < N; c0 += e.pre_chunk) {
+        const int cn = std::min(e.pre_chunk, N - c0);
+        EpiParams ep{};
+        ep.mode = EPI_LOGITS;
+        ep.partials = e.pre_partials;
+        ep.tgt_logit = e.pre_tgt;
+        ep.targets = e.pre_tok + c0;
+        gemm_run(e, e.wa, st, static_cast<const T*>(e.pre_hf) + static_cast<size_t>(c0) * Da, cn, Da, Da,
+                 actor.lm_head, V, Da, ep);
+        logits_combine<<<cdiv(cn, 4), 128, 0, st>>>(e.pre_partials, nt, V, cn, nullptr, e.pre_tgt, nullptr, nullptr,
+                                                    nullptr, e.pre_new + c0, 0, e.pre_lse + c0, nullptr);
+    }
+    e.launches += 1 + 2 * cdiv(N, e.pre_chunk);
+    OPPO_CUDA_CHECK(cudaGetLastError());
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_pre, st));
+    e.pre_version = e.lm_version;
+}
+
 template <class T>
 void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chunk, int mode,
                    int stop_after, std::vector<oppo_seq_outcome>& out, oppo_ledger& ledger) {
@@ -1567,6 +1654,12 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
                      host_enqueue_us / 1e3, static_cast<long long>(t_end), e.tma_cache.size());
     fire_waves_at(t_end);  // (t_end == 0 or already fired: no-op)
     if (wi != waves.size()) internal_error("unfired scorer waves");
+    if (e.pre_lp) {  // the actor SMs are idle until the scorers finish: policy log-probs for the update
+        std::vector<int> fs;
+        for (int i = 0; i < n; ++i)
+            if (active[i].generated + plan.outcomes[i].tokens_decoded >= active[i].target_len) fs.push_back(slot[i]);
+        precompute_policy_lp<T>(e, fs, e.sa);
+    }
     worker.drain();  // every scorer launch is enqueued on ss (rethrows a worker error)
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_sc_end, e.ss));
     OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.sa, e.ev_sc_end, 0));
@@ -1627,6 +1720,17 @@ __global__ void gather_batch(const int32_t* __restrict__ slots, const int32_t* _
     if (threadIdx.x == 0) {
         o_vals[a + i + L] = 0.f;  // terminal convention (ppo.cpp:278)
         o_score[i] = reward[s];
+    }
+}
+__global__ void gather_pre_lp(const int32_t* __restrict__ src, const int32_t* __restrict__ off, int n,
+                              const float* __restrict__ pre_new, const float* __restrict__ pre_lse, float* o_new,
+                              float* o_lse) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    const int a = off[i], L = off[i + 1] - a, b = src[i];
+    for (int t = threadIdx.x; t < L; t += blockDim.x) {
+        o_new[a + t] = pre_new[b + t];
+        o_lse[a + t] = pre_lse[b + t];
     }
 }
 template <class T>
@@ -1734,7 +1838,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     const int Da = actor.dims.d_model, Dc = critic.dims.d_model, V = actor.dims.vocab;
     const int Npad = (N + 7) / 8 * 8;
     // device buffers (grown on demand)
-    const size_t need = static_cast<size_t>(Npad) * (4 * 12) + static_cast<size_t>(n + 1) * 16 * 4 +
+    const size_t need = static_cast<size_t>(Npad) * (4 * 12) + static_cast<size_t>(n + 1) * 20 * 4 +
                         static_cast<size_t>(Npad) * (Da + Dc) * sizeof(T) + 4096 * 8 + 1024;
     if (need > e.ppo_buf_bytes) {
         if (e.ppo_buf) cudaFree(e.ppo_buf);
@@ -1811,11 +1915,27 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         samples_glob = g[4];
     }
     const float inv_n_glob = 1.0f / static_cast<float>(std::max(1.0, n_glob));
-    // current-policy log-probs of the sampled tokens from the cached actor hidden states
+    // current-policy log-probs of the sampled tokens from the cached actor
+    // hidden states: computed at the end of run_step while the scorers
+    // finished (precompute_policy_lp) when every sequence of the batch is
+    // there and the lm_head is unchanged, else here
     const int nt = gemm_logit_tiles(e.dtype, V);
     Work& w = e.ws;
+    bool use_pre = e.pre_lp && e.pre_version == e.lm_version && n > 0;
+    std::vector<int32_t> pre_src(n);
+    for (int i = 0; i < n && use_pre; ++i) {
+        const auto it = e.pre_index.find(e.slots[slots[i]].id);
+        if (it == e.pre_index.end() || it->second.second != off[i + 1] - off[i]) use_pre = false;
+        else pre_src[i] = it->second.first;
+    }
+    if (use_pre) {
+        int32_t* d_src = reinterpret_cast<int32_t*>(take(n * 4));
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(d_src, pre_src.data(), n * 4, cudaMemcpyHostToDevice, st));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(st, e.ev_pre, 0));
+        gather_pre_lp<<<n, 128, 0, st>>>(d_src, d_off, n, e.pre_new, e.pre_lse, d_new, d_lse);
+    }
     const int chunk_rows = std::max(32, std::min(w.max_rows, static_cast<int>((static_cast<size_t>(64) << 20) / (nt * 16))));
-    for (int c0 = 0; c0 < N; c0 += chunk_rows) {
+    for (int c0 = 0; c0 < N && !use_pre; c0 += chunk_rows) {
         const int cn = std::min(chunk_rows, N - c0);
         EpiParams ep{};
         ep.mode = EPI_LOGITS;
@@ -1877,6 +1997,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         }
         const size_t nn = nw;
         convert<float, T><<<cdiv(nn, 256), 256, 0, st>>>(actor.lm_master, static_cast<T*>(actor.lm_head), nn);
+        ++e.lm_version;  // precomputed policy log-probs are stale from here
         // critic value head: w -= vlr * (1/N) sum (V - R) h
         value_head_grad<T><<<cdiv(Dc, 128), 128, 0, st>>>(d_hc, Dc, N, d_vtok, d_ret, e.vgrad, inv_n_glob);
         if (dp)

@@ -140,6 +140,24 @@ struct Engine {
 
     Work wa, ws;                        // actor decode / scorer prefill
     Work wa2;                           // second decode branch (split iterations), rows view into wa.meta
+    // Policy log-probs (and log-sum-exp) of the sampled tokens of every sequence
+    // that finished in the last step, computed on the actor SMs while the
+    // scorers finish their last wave; oppo_ppo_update reuses them when the
+    // lm_head has not changed since (pre_version == lm_version).
+    bool pre_lp = true;
+    int64_t lm_version = 0, pre_version = -1;
+    std::unordered_map<int64_t, std::pair<int, int>> pre_index;  // seq id -> (token offset, tokens)
+    size_t pre_cap = 0;                 // tokens
+    void* pre_hf = nullptr;             // [pre_cap, d_actor] gathered final hidden states
+    int32_t* pre_tok = nullptr;         // [pre_cap] sampled tokens (targets)
+    float* pre_new = nullptr;           // [pre_cap] log pi(token)
+    float* pre_lse = nullptr;           // [pre_cap]
+    int32_t* pre_meta = nullptr;        // slots + offsets of the gather
+    int pre_meta_cap = 0;
+    float4* pre_partials = nullptr;     // [pre_chunk, vocab/256]
+    float* pre_tgt = nullptr;           // [pre_chunk]
+    int pre_chunk = 0;
+    cudaEvent_t ev_pre = nullptr;
     cudaStream_t sa2 = nullptr;         // second decode branch stream (actor SMs)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int dec_split_min = 0;              // decode iterations of >= this many rows run as two concurrent halves

@@ -313,6 +313,45 @@ def test_rope_append_epilogue_matches_separate_kernel(hd):
             assert np.array_equal(a[k], b[k]), k
 
 
+def test_policy_logprob_precompute_is_bit_identical():
+    """The update's current-policy log-probs, computed at the end of run_step
+    on the actor SMs while the scorers finish (OPPO_PRE_LP=1, default), give
+    the same PPO statistics and the same updated lm_head / value head, bit for
+    bit, as recomputing them inside oppo_ppo_update (OPPO_PRE_LP=0); two
+    rounds, so the second reuses log-probs taken after the first update."""
+    import os
+    shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                 vocab=1024, tied=1)
+    P, C = 16, 16
+    hp = abi.PpoHparams(gamma=1.0, lambda_=0.95, clip_epsilon=0.2, learning_rate=0.5,
+                        value_learning_rate=0.1, kl_coef=0.05, whiten=1)
+    res = []
+    for flag in ("1", "0"):
+        os.environ["OPPO_PRE_LP"] = flag
+        try:
+            eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=16, max_prompt_len=P,
+                         max_response_len=64, sample_seed=SAMPLE_SEED, train_heads=1)
+        finally:
+            os.environ.pop("OPPO_PRE_LP", None)
+        out = []
+        for rnd in range(2):
+            lens = [20 + (11 * i + 5 * rnd) % 40 for i in range(8)]
+            st = fresh_states(len(lens), P, lens, start_id=100 * rnd)
+            eng.admit(st)
+            eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+            stats = eng.ppo_update([s_["id"] for s_ in st], hp)
+            out.append((stats.ppo_objective, stats.kl_mean, stats.adv_mean, stats.adv_std,
+                        stats.value_loss))
+            eng.release([s_["id"] for s_ in st])
+        out.append(eng.get_tensor(0, "lm_head"))
+        out.append(eng.get_tensor(2, "head"))
+        res.append(out)
+        eng.close()
+    a, b = res
+    assert a[0] == b[0] and a[1] == b[1]
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+
+
 def test_two_branch_decode_iterations_vs_oracle():
     """Decode iterations split into two concurrent halves (OPPO_DEC_SPLIT_MIN:
     rows [0, M1) on the actor stream, [M1, M) on a second stream, one CUDA
