@@ -184,10 +184,11 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // prefill: 128x256 tiles, except narrow outputs (N <= 1024: the O and down
     // projections) of mid-size passes, where 128x128 tiles double the CTAs
     // (measured at 2048 rows: down 58.9 -> 34.7 us, O 24.6 -> 16.4 us; at
-    // 8192 rows 256 stays ahead).  OPPO_PREFILL_NARROW_ROWS moves the cut.
+    // 8192 rows 256 stays ahead; the cfg2 bench prefers the cut at 2048).
+    // OPPO_PREFILL_NARROW_ROWS moves the cut.
     static const int narrow_rows = [] {
         const char* v = std::getenv("OPPO_PREFILL_NARROW_ROWS");
-        return v ? std::atoi(v) : 4096;
+        return v ? std::atoi(v) : 2048;  // bench sweep 1024/2048/4096/8192: 2048 best by ~0.3%
     }();
     if (ep.mode == EPI_LOGITS || m_tiles > 4) {
         BN = (ep.mode != EPI_LOGITS && N <= 1024 && M <= narrow_rows) ? 128 : 256;
