@@ -87,6 +87,10 @@ int gemm_logit_tiles(int, int N) { return (N + kSampleBlock - 1) / kSampleBlock;
 // experimental, off: the 256x256 tile serialises its epilogue with the
 // mainloop at one CTA per SM and measured slower (249 vs 182 us, gate|up at
 // 8192 rows) than two 128x256 CTAs per SM
+bool persist_enabled() {  // read per call so tests can compare both kernels in one process
+    const char* v = std::getenv("OPPO_GEMM_PERSIST");
+    return v ? std::atoi(v) != 0 : false;  // off: faster alone, slower in the cfg2 bench (profiles/)
+}
 static const bool g_tc256 = [] {
     const char* v = std::getenv("OPPO_TC256");
     return v && std::atoi(v) != 0;
@@ -132,6 +136,46 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         if (ldx != K || ldw != K) throw Error(OPPO_ERR_INTERNAL, "SIMT GEMM needs packed rows");
         launch(e && e->pdl, gemm_simt<float>, dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock),
                dim3(128), 0, st, static_cast<const float*>(x), static_cast<const float*>(wt), sh, ep);
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    // Token-rich prefill GEMMs (>= 8 token tiles, not the logits epilogue):
+    // persistent kernel, one CTA per SM, 192 KB TMA ring, double-buffered TMEM
+    // (OPPO_GEMM_PERSIST=1; measured: qkv 28.8 -> 22.7 us, gate|up 183 -> 172 us
+    // at 8192 rows alone, but the cfg2 bench loses 1% with it: 212.2 -> 210.1)
+    // Epilogue-light modes only: with a residual read-modify-write or the
+    // transposed softmax-grad stores, the 4 epilogue warps fall behind the
+    // mainloop and the 2-CTA/SM kernel (8 epilogue warps per SM) wins
+    // (bench: update 60 -> 69 ms on the persistent kernel; O / down no gain).
+    const bool light = ep.mode == EPI_STORE || ep.mode == EPI_SWIGLU || ep.mode == EPI_ROPE_APPEND;
+    if (m_tiles >= 8 && light && dtype == OPPO_DTYPE_BF16 && persist_enabled()) {
+        // 128-wide tiles where a 256-wide last tile would waste > 5% (N = 896, 1152)
+        const int pad256 = (N + 255) / 256 * 256 - N;
+        const int BNp = (N % 128 == 0 && pad256 * 20 > N) ? 128 : 256;
+        sh.splits = 1;
+        sh.kb_per_split = (K + 63) / 64;
+        CUtensorMap s1, s2;
+        const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
+        const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, BNp, s2);
+        const int total = m_tiles * ((N + BNp - 1) / BNp);
+        const dim3 grid(std::min(total, num_sms));
+        if (BNp == 256) {
+            static std::once_flag a256;
+            std::call_once(a256, [] {
+                OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_persist<256>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     tc::CfgP<256>::SMEM));
+            });
+            launch(e && e->pdl, tc::gemm_bf16_persist<256>, grid, dim3(192), tc::CfgP<256>::SMEM, st, mx, mw, sh, ep);
+        } else {
+            static std::once_flag a128;
+            std::call_once(a128, [] {
+                OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_persist<128>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     tc::CfgP<128>::SMEM));
+            });
+            launch(e && e->pdl, tc::gemm_bf16_persist<128>, grid, dim3(192), tc::CfgP<128>::SMEM, st, mx, mw, sh, ep);
+        }
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }

@@ -111,6 +111,41 @@ def test_gemm_prefill_256x256_tile_vs_torch(M, N, K, epi, monkeypatch):
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
 
 
+@pytest.mark.parametrize("persist", ["1", "0"])
+@pytest.mark.parametrize("M,N,K,epi", [(1000, 896, 896, EPI_STORE), (8192, 9728, 896, EPI_SWIGLU),
+                                       (3000, 1152, 896, EPI_STORE), (1025, 896, 4864, EPI_ADD_F32),
+                                       (20000, 896, 896, EPI_STORE), (4100, 151936, 896, EPI_STORE)])
+def test_gemm_prefill_persistent_vs_torch(M, N, K, epi, persist, monkeypatch):
+    """Token-rich GEMMs on the persistent kernel (one CTA per SM, TMA ring,
+    double-buffered TMEM accumulators; 128- or 256-wide tiles by N; ragged
+    token counts, more tiles than SMs) and on the 2-CTA/SM tile kernel
+    (OPPO_GEMM_PERSIST=0) against torch: SwiGLU / bias-store run on the
+    persistent kernel, the residual add stays on the tile kernel."""
+    monkeypatch.setenv("OPPO_GEMM_PERSIST", persist)
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.03).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g) if epi == EPI_STORE else None
+    if epi == EPI_ADD_F32:
+        y0 = torch.randn(M, N, device="cuda", generator=g)
+        y = y0.clone()
+    else:
+        y = torch.empty(M, N // 2 if epi == EPI_SWIGLU else N, device="cuda", dtype=torch.bfloat16)
+    st = _lib().oppo_k_gemm(1, M, N, K, _ptr(x), _ptr(w), _ptr(b) if b is not None else None, _ptr(y),
+                            epi, _stream())
+    assert st == 0, _lib().oppo_last_error_global()
+    torch.cuda.synchronize()
+    z = x.float() @ w.float().T
+    if epi == EPI_SWIGLU:
+        ref = torch.nn.functional.silu(z[:, 0::2]) * z[:, 1::2]
+    elif epi == EPI_ADD_F32:
+        ref = y0 + z
+    else:
+        ref = z + b
+    err = (y.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
 # decode GEMM (swap-AB tcgen05, gemm_dec.cuh): partial sums over splits, SwiGLU, store+bias
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 1152, 896), (40, 896, 896), (64, 896, 4864),
                                    (129, 384, 256), (256, 896, 4864), (282, 1152, 896),
