@@ -43,6 +43,8 @@ def ref():
             "ref_run_seed": (i32, [P(abi.RunConfig), u64, P(abi.StepRecord), P(i32), P(i32)]),
             "ref_run_seeds_parallel": (i32, [P(abi.RunConfig), P(u64), i32, P(i64)]),
             "ref_write_outputs": (i32, [P(abi.RunConfig), P(u64), i32, C.c_char_p]),
+            "ref_load_config": (i32, [C.c_char_p, C.c_char_p, C.c_char_p, i32, C.c_char_p, C.c_char_p,
+                                      i32]),
             "ref_trace_seed": (i32, [P(abi.RunConfig), u64, P(abi.StepRecord), P(i32), P(i64),
                                      P(abi.SeqState), i32, P(i32)]),
             "ref_compute_gae": (i32, [P(dbl), P(dbl), i32, dbl, dbl, P(dbl)]),
@@ -142,3 +144,17 @@ def run_seeds_parallel(cfg, seeds):
     tot = C.c_int64()
     rcheck(ref().ref_run_seeds_parallel(C.byref(cfg), arr, len(seeds), C.byref(tot)))
     return tot.value
+
+
+def ref_load_config(text):
+    """rlpipe::load_config_text + config_echo + task_fingerprint + the echo of
+    baseline(): dict(ok, echo, baseline_echo, fingerprint, error)."""
+    cap = 1 << 16
+    echo, base, fp, err = (C.create_string_buffer(cap), C.create_string_buffer(cap),
+                           C.create_string_buffer(32), C.create_string_buffer(cap))
+    st = ref().ref_load_config(text.encode("utf-8"), echo, base, cap, fp, err, cap)
+    if st == 0:
+        return dict(ok=True, echo=echo.value.decode(), baseline_echo=base.value.decode(),
+                    fingerprint=fp.value.decode(), error="")
+    return dict(ok=False, echo="", baseline_echo="", fingerprint="", error=err.value.decode(),
+                config_error=st == 1)

@@ -11,6 +11,7 @@
 // (driver.cpp:103-195) that records selected ids, validated in the tests
 // against rlpipe::run_seed's own StepRecords.
 #include <algorithm>
+#include <cstdio>
 #include <filesystem>
 #include <cstring>
 #include <exception>
@@ -309,6 +310,29 @@ int ref_run_seed(const oppo_run_config* cfg, uint64_t seed, oppo_step_record* re
         *n_recs = static_cast<int>(run.steps.size());
         *complete = run.complete;
     });
+}
+
+// rlpipe::load_config_text + config_echo + RunConfig::task_fingerprint
+// (config.cpp:75-250, :306-409), and the echo of RunConfig::baseline()
+// (config.cpp:411-420): the JSON config schema parity tests.
+// Returns 0 (ok: echo / baseline echo / fingerprint filled), 1 (ConfigError:
+// message in err), 2 (other error).
+int ref_load_config(const char* text, char* echo, char* base_echo, int cap, char* fp, char* err,
+                    int err_cap) {
+    try {
+        const RunConfig c = load_config_text(text);
+        const std::string e = config_echo(c), b = config_echo(c.baseline()), f = c.task_fingerprint();
+        std::snprintf(echo, cap, "%s", e.c_str());
+        std::snprintf(base_echo, cap, "%s", b.c_str());
+        std::snprintf(fp, 17, "%s", f.c_str());
+        return 0;
+    } catch (const ConfigError& x) {
+        std::snprintf(err, err_cap, "%s", x.what());
+        return 1;
+    } catch (const std::exception& x) {
+        std::snprintf(err, err_cap, "%s", x.what());
+        return 2;
+    }
 }
 
 // rlpipe::run_experiment_in_memory + write_outputs (driver.cpp:228-350):
