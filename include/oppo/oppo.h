@@ -357,6 +357,16 @@ oppo_status oppo_ppo_update(oppo_engine* e, const int64_t* batch_ids, int32_t n,
 /* Free the KV pages / slot of finished sequences. */
 oppo_status oppo_release(oppo_engine* e, const int64_t* ids, int32_t n);
 
+/* Engine checkpoint between steps (the reference keeps its
+ * carry buffer in memory only, driver.cpp:103-195): slot table, page tables,
+ * prompts, tokens / log-probs / values / rewards, cached hidden states, the
+ * KV pages of every admitted sequence in all four models, and the trained
+ * heads.  Load into a fresh engine created with the same configuration
+ * (OPPO_ERR_CONFIG otherwise); the host-side buffer of oppo_seq_state,
+ * Delta controller and tuner state stay the caller's (plain data). */
+oppo_status oppo_engine_save(oppo_engine* e, const char* path);
+oppo_status oppo_engine_load(oppo_engine* e, const char* path);
+
 /* Parity dump of one sequence: tokens, old log-probs, ref log-probs, values (len+1),
  * reward.  cap = room in the token-indexed arrays. */
 oppo_status oppo_read_rollout(oppo_engine* e, int64_t id, int32_t* tokens, float* old_lp,

@@ -2058,6 +2058,158 @@ oppo_status eguard(Engine* e, F&& f) {
     }
 }
 
+// ----------------------------------------------------------- checkpoints
+// Engine state between steps (the carry buffer's device side +
+// KV page tables): which slots hold which sequences, their pages, prompts,
+// tokens / log-probs / values / rewards / cached hidden states, the KV pages
+// they own in every model's pool, and the trained heads.  Weights that are
+// not trained are regenerated from the engine's weight seed, so a checkpoint
+// loads into a fresh engine created with the same configuration.
+constexpr char kCkptMagic[8] = {'O', 'P', 'P', 'O', 'C', 'K', 'P', '1'};
+
+struct CkptSig {  // configuration fields a checkpoint depends on
+    oppo_model_dims dims[N_MODELS];
+    int32_t dtype, S, Pmax, Lmax, page_size, n_pages, train_heads, carry;
+    uint64_t weight_seed, sample_seed;
+};
+
+CkptSig ckpt_sig(const Engine& e) {
+    CkptSig g;
+    std::memset(&g, 0, sizeof(g));
+    for (int i = 0; i < N_MODELS; ++i) g.dims[i] = e.models[i].dims;
+    g.dtype = e.dtype;
+    g.S = e.S;
+    g.Pmax = e.Pmax;
+    g.Lmax = e.Lmax;
+    g.page_size = e.page_size;
+    g.n_pages = e.n_pages;
+    g.train_heads = e.cfg.train_heads;
+    g.carry = e.cfg.carry_granularity;
+    g.weight_seed = e.cfg.weight_seed;
+    g.sample_seed = e.cfg.sample_seed;
+    return g;
+}
+
+struct CkptFile {
+    std::FILE* f;
+    bool writing;
+    CkptFile(const char* path, bool w) : f(std::fopen(path, w ? "wb" : "rb")), writing(w) {
+        if (!f) input_error(std::string("cannot open checkpoint ") + path);
+    }
+    ~CkptFile() {
+        if (f) std::fclose(f);
+    }
+    void raw(void* p, size_t n) {
+        const size_t k = writing ? std::fwrite(p, 1, n, f) : std::fread(p, 1, n, f);
+        if (k != n) input_error(writing ? "checkpoint write failed" : "checkpoint truncated");
+    }
+    template <class V>
+    void pod(V& v) {
+        raw(&v, sizeof(V));
+    }
+    template <class V>
+    void vec(std::vector<V>& v) {
+        uint64_t n = v.size();
+        pod(n);
+        if (!writing) {
+            if (n > (uint64_t(1) << 32)) input_error("checkpoint corrupt");
+            v.resize(n);
+        }
+        if (n) raw(v.data(), n * sizeof(V));
+    }
+    // device range through a host staging buffer
+    void dev(void* d, size_t n) {
+        std::vector<uint8_t> h(n);
+        if (writing) OPPO_CUDA_CHECK(cudaMemcpy(h.data(), d, n, cudaMemcpyDeviceToHost));
+        raw(h.data(), n);
+        if (!writing) OPPO_CUDA_CHECK(cudaMemcpy(d, h.data(), n, cudaMemcpyHostToDevice));
+    }
+    // rows [0, layers) of `width` bytes, `pitch` bytes apart (one KV page over all layers)
+    void dev2d(void* d, size_t pitch, size_t width, size_t rows) {
+        std::vector<uint8_t> h(width * rows);
+        if (writing) OPPO_CUDA_CHECK(cudaMemcpy2D(h.data(), width, d, pitch, width, rows, cudaMemcpyDeviceToHost));
+        raw(h.data(), h.size());
+        if (!writing) OPPO_CUDA_CHECK(cudaMemcpy2D(d, pitch, h.data(), width, width, rows, cudaMemcpyHostToDevice));
+    }
+};
+
+// One routine for both directions keeps the file layout in one place.
+void checkpoint_io(Engine& e, CkptFile& io) {
+    if (e.step_open) input_error("checkpoint inside an open step");
+    OPPO_CUDA_CHECK(cudaDeviceSynchronize());
+    char magic[8];
+    std::memcpy(magic, kCkptMagic, 8);
+    io.raw(magic, 8);
+    if (std::memcmp(magic, kCkptMagic, 8) != 0) input_error("not an oppo checkpoint");
+    CkptSig sig = ckpt_sig(e), cur = sig;
+    io.pod(sig);
+    if (std::memcmp(&sig, &cur, sizeof(sig)) != 0)
+        config_error("checkpoint was written by an engine with another configuration");
+    if (!io.writing && !e.slot_of.empty()) input_error("checkpoint load needs an engine without sequences");
+    // host state
+    io.pod(e.lm_version);
+    io.vec(e.free_slots);
+    io.vec(e.free_pages);
+    std::vector<int32_t> live;
+    if (io.writing)
+        for (int s = 0; s < e.S; ++s)
+            if (e.slots[s].id >= 0) live.push_back(s);
+    io.vec(live);
+    for (int s : live) {
+        if (s < 0 || s >= e.S) input_error("checkpoint corrupt");
+        auto& info = e.slots[s];
+        int32_t flags = (info.ref_pending ? 1 : 0) | (info.scored_prompt ? 2 : 0);
+        io.pod(info.id);
+        io.pod(info.prompt_len);
+        io.pod(info.target_len);
+        io.pod(flags);
+        io.vec(info.pages);
+        if (!io.writing) {
+            info.ref_pending = flags & 1;
+            info.scored_prompt = flags & 2;
+            e.slot_of[info.id] = s;
+        }
+    }
+    // per-slot device arrays (whole: a few MB), cached hidden rows of live slots
+    const size_t S1 = e.S + 1, TS = e.tok_stride;
+    io.dev(e.d_page_table, S1 * e.max_pages * 4);
+    io.dev(e.d_prompt, S1 * e.Pmax * 4);
+    io.dev(e.d_tok, S1 * TS * 4);
+    io.dev(e.d_old_lp, S1 * TS * 4);
+    io.dev(e.d_ref_lp, S1 * TS * 4);
+    io.dev(e.d_values, S1 * TS * 4);
+    io.dev(e.d_reward, S1 * 4);
+    io.dev(e.d_target_len, S1 * 4);
+    io.dev(e.d_ref_pending, S1 * e.models[REF].dims.d_model * e.esz);
+    for (int s : live) {
+        const size_t ra = TS * e.models[ACTOR].dims.d_model * e.esz, rc = TS * e.models[CRITIC].dims.d_model * e.esz;
+        io.dev(static_cast<uint8_t*>(e.d_hf_actor) + s * ra, ra);
+        io.dev(static_cast<uint8_t*>(e.d_hf_critic) + s * rc, rc);
+    }
+    // KV pages owned by live slots, every model and layer
+    for (auto& m : e.models) {
+        if (!m.used) continue;
+        const size_t page_elems = static_cast<size_t>(m.dims.n_kv_heads) * e.page_size * m.dims.head_dim;
+        for (int s : live)
+            for (int pg : e.slots[s].pages)
+                for (void* pool : {m.k_pool, m.v_pool})
+                    io.dev2d(static_cast<uint8_t*>(pool) + pg * page_elems * e.esz, m.layer_stride * e.esz,
+                             page_elems * e.esz, m.dims.n_layers);
+    }
+    // trained heads
+    if (e.cfg.train_heads) {
+        Model& a = e.models[ACTOR];
+        const size_t nw = static_cast<size_t>(a.dims.vocab) * a.dims.d_model;
+        io.dev(a.lm_head, nw * e.esz);
+        if (a.lm_master) io.dev(a.lm_master, nw * 4);
+        io.dev(e.models[CRITIC].head, e.models[CRITIC].dims.d_model * 4);
+    }
+    if (!io.writing) {
+        e.pre_version = -1;  // precomputed policy log-probs are not part of a checkpoint
+        e.pre_index.clear();
+    }
+}
+
 void release_slot(Engine& e, int64_t id) {
     auto it = e.slot_of.find(id);
     if (it == e.slot_of.end()) input_error("release of unknown sequence " + std::to_string(id));
@@ -2163,6 +2315,22 @@ oppo_status oppo_ppo_update(oppo_engine* eh, const int64_t* ids, int32_t n,
         }
         if (e->dtype == OPPO_DTYPE_F32) oppo::ppo_update_impl<float>(*e, slots, *hp, *out);
         else oppo::ppo_update_impl<__nv_bfloat16>(*e, slots, *hp, *out);
+    });
+}
+
+oppo_status oppo_engine_save(oppo_engine* eh, const char* path) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        oppo::CkptFile io(path, true);
+        oppo::checkpoint_io(*e, io);
+    });
+}
+
+oppo_status oppo_engine_load(oppo_engine* eh, const char* path) {
+    Engine* e = reinterpret_cast<Engine*>(eh);
+    return oppo::eguard(e, [&] {
+        oppo::CkptFile io(path, false);
+        oppo::checkpoint_io(*e, io);
     });
 }
 

@@ -117,6 +117,18 @@ class Engine:
         self._check(lib().oppo_ppo_update(self.h, arr, len(ids), C.byref(hp), C.byref(st)))
         return st
 
+    def save(self, path):
+        """oppo_engine_save: slot table, KV pages, rollout buffers, trained heads."""
+        L = lib()
+        L.oppo_engine_save.argtypes = [C.c_void_p, C.c_char_p]
+        self._check(L.oppo_engine_save(self.h, str(path).encode()))
+
+    def load(self, path):
+        """oppo_engine_load into this (fresh, same-configuration) engine."""
+        L = lib()
+        L.oppo_engine_load.argtypes = [C.c_void_p, C.c_char_p]
+        self._check(L.oppo_engine_load(self.h, str(path).encode()))
+
     def release(self, ids):
         arr = (C.c_int64 * max(1, len(ids)))(*ids)
         self._check(lib().oppo_release(self.h, arr, len(ids)))

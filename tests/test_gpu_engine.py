@@ -352,6 +352,68 @@ def test_policy_logprob_precompute_is_bit_identical():
     assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
+def test_engine_checkpoint_resume_is_bit_identical(tmp_path):
+    """oppo_engine_save after a step with carried sequences (token carry: KV
+    pages, partial tokens and log-probs of the stragglers, trained heads),
+    oppo_engine_load into a fresh engine of the same configuration: the next
+    step (refill, decode of the carried and the fresh sequences, scoring,
+    selection, PPO update) is bit-identical on the original and the restored
+    engine; a mismatching configuration is refused."""
+    shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                 vocab=1024, tied=1)
+    P, C, B = 16, 16, 4
+    hp = abi.PpoHparams(gamma=1.0, lambda_=0.95, clip_epsilon=0.2, learning_rate=0.5,
+                        value_learning_rate=0.1, kl_coef=0.05, whiten=1)
+
+    def make(**kw):
+        return Engine(shape, dtype=abi.DTYPE_BF16, max_slots=16, max_prompt_len=P, max_response_len=64,
+                      sample_seed=SAMPLE_SEED, train_heads=1, carry=abi.CARRY_TOKEN, **kw)
+
+    def fresh(ids, lens):
+        return [S.seq_array([dict(id=i, prompt_len=P, target_len=L)])[0] for i, L in zip(ids, lens)]
+
+    def step(eng, entries):
+        active = [e for e in entries if not e.scored]
+        outs, _ = eng.run_step(active, C, abi.MODE_STREAMED, B - (len(entries) - len(active)))
+        batch, entries, _ = S.select_finished(entries, outs, B)
+        ids = [b.id for b in batch]
+        st = eng.ppo_update(ids, hp)
+        ro = [eng.read_rollout(i) for i in ids]
+        eng.release(ids)
+        return entries, ids, (st.ppo_objective, st.kl_mean, st.value_loss, st.mean_reward), ro
+
+    a = make()
+    first = fresh(range(8), [45, 12, 60, 20, 33, 64, 9, 27])
+    a.admit(first)
+    entries, _, _, _ = step(a, first)
+    assert any(e.generated > 0 for e in entries)  # carried stragglers with decoded tokens
+    ck = tmp_path / "engine.ckpt"
+    a.save(ck)
+    b = make()
+    b.load(ck)
+    res = []
+    for eng in (a, b):
+        more = fresh(range(8, 12), [30, 50, 14, 41])
+        eng.admit(more)
+        ents, ids, stats, ro = step(eng, [S.seq_array([e])[0] for e in entries] + more)
+        res.append((ids, stats, ro, eng.get_tensor(0, "lm_head"), eng.get_tensor(2, "head"),
+                    [(e.id, e.generated, e.prefilled_tokens) for e in ents]))
+    (ia, sa, ra, la, ha, ea), (ib, sb, rb, lb, hb, eb) = res
+    assert ia == ib and sa == sb and ea == eb
+    for x, y in zip(ra, rb):
+        assert x["reward"] == y["reward"]
+        for k in ("tokens", "old_lp", "ref_lp", "values"):
+            assert np.array_equal(x[k], y[k]), k
+    assert np.array_equal(la, lb) and np.array_equal(ha, hb)
+    a.close()
+    b.close()
+    c = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=64,
+               sample_seed=SAMPLE_SEED, train_heads=1, carry=abi.CARRY_TOKEN)
+    with pytest.raises(Exception, match="configuration"):
+        c.load(ck)
+    c.close()
+
+
 def test_two_branch_decode_iterations_vs_oracle():
     """Decode iterations split into two concurrent halves (OPPO_DEC_SPLIT_MIN:
     rows [0, M1) on the actor stream, [M1, M) on a second stream, one CUDA
