@@ -149,9 +149,36 @@ def abi_stats():
     return abi.PpoStats()
 
 
+def workload_from_config(path):
+    """A bench workload from a reference-schema JSON run config (+ our optional
+    "model" / "gpu" blocks, paper_2509_25762_b200/config.py): the config's
+    batch, prompt length, Delta range and controller, chunk size and length
+    distribution drive the step loop; the metric stays BASELINE.json's."""
+    from paper_2509_25762_b200 import abi
+    from paper_2509_25762_b200 import config as K
+    c = K.load_config(path, extended=True)
+    if c["lengths"]["kind"] != abi.LEN_LOGNORMAL:
+        raise K.ConfigError("bench --config needs lognormal lengths (the BASELINE workload shape)")
+    model, gpu = c.get("model") or {}, c.get("gpu") or {}
+    actor, scorer = model.get("actor", "0.5b"), model.get("reward", "0.5b")
+    if not isinstance(actor, str) or not isinstance(scorer, str):
+        raise K.ConfigError("bench --config takes engine shape names in model.actor / model.reward")
+    rc = K.to_run_config(c)
+    rc.mode, rc.steps = abi.RUN_TRAIN, 1000
+    rc.carry_granularity = gpu.get("carry", abi.CARRY_TOKEN)
+    rc.ppo.kl_coef, rc.ppo.whiten = gpu.get("kl_coef", 0.05), int(gpu.get("whiten", True))
+    return dict(name=f"config {os.path.basename(path)} (fingerprint {K.task_fingerprint(c)})", actor=actor,
+                scorer=scorer, batch=c["batch_size"], prompt_len=c["prompt_len"], mu=c["lengths"]["mu_log"],
+                sigma=c["lengths"]["sigma_log"], cap=c["lengths"]["cap"], chunk=c["chunk_size"],
+                delta=c["delta_max"], run_cfg=rc, scorer_sms=gpu.get("scorer_sms"))
+
+
 def make_cfg(wl, baseline=False):
     from paper_2509_25762_b200 import abi
     from paper_2509_25762_b200 import scheduler as S
+    if "run_cfg" in wl:
+        cfg = abi.RunConfig.from_buffer_copy(wl["run_cfg"])
+        return S.baseline(cfg) if baseline else cfg
     cfg = S.default_config(
         mode=abi.RUN_TRAIN, steps=1000, batch_size=wl["batch"], prompt_len=wl["prompt_len"],
         delta_init=wl["delta"], delta_min=0, delta_max=wl["delta"], chunk_size=wl["chunk"],
@@ -432,7 +459,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scorer-sms", type=int, default=64,
                     help="fixed SM partition for the scorer stream in the overlapped arm (0: shared)")
+    ap.add_argument("--config", default=None,
+                    help="reference-schema JSON run config (+ model/gpu blocks) instead of --workload")
     args = ap.parse_args()
+    if args.config:
+        wl = workload_from_config(args.config)
+        WORKLOADS["config"] = wl
+        args.workload = "config"
+        if wl.get("scorer_sms") is not None:
+            args.scorer_sms = wl["scorer_sms"]
     if args.impl == "reference":
         reference(args)
     else:

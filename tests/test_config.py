@@ -126,3 +126,18 @@ def test_random_configs_against_live_reference():
     for _ in range(1500):
         text = json.dumps(_mutations(rng, base))
         check(text, R.ref_load_config(text))
+
+
+def test_bench_workload_from_config_matches_cfg2():
+    """configs/cfg2.json (reference schema + model/gpu blocks) drives bench.py
+    --config with exactly the RunConfig of the built-in cfg2 workload."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    wl = bench.workload_from_config(os.path.join(root, "configs", "cfg2.json"))
+    a, b = bench.make_cfg(wl), bench.make_cfg(bench.WORKLOADS["cfg2"])
+    assert bytes(a) == bytes(b)
+    assert bytes(bench.make_cfg(wl, True)) == bytes(bench.make_cfg(bench.WORKLOADS["cfg2"], True))
+    assert (wl["batch"], wl["chunk"], wl["delta"], wl["scorer_sms"]) == (256, 64, 26, 64)
