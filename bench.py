@@ -237,6 +237,20 @@ def gemm_microbench(hbm_peak):
             "avg_launch_us": round(us.value, 3)}
 
 
+def prefill_gemm_microbench(tf_peak):
+    """The scorers' dominant kernel: the prefill gate|up GEMM (tcgen05 + TMA,
+    128x256 tiles, SwiGLU epilogue) at an 8192-row pass, tensor roofline."""
+    from paper_2509_25762_b200._lib import lib
+    M, N, K = 8192, 2 * 4864, 896
+    us = C.c_float()
+    if lib().oppo_k_gemm_bench(M, N, K, 2, 50, 2, C.byref(us)) != 0:
+        return None
+    ach = 2.0 * M * N * K / (us.value * 1e-6) / 1e12
+    return {"kernel": "gemm_bf16_tc<256> (tcgen05+TMA, 2 CTAs/SM) gate|up+SwiGLU, M=8192 N=9728 K=896",
+            "bound": "tensor", "achieved": round(ach, 1), "unit": "TFLOP/s", "peak": tf_peak,
+            "frac": round(ach / tf_peak, 4), "avg_launch_us": round(us.value, 3)}
+
+
 def cpu_baseline(wl, budget_s=12.0):
     """The reference's own path (oracle/_ref = /root/reference core compiled here):
     run_seed in train mode (tabular policy, V=16) at this workload's B / delta /
@@ -392,7 +406,7 @@ def ours(args):
         "prefill_tokens_per_step": int(np.mean([r["prefill_tokens"] for r in rec])),
     }
     line["roofline"] = decode_roofline(rec, hbm, peak_src)
-    line["kernels"] = {"decode_gemm_gate_up": gemm_microbench(hbm)}
+    line["kernels"] = {"decode_gemm_gate_up": gemm_microbench(hbm), "prefill_gemm_gate_up": prefill_gemm_microbench(tflops)}
     line["cpu_baseline"] = cpu_baseline(wl) if not args.no_cpu else None
     if line["cpu_baseline"] is not None and not args.no_cpu:
         # the reference's CPU path runs its toy tabular policy; the same neural
