@@ -938,6 +938,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->rope_epi = env_int("OPPO_ROPE_EPI", 1) != 0;
         e->pre_lp = env_int("OPPO_PRE_LP", 1) != 0;
+        e->g_chunk = std::max(64, env_int("OPPO_G_CHUNK", e->g_chunk)) / 8 * 8;  // update token chunk
         // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
         // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
         e->attn_tp16 = env_int("OPPO_ATTN_TP16", -1);

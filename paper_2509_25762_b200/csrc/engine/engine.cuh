@@ -210,7 +210,7 @@ struct Engine {
     size_t ppo_buf_bytes = 0;
     void* g_buf = nullptr;   // softmax-grad G [V, chunk]
     void* ht_buf = nullptr;  // transposed hidden [d, chunk]
-    int g_chunk = 4096;
+    int g_chunk = 16384;  // update token chunk (OPPO_G_CHUNK): 4096 -> 16384 cut the update 59.7 -> 55.6 ms
     float* vgrad = nullptr;
     float* g_lm = nullptr;   // DP: lm_head gradient buffer (allreduced)
     void* nccl = nullptr;

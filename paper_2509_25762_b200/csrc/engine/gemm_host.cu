@@ -235,7 +235,11 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         return v ? std::atoi(v) : 2048;  // bench sweep 1024/2048/4096/8192: 2048 best by ~0.3%
     }();
     if (ep.mode == EPI_LOGITS || m_tiles > 4) {
-        BN = (ep.mode != EPI_LOGITS && N <= 1024 && M <= narrow_rows) ? 128 : 256;
+        static const int wide_m = [] {  // vocabulary-row GEMMs (the update's dW): M >= this -> 128-wide
+            const char* v = std::getenv("OPPO_NARROW_WIDE_M");
+            return v ? std::atoi(v) : 0;
+        }();
+        BN = (ep.mode != EPI_LOGITS && N <= 1024 && (M <= narrow_rows || (wide_m > 0 && M >= wide_m))) ? 128 : 256;
     } else {
         BN = 64;
         for (int b : {256, 128})
