@@ -42,6 +42,23 @@ def _raise(code, msg):
     raise cls(code, msg)
 
 
+def _preload_nccl():
+    """liboppo.so links libnccl.so.2 by soname.  Load the NCCL that torch
+    ships (pip nvidia-nccl, 2.28) first, so whichever of liboppo and torch is
+    imported first, both bind to it: the system libnccl (2.27) lacks symbols
+    libtorch_cuda needs (ncclDevCommCreate) and would break a later
+    `import torch` if the loader picked it up for liboppo."""
+    try:
+        import nvidia.nccl as nn
+    except ImportError:
+        return
+    for base in getattr(nn, "__path__", []):
+        so = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(so):
+            C.CDLL(so, mode=C.RTLD_GLOBAL)
+            return
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -49,6 +66,7 @@ def lib():
             raise ImportError(
                 f"{LIB_PATH} is not built; run `make -C {_HERE}/csrc` "
                 "(or __graft_entry__.build()). There is no CPU fallback.")
+        _preload_nccl()
         _lib = C.CDLL(LIB_PATH)
         _declare(_lib)
         _check_layout(_lib)

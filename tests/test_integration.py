@@ -51,3 +51,16 @@ def test_rlpipe_adapter_matches_reference_run_step(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "mismatches 0" in r.stdout and "error_mapping ok" in r.stdout
+
+
+def test_liboppo_then_torch_import_order():
+    """Loading liboppo.so before torch must not bind libnccl.so.2 to the
+    system NCCL (2.27: libtorch_cuda then fails on ncclDevCommCreate); _lib
+    preloads the NCCL torch ships.  Runs in a fresh interpreter."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("from paper_2509_25762_b200 import _lib; _lib.lib(); import torch; "
+            "print('ok', torch.__version__)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
