@@ -219,7 +219,11 @@ void make_sm_partition(Engine& e, int scorer_sms, int prio_hi, int prio_lo) {
     OPPO_CU_CHECK(driver_fn<GenDesc>("cuDevResourceGenerateDesc")(&da, &rest, 1));
     OPPO_CU_CHECK(driver_fn<GCreate>("cuGreenCtxCreate")(&e.gctx_scorer, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM));
     OPPO_CU_CHECK(driver_fn<GCreate>("cuGreenCtxCreate")(&e.gctx_actor, da, dev, CU_GREEN_CTX_DEFAULT_STREAM));
-    CUstream a, a2, s;
+    CUstream a, a2, s, s1, s2;
+    OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&s1, e.gctx_scorer, CU_STREAM_NON_BLOCKING, prio_lo));
+    OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&s2, e.gctx_scorer, CU_STREAM_NON_BLOCKING, prio_lo));
+    e.ss_m[0] = reinterpret_cast<cudaStream_t>(s1);
+    e.ss_m[1] = reinterpret_cast<cudaStream_t>(s2);
     OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&a, e.gctx_actor, CU_STREAM_NON_BLOCKING, prio_hi));
     OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&a2, e.gctx_actor, CU_STREAM_NON_BLOCKING, prio_hi));
     OPPO_CU_CHECK(driver_fn<GStream>("cuGreenCtxStreamCreate")(&s, e.gctx_scorer, CU_STREAM_NON_BLOCKING, prio_lo));
@@ -839,11 +843,12 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa, cudaStreamNonBlocking, hi));
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->sa2, cudaStreamNonBlocking, hi));
             OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&e->ss, cudaStreamNonBlocking, lo));
+            for (auto& sm : e->ss_m) OPPO_CUDA_CHECK(cudaStreamCreateWithPriority(&sm, cudaStreamNonBlocking, lo));
             e->su = e->sa;
         }
         for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
-        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join, &e->ev_pre})
+        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join, &e->ev_pre, &e->ev_seg, &e->ev_m[0], &e->ev_m[1]})
             OPPO_CUDA_CHECK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
 
         e->S = cfg.max_slots;
@@ -912,6 +917,14 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         e->wa.sms = e->sms_actor;
         e->ws.sms = e->sms_scorer;
+        // reward | critic | reference passes concurrently on three scorer streams:
+        // score end 1145 -> 1119 ms per cfg2 step (profiles/r01_experiments.txt)
+        e->scorer_streams = env_int("OPPO_SCORER_STREAMS", 3) >= 3 ? 3 : 1;
+        for (int k = 0; k < 2 && e->scorer_streams == 3; ++k) {
+            if (e->dtype == OPPO_DTYPE_F32) alloc_work<float>(*e, e->ws_m[k], e->prefill_rows, true);
+            else alloc_work<__nv_bfloat16>(*e, e->ws_m[k], e->prefill_rows, true);
+            e->ws_m[k].sms = e->sms_scorer;
+        }
         // two-branch decode iterations (bf16): the rows split in halves that run
         // concurrently on sa / sa2, each half's launch latencies hidden behind
         // the other's kernels (the weights are streamed twice)
@@ -937,7 +950,9 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_w8_tenths = env_int("OPPO_ATTN_W8_TENTHS", 20);  // auto: 8 warps up to 2.0 CTAs/SM
         e->dec_qkv_max = env_int("OPPO_DEC_QKV_MAX", 96);
         e->rope_epi = env_int("OPPO_ROPE_EPI", 1) != 0;
-        e->pre_lp = env_int("OPPO_PRE_LP", 1) != 0;
+        // off: with concurrent scorer passes the scorers finish within ~8 ms of
+        // decode, shorter than the precompute on the actor SMs (215.4 vs 213.6)
+        e->pre_lp = env_int("OPPO_PRE_LP", 0) != 0;
         e->g_chunk = std::max(64, env_int("OPPO_G_CHUNK", e->g_chunk)) / 8 * 8;  // update token chunk
         // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
         // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
@@ -995,7 +1010,11 @@ void engine_free(Engine* e) {
                     static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
-    for (Work* w : {&e->wa, &e->wa2, &e->ws}) free_work(*w);
+    for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) free_work(*w);
+    for (cudaEvent_t ev : {e->ev_seg, e->ev_m[0], e->ev_m[1]})
+        if (ev) cudaEventDestroy(ev);
+    for (cudaStream_t sm : e->ss_m)
+        if (sm) cudaStreamDestroy(sm);
     for (cudaEvent_t ev : {e->ev_begin, e->ev_dec_end, e->ev_sc_end, e->ev_done, e->ev_loop0, e->ev_fork, e->ev_join,
                            e->ev_pre})
         if (ev) cudaEventDestroy(ev);
@@ -1252,6 +1271,21 @@ void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, in
                                           e.tok_stride, w.meta);
     const QBlock* qb = A.at<QBlock>(p.qb_off);
     tokens += p.rows;
+    // three concurrent model passes: critic and reference on their own
+    // streams / workspaces (row metadata shared), joined before the next
+    // pass rewrites the metadata
+    const bool conc = e.scorer_streams == 3;
+    Work wc = conc ? e.ws_m[0] : w, wr = conc ? e.ws_m[1] : w;
+    cudaStream_t sc = st, sr = st;
+    if (conc) {
+        wc.meta = w.meta;
+        wr.meta = w.meta;
+        sc = e.ss_m[0];
+        sr = e.ss_m[1];
+        OPPO_CUDA_CHECK(cudaEventRecord(e.ev_seg, st));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(sc, e.ev_seg, 0));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(sr, e.ev_seg, 0));
+    }
     // reward model: last-token scalar head
     {
         Final<T> fin;
@@ -1269,8 +1303,8 @@ void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, in
         fin.cache = static_cast<T*>(e.d_hf_critic);
         fin.t_lo = 1;
         fin.t_hi = e.Lmax;
-        forward<T>(e, e.models[CRITIC], w, st, p.rows, false, 0, qb, p.n_qb, fin);
-        scatter_rows<<<cdiv(p.rows, 256), 256, 0, st>>>(w.head_out, w.meta.slot, w.meta.t, p.rows,
+        forward<T>(e, e.models[CRITIC], wc, sc, p.rows, false, 0, qb, p.n_qb, fin);
+        scatter_rows<<<cdiv(p.rows, 256), 256, 0, sc>>>(wc.head_out, wc.meta.slot, wc.meta.t, p.rows,
                                                         e.d_values, e.tok_stride, 1, e.d_target_len, 0);
     }
     // reference: log-probs of the actor's tokens (lm_head + log-sum-exp)
@@ -1278,30 +1312,36 @@ void run_scorer_pass(Engine& e, const PassPlan& p, Arena& A, cudaStream_t st, in
         Model& m = e.models[REF];
         Final<T> fin;
         fin.write_h = true;
-        forward<T>(e, m, w, st, p.rows, false, 0, qb, p.n_qb, fin);
+        forward<T>(e, m, wr, sr, p.rows, false, 0, qb, p.n_qb, fin);
         const int D = m.dims.d_model;
         if (p.n_lm > 0) {
-            gather_lm_rows<T><<<p.n_lm, 128, 0, st>>>(A.at<LmRow>(p.lm_off), p.n_lm,
-                                                      static_cast<const T*>(w.h),
+            gather_lm_rows<T><<<p.n_lm, 128, 0, sr>>>(A.at<LmRow>(p.lm_off), p.n_lm,
+                                                      static_cast<const T*>(wr.h),
                                                       static_cast<const T*>(e.d_ref_pending), D,
-                                                      e.d_tok, e.tok_stride, static_cast<T*>(w.lm_in),
-                                                      w.lm_tgt, w.lm_slot, w.lm_t);
+                                                      e.d_tok, e.tok_stride, static_cast<T*>(wr.lm_in),
+                                                      wr.lm_tgt, wr.lm_slot, wr.lm_t);
             EpiParams ep{};
             ep.mode = EPI_LOGITS;
-            ep.partials = w.partials;
-            ep.tgt_logit = w.tgt_logit;
-            ep.targets = w.lm_tgt;
+            ep.partials = wr.partials;
+            ep.tgt_logit = wr.tgt_logit;
+            ep.targets = wr.lm_tgt;
             ep.keys = nullptr;
-            gemm_run(e, w, st, w.lm_in, p.n_lm, D, D, m.lm_head, m.dims.vocab, D, ep);
-            logits_combine<<<cdiv(p.n_lm, 4), 128, 0, st>>>(
-                w.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, p.n_lm, nullptr, w.tgt_logit, w.lm_slot, w.lm_t,
+            gemm_run(e, wr, sr, wr.lm_in, p.n_lm, D, D, m.lm_head, m.dims.vocab, D, ep);
+            logits_combine<<<cdiv(p.n_lm, 4), 128, 0, sr>>>(
+                wr.partials, gemm_logit_tiles(e.dtype, m.dims.vocab), m.dims.vocab, p.n_lm, nullptr, wr.tgt_logit, wr.lm_slot, wr.lm_t,
                 nullptr, e.d_ref_lp, e.tok_stride, nullptr, nullptr);
         }
         if (p.n_pend > 0)
-            store_pending<T><<<p.n_pend, 128, 0, st>>>(A.at<int32_t>(p.pend_off),
+            store_pending<T><<<p.n_pend, 128, 0, sr>>>(A.at<int32_t>(p.pend_off),
                                                        A.at<int32_t>(p.pend_off) + p.n_pend, p.n_pend,
-                                                       static_cast<const T*>(w.h),
+                                                       static_cast<const T*>(wr.h),
                                                        static_cast<T*>(e.d_ref_pending), D);
+    }
+    if (conc) {  // the next pass's segment_rows rewrites the shared metadata
+        OPPO_CUDA_CHECK(cudaEventRecord(e.ev_m[0], sc));
+        OPPO_CUDA_CHECK(cudaEventRecord(e.ev_m[1], sr));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(st, e.ev_m[0], 0));
+        OPPO_CUDA_CHECK(cudaStreamWaitEvent(st, e.ev_m[1], 0));
     }
     e.launches += 8;
     OPPO_CUDA_CHECK(cudaGetLastError());

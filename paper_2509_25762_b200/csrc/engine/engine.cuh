@@ -140,11 +140,17 @@ struct Engine {
 
     Work wa, ws;                        // actor decode / scorer prefill
     Work wa2;                           // second decode branch (split iterations), rows view into wa.meta
+    // concurrent scorer models: critic and reference passes on their own
+    // streams (scorer SMs) and workspaces, reading the reward pass's row metadata
+    int scorer_streams = 1;
+    Work ws_m[2];
+    cudaStream_t ss_m[2] = {nullptr, nullptr};
+    cudaEvent_t ev_seg = nullptr, ev_m[2] = {nullptr, nullptr};
     // Policy log-probs (and log-sum-exp) of the sampled tokens of every sequence
     // that finished in the last step, computed on the actor SMs while the
     // scorers finish their last wave; oppo_ppo_update reuses them when the
     // lm_head has not changed since (pre_version == lm_version).
-    bool pre_lp = true;
+    bool pre_lp = false;
     int64_t lm_version = 0, pre_version = -1;
     std::unordered_map<int64_t, std::pair<int, int>> pre_index;  // seq id -> (token offset, tokens)
     size_t pre_cap = 0;                 // tokens

@@ -239,7 +239,8 @@ def test_ppo_update_vs_oracle_fp32():
     eng.close()
 
 
-@pytest.mark.parametrize("attn_env", ["", "OPPO_ATTN_TP16=1", "OPPO_ATTN_WARPS=8", "OPPO_ATTN_WARPS=4"])
+@pytest.mark.parametrize("attn_env", ["", "OPPO_ATTN_TP16=1", "OPPO_ATTN_WARPS=8", "OPPO_ATTN_WARPS=4",
+                                      "OPPO_SCORER_STREAMS=3"])
 def test_gqa_05b_width_bf16_vs_oracle(attn_env):
     """0.5B geometry (d=896, 14 q heads over 2 kv heads, head_dim 64, SwiGLU
     4864) at 2 layers / small vocabulary: tensor-core attention (decode and
