@@ -928,7 +928,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         // two-branch decode iterations (bf16): the rows split in halves that run
         // concurrently on sa / sa2, each half's launch latencies hidden behind
         // the other's kernels (the weights are streamed twice)
-        e->dec_split_min = env_int("OPPO_DEC_SPLIT_MIN", 176);  // measured: wins from ~192 rows
+        e->dec_split_min = env_int("OPPO_DEC_SPLIT_MIN", 144);  // bench sweep 96/128/144/176/208: 144 best
         if (e->dec_split_min > 0 && e->dtype == OPPO_DTYPE_BF16) {
             alloc_work<__nv_bfloat16>(*e, e->wa2, std::max(e->S + 16, 32), false);
             e->wa2.sms = e->sms_actor;
