@@ -173,13 +173,20 @@ def workload_from_config(path):
                 delta=c["delta_max"], run_cfg=rc, scorer_sms=gpu.get("scorer_sms"))
 
 
-def make_cfg(wl, baseline=False):
+def make_cfg(wl, baseline=False, ref_side=False):
+    """The workload's RunConfig.  ref_side: built by the reference library
+    (oracle/_ref) alone, so the reference arm never maps liboppo.so."""
     from paper_2509_25762_b200 import abi
-    from paper_2509_25762_b200 import scheduler as S
+    if ref_side:
+        from oracle import ref as R
+        default_config, base_fn = R.default_config, R.baseline_config
+    else:
+        from paper_2509_25762_b200 import scheduler as S
+        default_config, base_fn = S.default_config, S.baseline
     if "run_cfg" in wl:
         cfg = abi.RunConfig.from_buffer_copy(wl["run_cfg"])
-        return S.baseline(cfg) if baseline else cfg
-    cfg = S.default_config(
+        return base_fn(cfg) if baseline else cfg
+    cfg = default_config(
         mode=abi.RUN_TRAIN, steps=1000, batch_size=wl["batch"], prompt_len=wl["prompt_len"],
         delta_init=wl["delta"], delta_min=0, delta_max=wl["delta"], chunk_size=wl["chunk"],
         schedule_mode=abi.MODE_STREAMED, carry_granularity=abi.CARRY_TOKEN,
@@ -188,7 +195,7 @@ def make_cfg(wl, baseline=False):
         latency_reward_residual=0, latency_placement=abi.PLACE_DISAGGREGATED,
         ppo_gamma=1.0, ppo_lambda=0.95, ppo_clip_epsilon=0.2, ppo_learning_rate=1e-3,
         ppo_value_learning_rate=1e-3, ppo_kl_coef=0.05, ppo_whiten=1)
-    return S.baseline(cfg) if baseline else cfg
+    return base_fn(cfg) if baseline else cfg
 
 
 def decode_roofline(recs, hbm_peak, peak_src):
@@ -259,10 +266,9 @@ def cpu_baseline(wl, budget_s=12.0):
         from oracle import ref as R
         if not R.available():
             return None
-        from paper_2509_25762_b200 import abi
         from paper_2509_25762_b200 import scheduler as S
         cores = os.cpu_count() or 1
-        cfg = make_cfg(wl)
+        cfg = make_cfg(wl, ref_side=True)
         S.set_field(cfg, "vocab", 16)
         S.set_field(cfg, "ppo_learning_rate", 0.1)
         S.set_field(cfg, "ppo_value_learning_rate", 0.2)
@@ -432,7 +438,7 @@ def reference(args):
         if not R.available():
             raise FileNotFoundError("oracle/_ref/librlpipe_ref.so not built")
         cores = os.cpu_count() or 1
-        cfg = make_cfg(wl)
+        cfg = make_cfg(wl, ref_side=True)
         S.set_field(cfg, "vocab", 16)
         S.set_field(cfg, "ppo_learning_rate", 0.1)
         S.set_field(cfg, "ppo_value_learning_rate", 0.2)

@@ -147,8 +147,13 @@ typedef struct oppo_ppo_hparams {
     double value_learning_rate;
     double kl_coef;      /* 0 -> terminal reward only, as the reference */
     int32_t whiten;      /* 0 -> raw GAE advantages, as the reference    */
-    int32_t _pad;
+    int32_t value_target; /* critic regression target: OPPO_VALUE_MC_RETURN (0): gamma-discounted
+                             return of the terminal reward, as the reference's value fit
+                             (ppo.cpp:296-314); OPPO_VALUE_GAE_RETURN (1): GAE lambda-return
+                             adv + V of the KL-shaped rewards (TRL style) */
 } oppo_ppo_hparams;
+#define OPPO_VALUE_MC_RETURN 0
+#define OPPO_VALUE_GAE_RETURN 1
 
 #define OPPO_MAX_CANDIDATES 16
 /* rlpipe::RunConfig (config.hpp:28-77), the fields the hot path reads. */

@@ -101,9 +101,11 @@ inline std::pair<rlpipe::StepTimeline, rlpipe::ResourceLedger> run_step(
     std::vector<oppo_seq_outcome> out(c.size());
     oppo_ledger led{};
     const int32_t stop = stop_after ? *stop_after : static_cast<int32_t>(c.size());
-    check(oppo_run_step(e, c.data(), static_cast<int32_t>(c.size()), schedule.chunk_size,
-                        mode_of(schedule), stop, out.data(), &led),
-          oppo_last_error(e));
+    // status first: argument evaluation order is unspecified, and the error
+    // string must be read after the call that sets it
+    const oppo_status st = oppo_run_step(e, c.data(), static_cast<int32_t>(c.size()),
+                                         schedule.chunk_size, mode_of(schedule), stop, out.data(), &led);
+    check(st, st == OPPO_OK ? nullptr : oppo_last_error(e));
     return finish(out, led);
 }
 
@@ -116,9 +118,10 @@ inline std::pair<rlpipe::StepTimeline, rlpipe::ResourceLedger> run_step_logical(
     std::vector<oppo_seq_outcome> out(c.size());
     oppo_ledger led{};
     const int32_t stop = stop_after ? *stop_after : static_cast<int32_t>(c.size());
-    check(oppo_plan_step(c.data(), static_cast<int32_t>(c.size()), schedule.chunk_size,
-                         mode_of(schedule), stop, carry, out.data(), &led),
-          oppo_last_error_global());
+    const oppo_status st = oppo_plan_step(c.data(), static_cast<int32_t>(c.size()),
+                                          schedule.chunk_size, mode_of(schedule), stop, carry,
+                                          out.data(), &led);
+    check(st, st == OPPO_OK ? nullptr : oppo_last_error_global());
     return finish(out, led);
 }
 

@@ -42,6 +42,8 @@ def ref():
             "ref_tuner_replay": (i32, [P(i32), i32, i32, P(i32), P(dbl), i32, P(i32)]),
             "ref_run_seed": (i32, [P(abi.RunConfig), u64, P(abi.StepRecord), P(i32), P(i32)]),
             "ref_run_seeds_parallel": (i32, [P(abi.RunConfig), P(u64), i32, P(i64)]),
+            "ref_run_config_default": (i32, [P(abi.RunConfig)]),
+            "ref_run_config_baseline": (i32, [P(abi.RunConfig), P(abi.RunConfig)]),
             "ref_write_outputs": (i32, [P(abi.RunConfig), P(u64), i32, C.c_char_p]),
             "ref_load_config": (i32, [C.c_char_p, C.c_char_p, C.c_char_p, i32, C.c_char_p, C.c_char_p,
                                       i32]),
@@ -137,6 +139,25 @@ def trace_seed(cfg, seed, buf_cap=0):
                     for i in range(n.value)]
     return (list(recs[:n.value]), [list(sel[i * b:(i + 1) * b]) for i in range(n.value)],
             out_bufs)
+
+
+def default_config(**overrides):
+    """rlpipe::RunConfig{} (config.hpp:28-77) from the reference itself, with
+    the same keyword overrides as scheduler.default_config; never touches
+    liboppo.so (the reference arm of bench.py must not map the product)."""
+    from paper_2509_25762_b200.scheduler import set_field  # pure ctypes field setter
+    cfg = abi.RunConfig()
+    rcheck(ref().ref_run_config_default(C.byref(cfg)))
+    for k, v in overrides.items():
+        set_field(cfg, k, v)
+    return cfg
+
+
+def baseline_config(cfg):
+    """rlpipe::RunConfig::baseline (config.cpp:411-420) from the reference."""
+    out = abi.RunConfig()
+    rcheck(ref().ref_run_config_baseline(C.byref(cfg), C.byref(out)))
+    return out
 
 
 def run_seeds_parallel(cfg, seeds):

@@ -121,6 +121,80 @@ RunConfig to_ref(const oppo_run_config& c) {
     return r;
 }
 
+oppo_length_dist from_ref(const LengthDistribution& d) {
+    oppo_length_dist r{};
+    r.kind = static_cast<int32_t>(d.kind);
+    r.fast_len = d.fast_len;
+    r.slow_len = d.slow_len;
+    r.p_slow = d.p_slow;
+    r.mu_log = d.mu_log;
+    r.sigma_log = d.sigma_log;
+    r.cap = d.cap;
+    r.table_n = 0;
+    for (const auto& [len, w] : d.table) {
+        if (r.table_n >= static_cast<int>(sizeof(r.table_len) / sizeof(r.table_len[0]))) break;
+        r.table_len[r.table_n] = len;
+        r.table_w[r.table_n] = w;
+        ++r.table_n;
+    }
+    return r;
+}
+
+oppo_latency from_ref(const LatencyModel& m) {
+    oppo_latency l{};
+    l.decode_per_token = m.decode_per_token;
+    l.prefill_per_token = m.prefill_per_token;
+    l.reward_residual = m.reward_residual;
+    l.chunk_switch_cost = m.chunk_switch_cost;
+    l.transfer_per_chunk = m.transfer_per_chunk;
+    l.placement = static_cast<int32_t>(m.placement);
+    l.count_prompt_in_prefill = m.count_prompt_in_prefill ? 1 : 0;
+    return l;
+}
+
+// rlpipe::RunConfig as the C struct (inverse of to_ref), so the reference arm
+// of bench.py builds its configs from the reference alone.
+void from_ref(const RunConfig& r, oppo_run_config& c) {
+    std::memset(&c, 0, sizeof(c));
+    c.mode = static_cast<int32_t>(r.mode);
+    c.steps = r.steps;
+    c.batch_size = r.batch_size;
+    c.prompt_len = r.prompt_len;
+    c.prompt_count = r.prompt_count;
+    c.delta_init = r.delta_init;
+    c.delta_min = r.delta_min;
+    c.delta_max = r.delta_max;
+    c.controller = static_cast<int32_t>(r.controller);
+    c.window = r.window;
+    c.delta_inc = r.delta_inc;
+    c.delta_dec = r.delta_dec;
+    c.chunk_size = r.chunk_size;
+    c.schedule_mode = static_cast<int32_t>(r.schedule_mode);
+    c.tune_chunks = r.tune_chunks ? 1 : 0;
+    c.n_candidates = 0;
+    for (int x : r.chunk_candidates) {
+        if (c.n_candidates >= static_cast<int>(sizeof(c.chunk_candidates) / sizeof(c.chunk_candidates[0]))) break;
+        c.chunk_candidates[c.n_candidates++] = x;
+    }
+    c.retune_period = r.retune_period;
+    c.latency = from_ref(r.latency);
+    c.lengths = from_ref(r.lengths);
+    c.ppo.gamma = r.ppo.gamma;
+    c.ppo.lambda = r.ppo.lambda;
+    c.ppo.clip_epsilon = r.ppo.clip_epsilon;
+    c.ppo.learning_rate = r.ppo.learning_rate;
+    c.ppo.value_learning_rate = r.ppo.value_learning_rate;
+    c.vocab = r.vocab;
+    c.target_token = r.target_token;
+    c.reward_scale = r.reward_scale;
+    c.reward_bias = r.reward_bias;
+    c.proxy_kind = static_cast<int32_t>(r.reward_proxy.kind);
+    c.proxy_value = r.reward_proxy.value;
+    c.proxy_ramp_scale = r.reward_proxy.ramp_scale;
+    c.proxy_ramp_steps = r.reward_proxy.ramp_steps;
+    c.fail_after_step = r.fail_after_step;
+}
+
 SequenceState to_ref(const oppo_seq_state& s) {
     SequenceState r;
     r.prompt.id = s.id;
@@ -344,6 +418,21 @@ int ref_write_outputs(const oppo_run_config* cfg, const uint64_t* seeds, int n_s
         config.seeds.assign(seeds, seeds + n_seeds);
         const auto exp = run_experiment_in_memory(config);
         write_outputs(exp, std::filesystem::path(dir));
+    });
+}
+
+// RunConfig{} defaults (config.hpp:28-77); with base != 0, of RunConfig::baseline()
+// applied to *cfg (config.cpp:411-420).
+int ref_run_config_default(oppo_run_config* out) {
+    return guard([&] { from_ref(RunConfig{}, *out); });
+}
+int ref_run_config_baseline(const oppo_run_config* cfg, oppo_run_config* out) {
+    return guard([&] {
+        const RunConfig b = to_ref(*cfg).baseline();
+        oppo_run_config c{};
+        from_ref(b, c);
+        c.carry_granularity = cfg->carry_granularity;  // engine-side field, not in rlpipe
+        *out = c;
     });
 }
 

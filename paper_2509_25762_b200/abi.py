@@ -70,7 +70,10 @@ class LengthDist(C.Structure):
 class PpoHparams(C.Structure):
     _fields_ = [("gamma", C.c_double), ("lambda_", C.c_double), ("clip_epsilon", C.c_double),
                 ("learning_rate", C.c_double), ("value_learning_rate", C.c_double),
-                ("kl_coef", C.c_double), ("whiten", C.c_int32), ("_pad", C.c_int32)]
+                ("kl_coef", C.c_double), ("whiten", C.c_int32), ("value_target", C.c_int32)]
+
+
+VALUE_MC_RETURN, VALUE_GAE_RETURN = 0, 1
 
 
 class RunConfig(C.Structure):

@@ -59,6 +59,7 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
     size_t cap = 0;
     uint8_t* pinned = nullptr;
     size_t pinned_cap = 0;
+    cudaEvent_t copied = nullptr;  // the last upload's H2D copy (pinned staging reuse)
     size_t push(const void* p, size_t bytes) {
         const size_t off = (host.size() + 255) & ~size_t(255);
         host.resize(off + bytes);
@@ -75,6 +76,8 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
             cap = host.size() * 2;
             dev = dalloc(cap);
         }
+        if (copied) OPPO_CUDA_CHECK(cudaEventSynchronize(copied));  // staging no longer read
+        else OPPO_CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
         if (host.size() > pinned_cap) {
             if (pinned) cudaFreeHost(pinned);
             pinned_cap = host.size() * 2;
@@ -83,10 +86,13 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
         std::memcpy(pinned, host.data(), host.size());
         if (!host.empty())
             OPPO_CUDA_CHECK(cudaMemcpyAsync(dev, pinned, host.size(), cudaMemcpyHostToDevice, st));
+        OPPO_CUDA_CHECK(cudaEventRecord(copied, st));
     }
     void release() {
         if (dev) cudaFree(dev);
         if (pinned) cudaFreeHost(pinned);
+        if (copied) cudaEventDestroy(copied);
+        copied = nullptr;
         dev = nullptr;
         pinned = nullptr;
         cap = pinned_cap = 0;
@@ -848,7 +854,8 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         }
         for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_dec_end, &e->ev_sc_end, &e->ev_done, &e->ev_loop0})
             OPPO_CUDA_CHECK(cudaEventCreate(ev));
-        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join, &e->ev_pre, &e->ev_seg, &e->ev_m[0], &e->ev_m[1]})
+        for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_join, &e->ev_pre, &e->ev_seg, &e->ev_m[0], &e->ev_m[1],
+                                 &e->ev_admit})
             OPPO_CUDA_CHECK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
 
         e->S = cfg.max_slots;
@@ -1011,7 +1018,7 @@ void engine_free(Engine* e) {
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) free_work(*w);
-    for (cudaEvent_t ev : {e->ev_seg, e->ev_m[0], e->ev_m[1]})
+    for (cudaEvent_t ev : {e->ev_seg, e->ev_m[0], e->ev_m[1], e->ev_admit})
         if (ev) cudaEventDestroy(ev);
     for (cudaStream_t sm : e->ss_m)
         if (sm) cudaStreamDestroy(sm);
@@ -1059,15 +1066,34 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
     std::vector<int64_t> ids;
     std::vector<int32_t> pt_rows;  // page-table rows, S x max_pages layout subset
     std::vector<int32_t> tlen;
+    // Validate the whole batch before touching any host state, so a rejected
+    // admission leaves the engine exactly as it was (no half-registered
+    // sequences pointing at stale device rows).
+    {
+        std::unordered_map<int64_t, int> seen;
+        size_t pages_needed = 0, tot = 0;
+        for (int i = 0; i < n; ++i) {
+            const auto& s = seqs[i];
+            if (e.slot_of.count(s.id) || seen.count(s.id))
+                input_error("sequence " + std::to_string(s.id) + " already admitted");
+            seen[s.id] = i;
+            if (s.prompt_len < 1 || s.prompt_len > e.Pmax) input_error("prompt_len outside [1, max_prompt_len]");
+            if (s.target_len < 1 || s.target_len > e.Lmax)
+                input_error("target_len outside [1, max_response_len]");
+            pages_needed += cdiv(s.prompt_len + s.target_len + 1, e.page_size);
+            tot += s.prompt_len;
+        }
+        if (static_cast<size_t>(n) > e.free_slots.size()) input_error("no free slot (raise max_slots)");
+        if (pages_needed > e.free_pages.size()) input_error("KV page pool exhausted");
+        if (prompts) {
+            const int V = e.models[ACTOR].dims.vocab;
+            for (size_t i = 0; i < tot; ++i)
+                if (prompts[i] < 0 || prompts[i] >= V) input_error("prompt token outside the vocabulary");
+        }
+    }
     for (int i = 0; i < n; ++i) {
         const auto& s = seqs[i];
-        if (e.slot_of.count(s.id)) input_error("sequence " + std::to_string(s.id) + " already admitted");
-        if (s.prompt_len < 1 || s.prompt_len > e.Pmax) input_error("prompt_len outside [1, max_prompt_len]");
-        if (s.target_len < 1 || s.target_len > e.Lmax)
-            input_error("target_len outside [1, max_response_len]");
-        if (e.free_slots.empty()) input_error("no free slot (raise max_slots)");
         const int need = cdiv(s.prompt_len + s.target_len + 1, e.page_size);
-        if (static_cast<int>(e.free_pages.size()) < need) input_error("KV page pool exhausted");
         const int slot = e.free_slots.back();
         e.free_slots.pop_back();
         auto& info = e.slots[slot];
@@ -1100,9 +1126,6 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
     if (prompts) {
         size_t tot = 0;
         for (int i = 0; i < n; ++i) tot += lens[i];
-        const int V = e.models[ACTOR].dims.vocab;
-        for (size_t i = 0; i < tot; ++i)
-            if (prompts[i] < 0 || prompts[i] >= V) input_error("prompt token outside the vocabulary");
         o_prompts = A.push(prompts, tot * 4);
     }
     // actor prompt prefill: positions 0..P-2 (the last prompt token feeds decode step 1)
@@ -1117,20 +1140,43 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
             qbs.push_back({rows_total + b, std::min(e.qblock, np - b), slots[i], b});
         rows_total += np;
     }
-    const size_t o_segs = A.push_vec(segs), o_qbs = A.push_vec(qbs);
+    // prefill in passes of <= ws.max_rows rows (segments are whole prompts);
+    // every pass's metadata rides the one admission upload, so the passes run
+    // back to back on su without host round trips
+    Work& w = e.ws;  // the scorer workspace has prefill-sized buffers; the scorer stream is idle
+    struct AdmitPass { size_t o_seg, o_qb; int n_seg, n_qb, rows; };
+    std::vector<AdmitPass> passes;
+    for (size_t si = 0; si < segs.size();) {
+        size_t sj = si;
+        int rows_pass = 0;
+        while (sj < segs.size() && (rows_pass + segs[sj].n <= w.max_rows || sj == si)) {
+            rows_pass += segs[sj].n;
+            ++sj;
+        }
+        if (rows_pass > w.max_rows) input_error("prompt longer than the prefill workspace");
+        std::vector<Segment> ps(segs.begin() + si, segs.begin() + sj);
+        std::vector<QBlock> pq;
+        const int base = segs[si].row0;
+        for (auto& sg : ps) sg.row0 -= base;
+        for (const auto& q : qbs)
+            if (q.row0 >= base && q.row0 < base + rows_pass) {
+                QBlock bq = q;
+                bq.row0 -= base;
+                pq.push_back(bq);
+            }
+        passes.push_back({A.push_vec(ps), A.push_vec(pq), static_cast<int>(ps.size()),
+                          static_cast<int>(pq.size()), rows_pass});
+        si = sj;
+    }
     A.upload(e.su);
-    cudaStream_t st = e.su;  // admission prefill: whole GPU (host-synchronised below)
+    cudaStream_t st = e.su;  // admission prefill: whole GPU
     for (int i = 0; i < n; ++i)
         OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_page_table + static_cast<size_t>(slots[i]) * e.max_pages,
                                         A.at<int32_t>(o_rows) + static_cast<size_t>(i) * e.max_pages,
                                         e.max_pages * 4, cudaMemcpyDeviceToDevice, st));
-    // target lengths
-    {
-        // scatter target_len by slot
-        for (int i = 0; i < n; ++i)
-            OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_target_len + slots[i], A.at<int32_t>(o_tlen) + i, 4,
-                                            cudaMemcpyDeviceToDevice, st));
-    }
+    for (int i = 0; i < n; ++i)  // target lengths, scattered by slot
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(e.d_target_len + slots[i], A.at<int32_t>(o_tlen) + i, 4,
+                                        cudaMemcpyDeviceToDevice, st));
     if (prompts) {
         size_t off = 0;
         for (int i = 0; i < n; ++i) {
@@ -1144,46 +1190,19 @@ void admit_impl(Engine& e, const oppo_seq_state* seqs, int n, const int32_t* pro
                                          A.at<int64_t>(o_ids), A.at<int32_t>(o_lens), n,
                                          e.cfg.sample_seed, e.models[ACTOR].dims.vocab);
     }
-    // prefill in passes of <= wa.max_rows rows (segments are whole prompts here)
-    Work& w = e.ws;  // the scorer workspace has prefill-sized buffers; the scorer stream is idle
-    size_t si = 0;
-    while (si < segs.size()) {
-        size_t sj = si;
-        int rows_pass = 0;
-        while (sj < segs.size() && (rows_pass + segs[sj].n <= w.max_rows || sj == si)) {
-            rows_pass += segs[sj].n;
-            ++sj;
-        }
-        if (rows_pass > w.max_rows) input_error("prompt longer than the prefill workspace");
-        // rebase rows of this pass
-        std::vector<Segment> ps(segs.begin() + si, segs.begin() + sj);
-        std::vector<QBlock> pq;
-        const int base = segs[si].row0;
-        for (auto& s : ps) s.row0 -= base;
-        for (const auto& q : qbs)
-            if (q.row0 >= base && q.row0 < base + rows_pass) {
-                QBlock b = q;
-                b.row0 -= base;
-                pq.push_back(b);
-            }
-        auto& B = g_extra[&e].step_arena;  // reuse step arena's device buffer is unsafe; use pass-local upload
-        (void)B;
-        Arena pa;
-        pa.push_vec(ps);
-        const size_t oq = pa.push_vec(pq);
-        pa.upload(st);
-        segment_rows<<<static_cast<int>(ps.size()), 128, 0, st>>>(pa.at<Segment>(0), e.d_prompt, e.Pmax,
-                                                                 e.d_tok, e.tok_stride, w.meta);
+    for (const auto& ap : passes) {
+        segment_rows<<<ap.n_seg, 128, 0, st>>>(A.at<Segment>(ap.o_seg), e.d_prompt, e.Pmax, e.d_tok,
+                                               e.tok_stride, w.meta);
         Final<T> fin;
         fin.write_h = false;
-        forward<T>(e, e.models[ACTOR], w, st, rows_pass, false, 0, pa.at<QBlock>(oq),
-                   static_cast<int>(pq.size()), fin);
-        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // pass-local arena is released below
-        pa.release();
-        si = sj;
+        forward<T>(e, e.models[ACTOR], w, st, ap.rows, false, 0, A.at<QBlock>(ap.o_qb), ap.n_qb, fin);
     }
-    (void)o_segs;
-    (void)o_qbs;
+    // order every admission write (page table, target lengths, prompts, actor
+    // KV) before the next decode on sa and the next scorer wave on ss, also
+    // when no prefill pass ran (all prompts of length 1)
+    OPPO_CUDA_CHECK(cudaEventRecord(e.ev_admit, st));
+    for (cudaStream_t o : {e.sa, e.ss})
+        if (o != st) OPPO_CUDA_CHECK(cudaStreamWaitEvent(o, e.ev_admit, 0));
 }
 
 }  // namespace
@@ -1928,6 +1947,10 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     gae_scan<float><<<cdiv(n * 32, 128), 128, 0, st>>>(n, d_off, d_rew, d_vals,
                                                       static_cast<float>(hp.gamma),
                                                       static_cast<float>(hp.lambda), d_adv, d_ret);
+    if (hp.value_target == OPPO_VALUE_MC_RETURN)  // the reference's value target (ppo.cpp:296-314)
+        mc_returns<float><<<cdiv(n, 128), 128, 0, st>>>(n, d_off, d_score, static_cast<float>(hp.gamma), d_ret);
+    else if (hp.value_target != OPPO_VALUE_GAE_RETURN)
+        config_error("value_target must be OPPO_VALUE_MC_RETURN or OPPO_VALUE_GAE_RETURN");
     // K9 whitening statistics.  Data-parallel runs allreduce
     // {sum adv, sum adv^2, n_tokens, sum reward, n_samples} in one fp64 NCCL
     // call: whitening uses the global moments, the token mean of the

@@ -146,6 +146,7 @@ struct Engine {
     Work ws_m[2];
     cudaStream_t ss_m[2] = {nullptr, nullptr};
     cudaEvent_t ev_seg = nullptr, ev_m[2] = {nullptr, nullptr};
+    cudaEvent_t ev_admit = nullptr;  // end of an admission's writes on su
     // Policy log-probs (and log-sum-exp) of the sampled tokens of every sequence
     // that finished in the last step, computed on the actor SMs while the
     // scorers finish their last wave; oppo_ppo_update reuses them when the

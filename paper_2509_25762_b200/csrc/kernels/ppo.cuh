@@ -98,6 +98,22 @@ __global__ void gae_scan(int n_seq, const int32_t* __restrict__ off, const R* __
     }
 }
 
+// Critic target of the reference's value fit (ppo.cpp:296-314): the
+// gamma-discounted return of terminal_rewards, ret_t = gamma^(L-1-t) * score,
+// accumulated in the reference's order (ret = r_t + gamma * ret, right to left).
+template <class R>
+__global__ void mc_returns(int n_seq, const int32_t* __restrict__ off, const R* __restrict__ score, R gamma,
+                           R* __restrict__ ret) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_seq) return;
+    const int a = off[i], len = off[i + 1] - a;
+    R run = 0;
+    for (int t = len - 1; t >= 0; --t) {
+        run = add_rn(t == len - 1 ? score[i] : R(0), mul_rn(gamma, run));
+        ret[a + t] = run;
+    }
+}
+
 // Block-partial sums for whitening statistics: [sum adv, sum adv^2, count].
 template <class R>
 __global__ void moments(const R* __restrict__ x, int n, double* __restrict__ partial) {

@@ -39,7 +39,7 @@ def tuner_rows(cfg, records, measure="wall"):
     cands = [cfg.chunk_candidates[i] for i in range(cfg.n_candidates)]
     if not cands:
         return []
-    order = sorted(cands)
+    order = sorted(set(cands))  # make_tuner dedupes the candidates (chunking.cpp:61-71)
     meas, steps = [], []
     for r in records:
         slot = r.step % cfg.retune_period
@@ -47,7 +47,7 @@ def tuner_rows(cfg, records, measure="wall"):
             m = float(r.wall_ticks) if measure == "wall" else float(r.step_us)
             meas.append((r.chunk_size, m))
             steps.append(r.step)
-    chosen = S.tuner_replay(cands, cfg.retune_period, meas)
+    chosen = S.tuner_replay(order, cfg.retune_period, meas)
     return [(s, c, m, ch) for s, (c, m), ch in zip(steps, meas, chosen)]
 
 

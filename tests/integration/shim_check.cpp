@@ -4,6 +4,7 @@
 // rlpipe::run_step under the lockstep latency model, on random active sets
 // (fresh and carried sequences, both schedule modes, random cuts).
 // Built and run by tests/test_integration.py where /root/reference exists.
+#include <string>
 #include <cstdio>
 #include <random>
 #include <vector>
@@ -77,10 +78,12 @@ int main() {
         one[0].prompt.id = 1;
         one[0].target_len = 5;
         oppo_rlpipe::run_step_logical(one, bad, 1);
-    } catch (const rlpipe::ConfigError&) {
-        mapped = true;
-    } catch (const rlpipe::InputError&) {
-        mapped = true;
+    } catch (const rlpipe::ConfigError& ex) {
+        mapped = std::string(ex.what()).find("chunk") != std::string::npos;  // the call's own message
+        if (!mapped) std::printf("error message: '%s'\n", ex.what());
+    } catch (const rlpipe::InputError& ex) {
+        mapped = std::string(ex.what()).find("chunk") != std::string::npos;
+        if (!mapped) std::printf("error message: '%s'\n", ex.what());
     }
     std::printf("cases %d mismatches %d error_mapping %s\n", cases, mismatches, mapped ? "ok" : "BAD");
     return (mismatches == 0 && mapped) ? 0 : 1;
