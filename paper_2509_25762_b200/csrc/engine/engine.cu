@@ -942,6 +942,13 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         } else {
             e->dec_split_min = 0;
         }
+        // OPPO_NUMERICS_SMS pins every SM-count-dependent kernel choice that
+        // changes the arithmetic (split-K factors, attention tile shapes, grid
+        // shares of the two decode branches) to one SM count, so engines with
+        // and without the SM partition compute bit-identical results (test
+        // knob; by default each stream plans for the SMs it runs on)
+        if (const int ns = env_int("OPPO_NUMERICS_SMS", 0); ns > 0)
+            for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) w->sms = ns;
         // persistent decode kernel: experimental, off by default (measured slower
         // than the PDL-chained kernels: 2 us per grid barrier x 168, profiles/)
         e->mega_max_rows = env_int("OPPO_MEGA_MAX_ROWS", 0);

@@ -1,0 +1,260 @@
+"""Parity at the benchmarked configuration (BASELINE.json configs[1], the line
+bench.py reports): 0.5B actor + 0.5B reward / critic / reference, bf16,
+V = 151,936, B = 256 + 26 overcommit, prompt 128, LN(5, 1) cap 1024, chunk 64,
+token-granular carry, the scorer SM partition (64 SMs, green contexts), three
+concurrent scorer streams and two-branch decode iterations — built exactly as
+bench.py builds the engine (bench.make_cfg / bench.CFG2 / bench.host_prompts).
+
+Checked over three steps:
+  * decisions (cut, chunk progress, selection, deferral) of every sequence
+    against the compiled reference's run_step under the lockstep latency model
+    (oracle/_ref) and the C restatement with token-granular credit;
+  * content of sampled sequences (short / median / capped, and a straggler
+    carried from step 0 into step 1) at full depth against the numpy fp64
+    oracle with the engine's bf16 rounding points (oracle/gpt_np.py): token ids
+    wherever the sampling margins exceed MARGIN, old / reference log-probs,
+    per-token values and the reward;
+  * with the numerics planning pinned to one SM count (OPPO_NUMERICS_SMS), the
+    same two steps are bit-identical with and without the SM partition and with
+    one or three scorer streams (the partition and the concurrency change where
+    kernels run, never what they compute).
+"""
+import os
+import subprocess
+import sys
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from oracle import gpt_np as N  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from oracle import ref as R  # noqa: E402
+from paper_2509_25762_b200 import abi  # noqa: E402
+from paper_2509_25762_b200 import scheduler as S  # noqa: E402
+from paper_2509_25762_b200.engine import Engine  # noqa: E402
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+SAMPLE_SEED, SEED, STEPS = 2, 7, 3
+# bf16 tolerances vs the bf16-rounding fp64 oracle, ~2.5x the maxima measured
+# over the sampled sequences (profiles/r02_headline_parity.json): log-prob max
+# 0.023 / mean 0.005 nats; per-token value 0.02 and reward 0.19 absolute, i.e.
+# 0.033 and 0.013 of the head's L2 norm (heads are dot products with
+# N(0, 0.02) / N(0, 0.5) weights over unit-RMS rows, so their error scales with
+# the head norm, not with the output, which cancels to O(1)).
+TOL_LP, TOL_LP_MEAN = 0.05, 0.012
+TOL_VAL_W = 0.08      # max |value - oracle| / ||critic head||_2
+TOL_REWARD_W = 0.03   # |reward - oracle| / ||reward head||_2
+MARGIN = 5e-3         # token ids compared strictly where both sampling margins exceed this
+AGREE_1E3 = 0.99      # ... and >= 99% agreement where they exceed 1e-3
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def run_cfg2(steps=STEPS, scorer_sms=64, env=None, keep=None, weights=False):
+    """Two cfg2 steps through the engine exactly as bench.py drives it.  Returns
+    per-step decisions + outcomes, and rollouts of the sequences in `keep`
+    (all selected sequences when keep == 'all')."""
+    wl = bench.CFG2
+    cfg = bench.make_cfg(wl)
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = v
+    try:
+        eng = Engine(wl["actor"], wl["scorer"], wl["scorer"], wl["scorer"], dtype=abi.DTYPE_BF16,
+                     max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
+                     max_response_len=wl["cap"], page_size=64, carry=cfg.carry_granularity,
+                     train_heads=1, sample_seed=SAMPLE_SEED, weight_seed=1, scorer_sms=scorer_sms)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    V = eng.cfg.actor.vocab
+    B, P = cfg.batch_size, cfg.prompt_len
+    lengths = S.sample_lengths(cfg.lengths, SEED, 4 * (B + cfg.delta_max))
+    entries, next_id = [], 0
+    log, rollouts, prompts = [], {}, {}
+    hp = abi.PpoHparams(gamma=1.0, lambda_=0.95, clip_epsilon=0.2, learning_rate=0.0,
+                        value_learning_rate=0.0, kl_coef=0.05, whiten=1)
+    for step in range(steps):
+        fresh = []
+        while len(entries) + len(fresh) < B + cfg.delta_init:
+            fresh.append(S.seq_array([dict(id=next_id, prompt_len=P, target_len=lengths[next_id],
+                                           admitted_at=step, arrival_step=step)])[0])
+            next_id += 1
+        pr = bench.host_prompts([f.id for f in fresh], P, V, 1234)
+        for f, p in zip(fresh, pr):
+            prompts[f.id] = p
+        eng.admit(fresh, prompts=pr)
+        entries = entries + fresh
+        active = [e for e in entries if not e.scored]
+        need = B - (len(entries) - len(active))
+        before = [a.as_tuple() for a in active]
+        outs, led = eng.run_step(active, cfg.chunk_size, cfg.schedule_mode, need)
+        batch, entries, _ = S.select_finished(entries, outs, B)
+        ids = [b.id for b in batch]
+        log.append(dict(active=before, outs=[o.as_tuple() for o in outs], need=need, selected=ids,
+                        iters=led.decode_iters))
+        for i in ids:
+            if keep == "all" or (keep and i in keep):
+                rollouts[i] = eng.read_rollout(i)
+        eng.ppo_update(ids, hp)
+        eng.release(ids)
+    w = [eng.export_weights(m) for m in range(4)] if weights else None
+    eng.close()
+    torch.cuda.empty_cache()
+    return dict(log=log, rollouts=rollouts, prompts=prompts, weights=w, lengths=lengths)
+
+
+def _mk(t):
+    s = abi.SeqState()
+    names = [f for f, _ in abi.SeqState._fields_ if f != "_pad"]
+    for f, v in zip(names, t):
+        setattr(s, f, v)
+    return s
+
+
+@pytest.fixture(scope="module")
+def headline():
+    _cuda()
+    run = run_cfg2(keep="all", weights=True)
+    # sampled sequences: the shortest, median and longest of step 0's batch,
+    # and a straggler carried out of step 0 and finished in a later step
+    sel0 = run["log"][0]["selected"]
+    by_len = sorted(sel0, key=lambda i: (run["rollouts"][i]["length"], i))
+    picks = {by_len[0], by_len[len(by_len) // 2], by_len[-1]}
+    carried = [o[0] for o in run["log"][0]["outs"] if o[0] not in sel0]
+    later = [i for st in run["log"][1:] for i in st["selected"]]
+    straggler = next(c for c in carried if c in later)
+    picks.add(straggler)
+    run["picks"] = sorted(picks)
+    run["straggler"] = straggler
+    return run
+
+
+def test_headline_decisions_match_reference(headline):
+    """Every step's cut, chunk progress and selection equal the compiled
+    reference's run_step (lockstep latency model) on the fields carry does not
+    change, and the C restatement with token-granular credit on all fields."""
+    lat = R.lockstep_latency()
+    for st in headline["log"]:
+        act = [_mk(t) for t in st["active"]]
+        arr = (abi.SeqState * len(act))(*act)
+        ref_out, _ = R.run_step(arr, len(act), 64, abi.MODE_STREAMED, lat, st["need"])
+        got = st["outs"]
+        assert [(o.seq_id, o.score_ready) for o in ref_out] == [(g[0], g[1]) for g in got]
+        fin = [g for g, a in zip(got, act) if a.generated + g[2] >= a.target_len]
+        ref_fin = [o.as_tuple() for o, a in zip(ref_out, act) if a.generated + o.tokens_decoded >= a.target_len]
+        assert fin == ref_fin  # finished sequences: identical under both carry rules
+        tok_out, _ = O.run_step(arr, len(act), 64, abi.MODE_STREAMED, lat, st["need"], credit_partial=True)
+        assert [o.as_tuple() for o in tok_out] == got
+    assert all(len(st["selected"]) == 256 for st in headline["log"])
+
+
+def _logsm(x):
+    m = x.max(-1, keepdims=True)
+    return x - m - np.log(np.exp(x - m).sum(-1, keepdims=True))
+
+
+def test_headline_content_vs_fp64_oracle(headline):
+    """Tokens, old / reference log-probs, values and the reward of the sampled
+    sequences (short, median, longest of the first batch, and a straggler
+    carried across the step boundary) at full depth against the bf16-rounding
+    fp64 oracle."""
+    P = 128
+    report = {}
+    (da, wa), (dr, wr), (dc, wc), (dref, wref) = headline["weights"]
+    seqs = {}
+    for i in headline["picks"]:
+        ro = headline["rollouts"][i]
+        seqs[i] = (ro, np.concatenate([headline["prompts"][i], ro["tokens"]]).astype(np.int64))
+        report[i] = dict(length=ro["length"], straggler=i == headline["straggler"])
+    m = N.GptNp(da, wa, bf16_mode=True)  # actor: tokens + old log-probs
+    for i, (ro, seq) in seqs.items():
+        L = ro["length"]
+        _, lg = m.forward(seq[:-1], rows=np.arange(P - 1, P + L - 1))
+        lp = _logsm(lg)[np.arange(L), ro["tokens"][:L]]
+        strict = [0, 0]
+        loose = [0, 0]
+        for j in range(L):
+            tok, _, mb, mi = O.sample_token(lg[j], O.token_key(SAMPLE_SEED, i, j + 1))
+            hit = int(tok == ro["tokens"][j])
+            if min(mb, mi) > MARGIN:
+                strict[0] += 1
+                strict[1] += hit
+            if min(mb, mi) > 1e-3:
+                loose[0] += 1
+                loose[1] += hit
+        err = np.abs(lp - ro["old_lp"])
+        report[i].update(tokens_strict=strict, tokens_1e3=loose, old_lp_max=float(err.max()),
+                         old_lp_mean=float(err.mean()))
+    del m
+    m = N.GptNp(dref, wref, bf16_mode=True)  # reference model: ref log-probs
+    for i, (ro, seq) in seqs.items():
+        L = ro["length"]
+        _, lg = m.forward(seq[:-1], rows=np.arange(P - 1, P + L - 1))
+        err = np.abs(_logsm(lg)[np.arange(L), ro["tokens"][:L]] - ro["ref_lp"])
+        report[i].update(ref_lp_max=float(err.max()), ref_lp_mean=float(err.mean()))
+    del m
+    m = N.GptNp(dc, wc, bf16_mode=True)  # critic: values of the states before each token
+    wn = float(np.linalg.norm(m.head))
+    for i, (ro, seq) in seqs.items():
+        L = ro["length"]
+        hf, _ = m.forward(seq, logits=False)
+        report[i]["value_err_w"] = float(np.abs(bf16_head(hf[P - 1:P + L - 1], m.head) - ro["values"]).max()) / wn
+    del m
+    m = N.GptNp(dr, wr, bf16_mode=True)  # reward model: last token
+    wn = float(np.linalg.norm(m.head))
+    for i, (ro, seq) in seqs.items():
+        hf, _ = m.forward(seq, logits=False)
+        r = float(bf16_head(hf[-1:], m.head)[0])
+        report[i].update(reward=float(ro["reward"]), reward_oracle=r, reward_err_w=abs(r - ro["reward"]) / wn)
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "r02_headline_parity.json"), "w") as f:
+            json.dump({str(k): v for k, v in report.items()}, f, indent=1, default=float)
+    print(json.dumps({str(k): v for k, v in report.items()}, default=float))
+    for i, r in report.items():
+        assert r["tokens_strict"][0] == r["tokens_strict"][1], (i, r)
+        assert r["tokens_1e3"][1] >= AGREE_1E3 * r["tokens_1e3"][0], (i, r)
+        assert r["old_lp_max"] <= TOL_LP and r["old_lp_mean"] <= TOL_LP_MEAN, (i, r)
+        assert r["ref_lp_max"] <= TOL_LP and r["ref_lp_mean"] <= TOL_LP_MEAN, (i, r)
+        assert r["value_err_w"] <= TOL_VAL_W, (i, r)
+        assert r["reward_err_w"] <= TOL_REWARD_W, (i, r)
+    assert any(r["straggler"] for r in report.values())
+
+
+def bf16_head(hf, w):
+    """The engine's head dot: bf16-rounded normed row x fp32 head weights."""
+    return hf @ np.asarray(w, dtype=np.float64)
+
+
+def test_headline_partition_and_streams_do_not_change_results():
+    """OPPO_NUMERICS_SMS pins the kernel configurations (split-K, attention
+    tiles) to one SM count; then the fixed SM partition (green contexts) and
+    the three concurrent scorer streams leave every token, log-prob, value and
+    reward of two cfg2 steps bit-identical."""
+    _cuda()
+    env = {"OPPO_NUMERICS_SMS": "84"}
+    a = run_cfg2(steps=2, scorer_sms=64, env={**env, "OPPO_SCORER_STREAMS": "3"}, keep="all")
+    b = run_cfg2(steps=2, scorer_sms=0, env={**env, "OPPO_SCORER_STREAMS": "1"}, keep="all")
+    assert [s["selected"] for s in a["log"]] == [s["selected"] for s in b["log"]]
+    assert a["rollouts"].keys() == b["rollouts"].keys()
+    for k in a["rollouts"]:
+        x, y = a["rollouts"][k], b["rollouts"][k]
+        for f in ("tokens", "old_lp", "ref_lp", "values"):
+            assert np.array_equal(x[f], y[f]), (k, f)
+        assert x["reward"] == y["reward"] or (np.isnan(x["reward"]) and np.isnan(y["reward"])), k
