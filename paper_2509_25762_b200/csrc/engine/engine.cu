@@ -31,6 +31,7 @@
 #include "engine.cuh"
 #include "host/driver.hpp"
 #include "kernels/ppo.cuh"
+#include "kernels/train.cuh"
 
 namespace oppo {
 
@@ -987,6 +988,7 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
 void engine_free(Engine* e) {
     if (!e) return;
     cudaDeviceSynchronize();
+    train_free(*e);
     auto it = g_extra.find(e);
     if (it != g_extra.end()) {
         it->second.scorer.shutdown();
@@ -1905,8 +1907,11 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     const int Da = actor.dims.d_model, Dc = critic.dims.d_model, V = actor.dims.vocab;
     const int Npad = (N + 7) / 8 * 8;
     // device buffers (grown on demand)
-    const size_t need = static_cast<size_t>(Npad) * (4 * 12) + static_cast<size_t>(n + 1) * 20 * 4 +
-                        static_cast<size_t>(Npad) * (Da + Dc) * sizeof(T) + 4096 * 8 + 1024;
+    size_t meta_bytes = 0;
+    for (int i = 0; i < n; ++i) meta_bytes += 16 * cdiv(e.slots[slots[i]].prompt_len + off[i + 1] - off[i], 32);
+    const size_t need = static_cast<size_t>(Npad) * (4 * 14) + static_cast<size_t>(n + 1) * 20 * 4 +
+                        static_cast<size_t>(Npad) * (Da + Dc) * sizeof(T) + 4096 * 8 + 1024 +
+                        meta_bytes + static_cast<size_t>(n) * 16 + 16384;
     if (need > e.ppo_buf_bytes) {
         if (e.ppo_buf) cudaFree(e.ppo_buf);
         e.ppo_buf_bytes = need * 3 / 2;
@@ -1986,13 +1991,17 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         samples_glob = g[4];
     }
     const float inv_n_glob = 1.0f / static_cast<float>(std::max(1.0, n_glob));
+    // full-parameter update (K11 / K12, train.cu): the actor's objective and the
+    // critic's value loss come from the training forward of every layer
+    const bool full = e.cfg.train_heads == 2;
+    const bool full_actor = full && hp.learning_rate != 0, full_critic = full && hp.value_learning_rate != 0;
     // current-policy log-probs of the sampled tokens from the cached actor
     // hidden states: computed at the end of run_step while the scorers
     // finished (precompute_policy_lp) when every sequence of the batch is
     // there and the lm_head is unchanged, else here
     const int nt = gemm_logit_tiles(e.dtype, V);
     Work& w = e.ws;
-    bool use_pre = e.pre_lp && e.pre_version == e.lm_version && n > 0;
+    bool use_pre = !full_actor && e.pre_lp && e.pre_version == e.lm_version && n > 0;
     std::vector<int32_t> pre_src(n);
     for (int i = 0; i < n && use_pre; ++i) {
         const auto it = e.pre_index.find(e.slots[slots[i]].id);
@@ -2006,7 +2015,7 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         gather_pre_lp<<<n, 128, 0, st>>>(d_src, d_off, n, e.pre_new, e.pre_lse, d_new, d_lse);
     }
     const int chunk_rows = std::max(32, std::min(w.max_rows, static_cast<int>((static_cast<size_t>(64) << 20) / (nt * 16))));
-    for (int c0 = 0; c0 < N && !use_pre; c0 += chunk_rows) {
+    for (int c0 = 0; c0 < N && !use_pre && !full_actor; c0 += chunk_rows) {
         const int cn = std::min(chunk_rows, N - c0);
         EpiParams ep{};
         ep.mode = EPI_LOGITS;
@@ -2020,11 +2029,47 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     }
     // K10 clipped objective and d obj / d logp
     const int cb = std::min(1024, cdiv(N, 256));
-    ppo_clip<float><<<cb, 256, 0, st>>>(N, d_new, d_old, d_adv, static_cast<float>(hp.clip_epsilon),
-                                        stats, 1e-8, d_dobj, d_part, inv_n_glob);
-    sum_partials<<<1, 32, 0, st>>>(d_part, cb, d_stats + 4);
+    if (!full_actor) {
+        ppo_clip<float><<<cb, 256, 0, st>>>(N, d_new, d_old, d_adv, static_cast<float>(hp.clip_epsilon),
+                                            stats, 1e-8, d_dobj, d_part, inv_n_glob);
+        sum_partials<<<1, 32, 0, st>>>(d_part, cb, d_stats + 4);
+    } else {
+        OPPO_CUDA_CHECK(cudaMemsetAsync(d_stats + 4, 0, 8, st));
+    }
+    float* d_sq = reinterpret_cast<float*>(take(Npad * 4));
+    if (full_actor || full_critic) {
+        TrainBatch tb;
+        for (int i = 0; i < n; ++i) {
+            tb.slot.push_back(slots[i]);
+            tb.P.push_back(e.slots[slots[i]].prompt_len);
+            tb.L.push_back(off[i + 1] - off[i]);
+        }
+        tb.off = off;
+        tb.rows_max = std::max(256, env_int("OPPO_TRAIN_ROWS", 16384));
+        tb.tok = d_tokv;
+        tb.adv = d_adv;
+        tb.old_lp = d_old;
+        tb.ret = d_ret;
+        tb.new_lp = d_new;
+        tb.lse = d_lse;
+        tb.dobj = d_dobj;
+        tb.stats = stats;
+        tb.clip_eps = static_cast<float>(hp.clip_epsilon);
+        tb.inv_n = inv_n_glob;
+        tb.part = d_part;
+        tb.obj_acc = d_stats + 4;
+        tb.sq = d_sq;
+        // micro-batch metadata: sequences, 32-row attention blocks, response-row map
+        size_t blocks = 0;
+        for (int i = 0; i < n; ++i) blocks += cdiv(tb.P[i] + tb.L[i] - 1, 32);
+        tb.meta_cap = static_cast<size_t>(n) * 16 + blocks * 16 + static_cast<size_t>(N) * 4 + 4096;
+        tb.meta_dev = take(tb.meta_cap);
+        if (e.dtype == OPPO_DTYPE_F32) train_full<float>(e, tb, hp, dp, st);
+        else train_full<__nv_bfloat16>(e, tb, hp, dp, st);
+        if (full_actor) ++e.lm_version;
+    }
     // K11 head update: lm_head += lr * dObj/dW  (gradient ascent, ppo.cpp:288-290)
-    if (e.cfg.train_heads && hp.learning_rate > 0) {
+    if (e.cfg.train_heads == 1 && hp.learning_rate > 0) {
         const int gc = e.g_chunk;
         if (!e.g_buf) {
             e.g_buf = dalloc(static_cast<size_t>(V) * gc * sizeof(T));
@@ -2076,7 +2121,12 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         head_sgd<<<cdiv(Dc, 128), 128, 0, st>>>(critic.head, e.vgrad, Dc,
                                                 static_cast<float>(hp.value_learning_rate));
     }
-    sq_err_sum<<<1, 256, 0, st>>>(d_vtok, d_ret, N, d_stats + 5);
+    if (full_critic) {  // value loss of the critic's training forward
+        OPPO_CUDA_CHECK(cudaMemsetAsync(d_stats + 5, 0, 8, st));
+        train::sum_to_double<<<1, 256, 0, st>>>(d_sq, N, d_stats + 5);
+    } else {
+        sq_err_sum<<<1, 256, 0, st>>>(d_vtok, d_ret, N, d_stats + 5);
+    }
     // statistics back to the host
     double hs[8] = {0};
     OPPO_CUDA_CHECK(cudaMemcpyAsync(hs, d_stats, 8 * 8, cudaMemcpyDeviceToHost, st));
@@ -2108,6 +2158,10 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
 }
 
 }  // namespace
+
+void dp_allreduce_pub(Engine& e, void* buf, int64_t count, bool f64, cudaStream_t st) {
+    dp_allreduce(e, buf, count, f64, st);
+}
 
 }  // namespace oppo
 
@@ -2267,8 +2321,11 @@ void checkpoint_io(Engine& e, CkptFile& io) {
                     io.dev2d(static_cast<uint8_t*>(pool) + pg * page_elems * e.esz, m.layer_stride * e.esz,
                              page_elems * e.esz, m.dims.n_layers);
     }
-    // trained heads
-    if (e.cfg.train_heads) {
+    // trained tensors: every actor / critic tensor and its fp32 master (full
+    // update), or the heads
+    if (e.cfg.train_heads == 2) {
+        for (auto& [ptr, bytes] : train_tensors(e, e.su)) io.dev(ptr, bytes);
+    } else if (e.cfg.train_heads) {
         Model& a = e.models[ACTOR];
         const size_t nw = static_cast<size_t>(a.dims.vocab) * a.dims.d_model;
         io.dev(a.lm_head, nw * e.esz);

@@ -221,11 +221,42 @@ struct Engine {
     float* vgrad = nullptr;
     float* g_lm = nullptr;   // DP: lm_head gradient buffer (allreduced)
     void* nccl = nullptr;
+    void* train_state = nullptr;  // full-parameter update state (train.cu)
+};
+
+// One PPO batch for the full-parameter update (train.cu): the sequences in
+// batch order and their per-response-token device arrays.
+struct TrainBatch {
+    std::vector<int> slot, P, L, off;  // off: response-token prefix sums (n + 1)
+    int rows_max = 16384;              // training rows per micro-batch (whole sequences)
+    const int32_t* tok = nullptr;      // [N] sampled tokens
+    float* adv = nullptr;              // [N] GAE advantages (whitened in place by ppo_clip)
+    const float* old_lp = nullptr;     // [N]
+    const float* ret = nullptr;        // [N] critic targets
+    float* new_lp = nullptr;           // [N] out: current-policy log-probs
+    float* lse = nullptr;              // [N] out
+    float* dobj = nullptr;             // [N] out: dObj/dlogp
+    const double* stats = nullptr;     // whitening moments (sum, sumsq, n) or null
+    float clip_eps = 0.2f, inv_n = 1.f;
+    double* part = nullptr;            // >= 1024 doubles
+    double* obj_acc = nullptr;         // += sum of clipped-objective terms
+    float* sq = nullptr;               // [N] out: squared value errors
+    float* v_new = nullptr;            // [N] out (optional): current critic values
+    void* meta_dev = nullptr;          // device staging of the micro-batch metadata
+    size_t meta_cap = 0;
 };
 
 // engine.cu
 Engine* engine_new(const oppo_engine_cfg& cfg);
 void engine_free(Engine* e);
+
+// train.cu
+template <class T>
+void train_full(Engine& e, TrainBatch& b, const oppo_ppo_hparams& hp, bool dp, cudaStream_t st);
+void train_free(Engine& e);
+std::vector<std::pair<void*, size_t>> train_tensors(Engine& e, cudaStream_t st);
+// engine.cu
+void dp_allreduce_pub(Engine& e, void* buf, int64_t count, bool f64, cudaStream_t st);
 
 // gemm_host.cu
 void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,

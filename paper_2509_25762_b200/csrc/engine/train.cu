@@ -1,0 +1,580 @@
+// train.cu — the full-parameter PPO update: actor
+// and critic trained through every layer, as the reference's
+// toy_rlhf_step updates every policy parameter (ppo.cpp:281-317:
+// theta += lr * clipped_objective_grad, value fit toward discounted returns).
+//
+// Per model, the update's sequences (prompt + response, minus the last
+// response token) are packed into micro-batches of whole sequences.  For each
+// micro-batch: a training forward that keeps every layer's input residual,
+// post-RoPE q|k|v, attention output + log-sum-exp, mid residual and gate|up
+// pre-activation; the loss head (actor: lm_head + log-softmax + clipped
+// surrogate, dObj/dlogits through the softmax-grad GEMM epilogue; critic:
+// value head + squared error to the returns); then the backward, layer by
+// layer, with dgrad GEMMs against transposed weight copies and wgrad GEMMs
+// (dY^T X over the token dimension) accumulating into fp32 gradient buffers.
+// After the last micro-batch the gradients are allreduced across the
+// data-parallel ranks (one NCCL call per tensor) and applied by SGD to the
+// fp32 masters, from which the bf16 compute weights are re-rounded.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "engine.cuh"
+#include "kernels/ppo.cuh"
+#include "kernels/train.cuh"
+
+namespace oppo {
+
+namespace {
+
+constexpr float kEps = 1e-6f;
+constexpr float kTheta = 1e6f;
+
+inline int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    OPPO_CUDA_CHECK(cudaMalloc(&p, bytes ? bytes : 16));
+    return p;
+}
+
+// One trainable tensor of a model.
+struct PT {
+    void* w = nullptr;        // compute tensor (T matrix or fp32 vector)
+    float* master = nullptr;  // fp32 master (bf16 matrices), else null (w is fp32)
+    float* grad = nullptr;    // fp32 gradient, same layout as w
+    void* wT = nullptr;       // transposed compute copy [cols][rows] (dgrad operand)
+    int64_t rows = 0, cols = 1;
+    bool matrix = false;
+    int64_t n() const { return rows * cols; }
+};
+
+struct LayerT {
+    PT wqkv, bqkv, wo, wgu, wdown, ln1, ln2;
+};
+
+struct ModelT {
+    bool ready = false;
+    PT embed, lm_head, final_norm, head;  // lm_head.w == embed.w when tied
+    std::vector<LayerT> layers;
+    std::vector<PT*> all() {
+        std::vector<PT*> v{&embed};
+        if (lm_head.w && lm_head.w != embed.w) v.push_back(&lm_head);
+        v.push_back(&final_norm);
+        if (head.w) v.push_back(&head);
+        for (auto& L : layers)
+            for (PT* p : {&L.wqkv, &L.bqkv, &L.wo, &L.wgu, &L.wdown, &L.ln1, &L.ln2}) v.push_back(p);
+        return v;
+    }
+};
+
+// Scratch of one micro-batch (grown on demand).
+struct Scratch {
+    size_t cap = 0;
+    std::vector<void*> bufs;
+    void* take(size_t bytes) {
+        void* p = dalloc(bytes);
+        bufs.push_back(p);
+        return p;
+    }
+    void release() {
+        for (void* p : bufs) cudaFree(p);
+        bufs.clear();
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct TrainState {
+    ModelT m[N_MODELS];
+    Scratch scr;
+    int rows_cap = 0;  // training rows the scratch is sized for
+    // per-layer saved activations
+    std::vector<float*> x_in, x_mid, lse;
+    std::vector<void*> qkv, o, gu;
+    // transients
+    float *x = nullptr, *dx = nullptr, *dh = nullptr, *dff = nullptr, *dqkv = nullptr, *dvec = nullptr,
+          *gscr = nullptr, *colp = nullptr, *head_out = nullptr, *dhf_c = nullptr;
+    void *h = nullptr, *hf = nullptr, *ff = nullptr, *dgu = nullptr, *dxc = nullptr, *dxT = nullptr,
+         *aT = nullptr, *bT = nullptr, *dO = nullptr, *dqkvc = nullptr, *hf_resp = nullptr, *hfT = nullptr,
+         *G = nullptr, *Gt = nullptr;
+    int32_t *tok = nullptr, *pos = nullptr;
+    int g_rows = 0;  // lm_head gradient chunk (rows)
+};
+
+void train_free(Engine& e) {
+    auto* ts = static_cast<TrainState*>(e.train_state);
+    if (!ts) return;
+    ts->scr.release();
+    for (auto& m : ts->m)
+        for (PT* p : m.all()) {
+            if (p->grad) cudaFree(p->grad);
+            if (p->wT) cudaFree(p->wT);
+            if (p->master && !(p == &m.embed && p->master == e.models[ACTOR].lm_master)) cudaFree(p->master);
+        }
+    delete ts;
+    e.train_state = nullptr;
+}
+
+namespace {
+
+PT make_pt(Engine& e, void* w, int64_t rows, int64_t cols, bool matrix, float* master_existing, bool want_T,
+           cudaStream_t st) {
+    PT p;
+    p.w = w;
+    p.rows = rows;
+    p.cols = cols;
+    p.matrix = matrix;
+    p.grad = static_cast<float*>(dalloc(p.n() * 4));
+    if (matrix && e.dtype == OPPO_DTYPE_BF16) {
+        if (master_existing) {
+            p.master = master_existing;
+        } else {
+            p.master = static_cast<float*>(dalloc(p.n() * 4));
+            convert<__nv_bfloat16, float><<<cdiv(p.n(), 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w),
+                                                                             p.master, p.n());
+        }
+    }
+    if (want_T) p.wT = dalloc(p.n() * e.esz);
+    return p;
+}
+
+void setup_model(Engine& e, TrainState& ts, int mid, cudaStream_t st) {
+    ModelT& mt = ts.m[mid];
+    if (mt.ready) return;
+    Model& m = e.models[mid];
+    const auto& d = m.dims;
+    const int64_t D = d.d_model, V = d.vocab, F = d.d_ff, qkv = m.qkv_width(), qw = m.q_width();
+    const bool actor = mid == ACTOR;
+    float* lm_master = actor ? m.lm_master : nullptr;
+    mt.embed = make_pt(e, m.embed, V, D, true, d.tied ? lm_master : nullptr, actor && d.tied, st);
+    if (!d.tied && actor) mt.lm_head = make_pt(e, m.lm_head, V, D, true, lm_master, true, st);
+    else mt.lm_head = mt.embed;
+    mt.final_norm = make_pt(e, m.final_norm, D, 1, false, nullptr, false, st);
+    if (m.head) mt.head = make_pt(e, m.head, D, 1, false, nullptr, false, st);
+    mt.layers.resize(d.n_layers);
+    for (int l = 0; l < d.n_layers; ++l) {
+        auto& L = m.layers[l];
+        auto& T = mt.layers[l];
+        T.wqkv = make_pt(e, L.wqkv, qkv, D, true, nullptr, true, st);
+        T.bqkv = make_pt(e, L.bqkv, qkv, 1, false, nullptr, false, st);
+        T.wo = make_pt(e, L.wo, D, qw, true, nullptr, true, st);
+        T.wgu = make_pt(e, L.wgu, 2 * F, D, true, nullptr, true, st);
+        T.wdown = make_pt(e, L.wdown, D, F, true, nullptr, true, st);
+        T.ln1 = make_pt(e, L.ln1, D, 1, false, nullptr, false, st);
+        T.ln2 = make_pt(e, L.ln2, D, 1, false, nullptr, false, st);
+    }
+    mt.ready = true;
+}
+
+template <class T>
+void transpose(const void* in, int rows, int cols, int ld_out, void* out, cudaStream_t st, bool in_f32 = false) {
+    const dim3 grid(cdiv(cols, 32), cdiv(std::max(rows, ld_out), 32)), block(32, 8);
+    if (in_f32)
+        train::transpose_cvt<float, T><<<grid, block, 0, st>>>(static_cast<const float*>(in), rows, cols, cols,
+                                                               ld_out, static_cast<T*>(out));
+    else
+        train::transpose_cvt<T, T><<<grid, block, 0, st>>>(static_cast<const T*>(in), rows, cols, cols, ld_out,
+                                                           static_cast<T*>(out));
+}
+
+// Y[M, N] (epilogue ep) = A[M, K] . B[N, K]^T, packed rows
+void mm(Engine& e, cudaStream_t st, const void* A, int M, int K, const void* B, int N, EpiParams ep) {
+    gemm_run(e, e.ws, st, A, M, K, K, B, N, K, ep);
+}
+EpiParams epi(int mode, void* y, int ldy, float scale = 1.f, const float* bias = nullptr) {
+    EpiParams p{};
+    p.mode = mode;
+    p.y = y;
+    p.ldy = ldy;
+    p.scale = scale;
+    p.bias = bias;
+    return p;
+}
+
+void colsum_into(TrainState& ts, const float* x, int rows, int cols, float* out, cudaStream_t st) {
+    if (rows <= 0) return;
+    const int chunks = std::min(64, std::max(1, rows / 64));
+    const int per = cdiv(rows, chunks);
+    train::colsum_part<<<dim3(cdiv(cols, 256), chunks), 256, 0, st>>>(x, rows, cols, cols, per, ts.colp);
+    train::colsum_final<<<cdiv(cols, 256), 256, 0, st>>>(ts.colp, chunks, cols, out);
+}
+
+template <class T>
+void rmsnorm(Engine& e, float* x, const float* g, T* out, int rows, int D, cudaStream_t st,
+             const float* head_w = nullptr, float* head_out = nullptr) {
+    rmsnorm_rows<T><<<cdiv(rows, 4), 128, 0, st>>>(x, g, out, rows, D, kEps, head_w, head_out, nullptr, nullptr,
+                                                   nullptr, 0, 0, -1, nullptr, 0, size_t(0));
+}
+
+template <class T>
+void cvt_f32(const float* in, T* out, int64_t n, cudaStream_t st) {
+    convert<float, T><<<cdiv(n, 256), 256, 0, st>>>(in, out, n);
+}
+
+template <class T, int HD>
+void attn_launch(int which, const train::TBlk* blks, int nb, const T* qkv, int ld, int H, int KV, T* o, float* lse,
+                 const T* dO, const float* dvec, float* dqkv, cudaStream_t st) {
+    using A = train::AttnT<HD>;
+    static bool attr = false;
+    if (!attr) {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::attn_train_fwd<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             A::SMEM_FWD));
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::attn_train_dq<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             A::SMEM_BWD));
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::attn_train_dkv<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             A::SMEM_BWD));
+        attr = true;
+    }
+    if (which == 0)
+        train::attn_train_fwd<T, HD><<<dim3(nb, H), 256, A::SMEM_FWD, st>>>(blks, qkv, ld, H, KV, o, lse);
+    else if (which == 1)
+        train::attn_train_dq<T, HD><<<dim3(nb, H), 256, A::SMEM_BWD, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
+    else
+        train::attn_train_dkv<T, HD><<<dim3(nb, KV), 256, A::SMEM_BWD, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
+}
+template <class T>
+void attn(int hd, int which, const train::TBlk* blks, int nb, const T* qkv, int ld, int H, int KV, T* o, float* lse,
+          const T* dO, const float* dvec, float* dqkv, cudaStream_t st) {
+    if (nb <= 0) return;
+    switch (hd) {
+    case 32: attn_launch<T, 32>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st); break;
+    case 64: attn_launch<T, 64>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st); break;
+    default: attn_launch<T, 128>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st); break;
+    }
+}
+
+// Sizes the scratch for `rows` training rows of the largest trained model.
+template <class T>
+void ensure_scratch(Engine& e, TrainState& ts, int rows, int resp_rows) {
+    int L = 0, D = 0, qkv = 0, qw = 0, F = 0, H = 0, V = 0;
+    for (int mid : {ACTOR, CRITIC}) {
+        const Model& m = e.models[mid];
+        L = std::max(L, m.dims.n_layers);
+        D = std::max(D, m.dims.d_model);
+        qkv = std::max(qkv, m.qkv_width());
+        qw = std::max(qw, m.q_width());
+        F = std::max(F, m.dims.d_ff);
+        H = std::max(H, m.dims.n_heads);
+        V = std::max(V, m.dims.vocab);
+    }
+    if (rows <= ts.rows_cap) return;
+    ts.scr.release();
+    ts.x_in.assign(L, nullptr);
+    ts.x_mid.assign(L, nullptr);
+    ts.lse.assign(L, nullptr);
+    ts.qkv.assign(L, nullptr);
+    ts.o.assign(L, nullptr);
+    ts.gu.assign(L, nullptr);
+    const size_t R = rows, Rp = (R + 31) / 32 * 32, es = sizeof(T);
+    for (int l = 0; l < L; ++l) {
+        ts.x_in[l] = static_cast<float*>(ts.scr.take(R * D * 4));
+        ts.x_mid[l] = static_cast<float*>(ts.scr.take(R * D * 4));
+        ts.lse[l] = static_cast<float*>(ts.scr.take(R * H * 4));
+        ts.qkv[l] = ts.scr.take(R * qkv * es);
+        ts.o[l] = ts.scr.take(R * qw * es);
+        ts.gu[l] = ts.scr.take(R * 2 * F * es);
+    }
+    const size_t wide = std::max<size_t>({static_cast<size_t>(D), static_cast<size_t>(qkv), static_cast<size_t>(2 * F)});
+    ts.x = static_cast<float*>(ts.scr.take(R * D * 4));
+    ts.dx = static_cast<float*>(ts.scr.take(R * D * 4));
+    ts.dh = static_cast<float*>(ts.scr.take(R * D * 4));
+    ts.dff = static_cast<float*>(ts.scr.take(R * F * 4));
+    ts.dqkv = static_cast<float*>(ts.scr.take(R * qkv * 4));
+    ts.dvec = static_cast<float*>(ts.scr.take(R * H * 4));
+    ts.gscr = static_cast<float*>(ts.scr.take(R * std::max(D, qkv) * 4));
+    ts.colp = static_cast<float*>(ts.scr.take(64 * wide * 4));
+    ts.head_out = static_cast<float*>(ts.scr.take(R * 4));
+    ts.h = ts.scr.take(R * D * es);
+    ts.hf = ts.scr.take(R * D * es);
+    ts.ff = ts.scr.take(R * F * es);
+    ts.dgu = ts.scr.take(R * 2 * F * es);
+    ts.dxc = ts.scr.take(R * D * es);
+    ts.dxT = ts.scr.take(Rp * D * es);
+    ts.aT = ts.scr.take(Rp * wide * es);
+    ts.bT = ts.scr.take(Rp * std::max(D, F) * es);
+    ts.dO = ts.scr.take(R * qw * es);
+    ts.dqkvc = ts.scr.take(R * qkv * es);
+    ts.tok = static_cast<int32_t*>(ts.scr.take(R * 4));
+    ts.pos = static_cast<int32_t*>(ts.scr.take(R * 4));
+    ts.hf_resp = ts.scr.take(static_cast<size_t>(resp_rows) * D * es);
+    ts.dhf_c = static_cast<float*>(ts.scr.take(static_cast<size_t>(resp_rows) * D * 4));
+    ts.g_rows = std::min(resp_rows, 4096);
+    const size_t gp = (ts.g_rows + 7) / 8 * 8;
+    ts.hfT = ts.scr.take(gp * D * es);
+    ts.G = ts.scr.take(gp * V * es);
+    ts.Gt = ts.scr.take(gp * V * es);
+    ts.rows_cap = rows;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------
+// One model's update over the batch (actor: clipped surrogate through the
+// lm_head; critic: squared error of the value head).  Gradients accumulate
+// into the tensors' fp32 grad buffers; the caller applies them.
+template <class T>
+void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
+    auto& ts = *static_cast<TrainState*>(e.train_state);
+    Model& m = e.models[mid];
+    ModelT& mt = ts.m[mid];
+    const auto& d = m.dims;
+    const int D = d.d_model, H = d.n_heads, KV = d.n_kv_heads, hd = d.head_dim, F = d.d_ff, V = d.vocab;
+    const int qkvw = m.qkv_width(), qw = m.q_width(), Lyr = d.n_layers;
+    const bool actor = mid == ACTOR;
+    // weight transposes (dgrad operands) and zeroed gradients
+    for (PT* p : mt.all()) OPPO_CUDA_CHECK(cudaMemsetAsync(p->grad, 0, p->n() * 4, st));
+    for (PT* p : mt.all())
+        if (p->wT) transpose<T>(p->w, static_cast<int>(p->rows), static_cast<int>(p->cols), static_cast<int>(p->rows),
+                                p->wT, st);
+    // micro-batches of whole sequences
+    const int n = static_cast<int>(b.slot.size());
+    int s0 = 0;
+    while (s0 < n) {
+        int s1 = s0, rows = 0;
+        while (s1 < n && (rows + b.P[s1] + b.L[s1] - 1 <= b.rows_max || s1 == s0)) {
+            rows += b.P[s1] + b.L[s1] - 1;
+            ++s1;
+        }
+        const int Tr = rows, Tp = (Tr + 7) / 8 * 8;
+        const int r0 = b.off[s0], Nr = b.off[s1] - r0;  // response tokens of this micro-batch
+        // metadata: sequences, attention blocks, response-row map
+        std::vector<train::TSeq> seqs;
+        std::vector<train::TBlk> blks;
+        std::vector<int32_t> map;
+        int row = 0;
+        for (int i = s0; i < s1; ++i) {
+            const int len = b.P[i] + b.L[i] - 1;
+            seqs.push_back({b.slot[i], b.P[i], row, len});
+            for (int q0 = 0; q0 < len; q0 += train::kBlk) blks.push_back({row, len, q0, 0});
+            for (int j = 0; j < b.L[i]; ++j) map.push_back(row + b.P[i] - 1 + j);
+            row += len;
+        }
+        std::vector<uint8_t> host;
+        auto put = [&](const void* p, size_t bytes) {
+            const size_t o = (host.size() + 255) & ~size_t(255);
+            host.resize(o + bytes);
+            std::memcpy(host.data() + o, p, bytes);
+            return o;
+        };
+        const size_t o_seq = put(seqs.data(), seqs.size() * sizeof(train::TSeq));
+        const size_t o_blk = put(blks.data(), blks.size() * sizeof(train::TBlk));
+        const size_t o_map = put(map.data(), map.size() * 4);
+        uint8_t* meta = static_cast<uint8_t*>(b.meta_dev);
+        if (host.size() > b.meta_cap) internal_error("training metadata buffer too small");
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(meta, host.data(), host.size(), cudaMemcpyHostToDevice, st));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // `host` is pageable and local
+        const auto* d_seq = reinterpret_cast<const train::TSeq*>(meta + o_seq);
+        const auto* d_blk = reinterpret_cast<const train::TBlk*>(meta + o_blk);
+        const auto* d_map = reinterpret_cast<const int32_t*>(meta + o_map);
+        const int nb = static_cast<int>(blks.size());
+        train::train_rows<<<s1 - s0, 128, 0, st>>>(d_seq, e.d_prompt, e.Pmax, e.d_tok, e.tok_stride, ts.tok, ts.pos);
+
+        // ------------------------------------------------------- forward
+        float* x = ts.x;
+        embed_rows<T><<<Tr, 128, 0, st>>>(static_cast<const T*>(m.embed), ts.tok, x, Tr, D);
+        T* h = static_cast<T*>(ts.h);
+        for (int l = 0; l < Lyr; ++l) {
+            auto& Lw = m.layers[l];
+            T* qkv = static_cast<T*>(ts.qkv[l]);
+            T* o = static_cast<T*>(ts.o[l]);
+            T* gu = static_cast<T*>(ts.gu[l]);
+            OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_in[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
+            rmsnorm<T>(e, x, Lw.ln1, h, Tr, D, st);
+            mm(e, st, h, Tr, D, Lw.wqkv, qkvw, epi(EPI_STORE, qkv, qkvw, 1.f, Lw.bqkv));
+            train::rope_rows<T><<<Tr, 128, 0, st>>>(qkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 0);
+            attn<T>(hd, 0, d_blk, nb, qkv, qkvw, H, KV, o, ts.lse[l], nullptr, nullptr, nullptr, st);
+            mm(e, st, o, Tr, qw, Lw.wo, D, epi(EPI_ADD_F32, x, D));
+            OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_mid[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
+            rmsnorm<T>(e, x, Lw.ln2, h, Tr, D, st);
+            mm(e, st, h, Tr, D, Lw.wgu, 2 * F, epi(EPI_STORE, gu, 2 * F));
+            train::swiglu_fwd<T><<<cdiv(static_cast<int64_t>(Tr) * F, 256), 256, 0, st>>>(gu, static_cast<T*>(ts.ff),
+                                                                                          static_cast<int64_t>(Tr) * F);
+            mm(e, st, ts.ff, Tr, F, Lw.wdown, D, epi(EPI_ADD_F32, x, D));
+        }
+        T* hf = static_cast<T*>(ts.hf);
+        rmsnorm<T>(e, x, m.final_norm, hf, Tr, D, st, actor ? nullptr : m.head, ts.head_out);
+
+        // ------------------------------------------------------- loss head
+        float* d_hf = ts.dh;  // dObj / d(final normed hidden), fp32 [Tr, D]
+        OPPO_CUDA_CHECK(cudaMemsetAsync(d_hf, 0, static_cast<size_t>(Tr) * D * 4, st));
+        if (actor) {
+            T* hr = static_cast<T*>(ts.hf_resp);
+            train::gather_rows_t<T><<<Nr, 128, 0, st>>>(hf, d_map, Nr, D, hr);
+            const int nt = gemm_logit_tiles(e.dtype, V);
+            Work& w = e.ws;
+            const int lrows = std::max(32, std::min(w.max_rows, static_cast<int>((static_cast<size_t>(64) << 20) / (nt * 16))));
+            for (int c0 = 0; c0 < Nr; c0 += lrows) {  // current-policy log-probs of the sampled tokens
+                const int cn = std::min(lrows, Nr - c0);
+                EpiParams ep{};
+                ep.mode = EPI_LOGITS;
+                ep.partials = w.partials;
+                ep.tgt_logit = w.tgt_logit;
+                ep.targets = b.tok + r0 + c0;
+                mm(e, st, hr + static_cast<size_t>(c0) * D, cn, D, m.lm_head, V, ep);
+                logits_combine<<<cdiv(cn, 4), 128, 0, st>>>(w.partials, nt, V, cn, nullptr, w.tgt_logit, nullptr,
+                                                            nullptr, nullptr, b.new_lp + r0 + c0, 0,
+                                                            b.lse + r0 + c0, nullptr);
+            }
+            // K10 clipped objective + dObj/dlogp over this micro-batch's tokens
+            const int cb = std::min(1024, std::max(1, cdiv(Nr, 256)));
+            ppo_clip<float><<<cb, 256, 0, st>>>(Nr, b.new_lp + r0, b.old_lp + r0, b.adv + r0, b.clip_eps, b.stats,
+                                                1e-8, b.dobj + r0, b.part, b.inv_n);
+            sum_partials_acc<<<1, 32, 0, st>>>(b.part, cb, b.obj_acc);
+            // dObj/dlogits = dobj * (onehot - softmax) in chunks: lm_head wgrad
+            // and the hidden-state dgrad
+            const PT& lm = mt.lm_head;
+            for (int c0 = 0; c0 < Nr; c0 += ts.g_rows) {
+                const int cn = std::min(ts.g_rows, Nr - c0), cp = (cn + 7) / 8 * 8;
+                EpiParams ep{};
+                ep.mode = EPI_SOFTMAX_GRAD;
+                ep.y = ts.G;
+                ep.ldy = cp;
+                ep.y2 = ts.Gt;
+                ep.ldy2 = V;
+                ep.lse = b.lse + r0 + c0;
+                ep.coef = b.dobj + r0 + c0;
+                ep.targets = b.tok + r0 + c0;
+                if (cp != cn) OPPO_CUDA_CHECK(cudaMemsetAsync(ts.G, 0, static_cast<size_t>(V) * cp * sizeof(T), st));
+                const T* hc = hr + static_cast<size_t>(c0) * D;
+                mm(e, st, hc, cn, D, m.lm_head, V, ep);
+                transpose<T>(hc, cn, D, cp, ts.hfT, st);
+                mm(e, st, ts.G, V, cp, ts.hfT, D, epi(EPI_ADD_F32, lm.grad, D));
+                mm(e, st, ts.Gt, cn, V, lm.wT, D, epi(EPI_STORE_F32, ts.dhf_c, D));
+                train::scatter_rows_f<<<cn, 128, 0, st>>>(ts.dhf_c, d_map + c0, cn, D, d_hf);
+            }
+        } else {
+            // K12 value regression toward the returns: (1/2N) sum (V - R)^2
+            train::value_loss_grad<T><<<Nr, 128, 0, st>>>(ts.head_out, hf, d_map, Nr, D, b.ret + r0, m.head, b.inv_n,
+                                                          d_hf, ts.gscr, b.sq + r0, b.v_new ? b.v_new + r0 : nullptr);
+            colsum_into(ts, ts.gscr, Nr, D, mt.head.grad, st);
+        }
+
+        // ------------------------------------------------------- backward
+        float* dx = ts.dx;
+        OPPO_CUDA_CHECK(cudaMemsetAsync(dx, 0, static_cast<size_t>(Tr) * D * 4, st));
+        train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(x, m.final_norm, d_hf, Tr, D, kEps, dx, ts.gscr);
+        colsum_into(ts, ts.gscr, Tr, D, mt.final_norm.grad, st);
+        T* dxc = static_cast<T*>(ts.dxc);
+        for (int l = Lyr - 1; l >= 0; --l) {
+            auto& Lw = m.layers[l];
+            auto& Lt = mt.layers[l];
+            T* qkv = static_cast<T*>(ts.qkv[l]);
+            T* o = static_cast<T*>(ts.o[l]);
+            T* gu = static_cast<T*>(ts.gu[l]);
+            T* ff = static_cast<T*>(ts.ff);
+            // down projection + SwiGLU
+            train::swiglu_fwd<T><<<cdiv(static_cast<int64_t>(Tr) * F, 256), 256, 0, st>>>(gu, ff, static_cast<int64_t>(Tr) * F);
+            cvt_f32<T>(dx, dxc, static_cast<int64_t>(Tr) * D, st);
+            transpose<T>(dx, Tr, D, Tp, ts.dxT, st, true);
+            transpose<T>(ff, Tr, F, Tp, ts.bT, st);
+            mm(e, st, ts.dxT, D, Tp, ts.bT, F, epi(EPI_ADD_F32, Lt.wdown.grad, F));
+            mm(e, st, dxc, Tr, D, Lt.wdown.wT, F, epi(EPI_STORE_F32, ts.dff, F));
+            train::swiglu_bwd<T><<<cdiv(static_cast<int64_t>(Tr) * F, 256), 256, 0, st>>>(
+                gu, ts.dff, static_cast<T*>(ts.dgu), static_cast<int64_t>(Tr) * F);
+            transpose<T>(ts.dgu, Tr, 2 * F, Tp, ts.aT, st);
+            rmsnorm<T>(e, ts.x_mid[l], Lw.ln2, h, Tr, D, st);
+            transpose<T>(h, Tr, D, Tp, ts.bT, st);
+            mm(e, st, ts.aT, 2 * F, Tp, ts.bT, D, epi(EPI_ADD_F32, Lt.wgu.grad, D));
+            mm(e, st, ts.dgu, Tr, 2 * F, Lt.wgu.wT, D, epi(EPI_STORE_F32, ts.dh, D));
+            train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_mid[l], Lw.ln2, ts.dh, Tr, D, kEps, dx, ts.gscr);
+            colsum_into(ts, ts.gscr, Tr, D, Lt.ln2.grad, st);
+            // O projection + attention
+            cvt_f32<T>(dx, dxc, static_cast<int64_t>(Tr) * D, st);
+            transpose<T>(dx, Tr, D, Tp, ts.dxT, st, true);
+            transpose<T>(o, Tr, qw, Tp, ts.bT, st);
+            mm(e, st, ts.dxT, D, Tp, ts.bT, qw, epi(EPI_ADD_F32, Lt.wo.grad, qw));
+            T* dO = static_cast<T*>(ts.dO);
+            mm(e, st, dxc, Tr, D, Lt.wo.wT, qw, epi(EPI_STORE, dO, qw));
+            train::attn_dvec<T><<<cdiv(static_cast<int64_t>(Tr) * H * 32, 256), 256, 0, st>>>(dO, o, Tr, H, hd, ts.dvec);
+            attn<T>(hd, 1, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
+            attn<T>(hd, 2, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
+            train::rope_rows<float><<<Tr, 128, 0, st>>>(ts.dqkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 1);
+            colsum_into(ts, ts.dqkv, Tr, qkvw, Lt.bqkv.grad, st);
+            T* dqc = static_cast<T*>(ts.dqkvc);
+            cvt_f32<T>(ts.dqkv, dqc, static_cast<int64_t>(Tr) * qkvw, st);
+            transpose<T>(ts.dqkv, Tr, qkvw, Tp, ts.aT, st, true);
+            rmsnorm<T>(e, ts.x_in[l], Lw.ln1, h, Tr, D, st);
+            transpose<T>(h, Tr, D, Tp, ts.bT, st);
+            mm(e, st, ts.aT, qkvw, Tp, ts.bT, D, epi(EPI_ADD_F32, Lt.wqkv.grad, D));
+            mm(e, st, dqc, Tr, qkvw, Lt.wqkv.wT, D, epi(EPI_STORE_F32, ts.dh, D));
+            train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_in[l], Lw.ln1, ts.dh, Tr, D, kEps, dx, ts.gscr);
+            colsum_into(ts, ts.gscr, Tr, D, Lt.ln1.grad, st);
+        }
+        train::embed_grad<<<Tr, 128, 0, st>>>(dx, ts.tok, Tr, D, mt.embed.grad);
+        OPPO_CUDA_CHECK(cudaGetLastError());
+        e.launches += 40 * Lyr + 20;
+        s0 = s1;
+    }
+}
+
+template <class T>
+void train_apply(Engine& e, int mid, float scale, bool dp, cudaStream_t st) {
+    auto& ts = *static_cast<TrainState*>(e.train_state);
+    for (PT* p : ts.m[mid].all()) {
+        if (dp) dp_allreduce_pub(e, p->grad, p->n(), false, st);
+        if (p->master)
+            train::sgd_apply<T><<<cdiv(p->n(), 256), 256, 0, st>>>(p->master, p->grad, p->n(), scale, static_cast<T*>(p->w));
+        else
+            train::sgd_apply<T><<<cdiv(p->n(), 256), 256, 0, st>>>(static_cast<float*>(p->w), p->grad, p->n(), scale,
+                                                                    static_cast<T*>(nullptr));
+    }
+    OPPO_CUDA_CHECK(cudaGetLastError());
+}
+
+template <class T>
+void train_full(Engine& e, TrainBatch& b, const oppo_ppo_hparams& hp, bool dp, cudaStream_t st) {
+    if (!e.train_state) e.train_state = new TrainState();
+    auto& ts = *static_cast<TrainState*>(e.train_state);
+    setup_model(e, ts, ACTOR, st);
+    setup_model(e, ts, CRITIC, st);
+    int max_seq = 0;
+    for (size_t i = 0; i < b.slot.size(); ++i) max_seq = std::max(max_seq, b.P[i] + b.L[i] - 1);
+    b.rows_max = std::max(b.rows_max, max_seq);
+    int max_resp = 0;  // response rows of the largest micro-batch
+    {
+        const int n = static_cast<int>(b.slot.size());
+        int s0 = 0;
+        while (s0 < n) {
+            int s1 = s0, rows = 0;
+            while (s1 < n && (rows + b.P[s1] + b.L[s1] - 1 <= b.rows_max || s1 == s0)) {
+                rows += b.P[s1] + b.L[s1] - 1;
+                ++s1;
+            }
+            max_resp = std::max(max_resp, b.off[s1] - b.off[s0]);
+            s0 = s1;
+        }
+    }
+    ensure_scratch<T>(e, ts, b.rows_max, std::max(max_resp, 8));
+    if (hp.learning_rate != 0) {
+        train_model<T>(e, b, ACTOR, st);
+        train_apply<T>(e, ACTOR, static_cast<float>(hp.learning_rate), dp, st);  // ascent (ppo.cpp:288-290)
+    }
+    if (hp.value_learning_rate != 0) {
+        train_model<T>(e, b, CRITIC, st);
+        train_apply<T>(e, CRITIC, -static_cast<float>(hp.value_learning_rate), dp, st);  // descent on (V-R)^2/2
+    }
+}
+
+// Every tensor the full update changes, for checkpoints: (device pointer,
+// bytes) of the compute tensors and fp32 masters of the actor and critic.
+std::vector<std::pair<void*, size_t>> train_tensors(Engine& e, cudaStream_t st) {
+    if (!e.train_state) e.train_state = new TrainState();
+    auto& ts = *static_cast<TrainState*>(e.train_state);
+    std::vector<std::pair<void*, size_t>> out;
+    for (int mid : {ACTOR, CRITIC}) {
+        setup_model(e, ts, mid, st);
+        for (PT* p : ts.m[mid].all()) {
+            out.emplace_back(p->w, static_cast<size_t>(p->n()) * (p->matrix ? e.esz : 4));
+            if (p->master) out.emplace_back(p->master, static_cast<size_t>(p->n()) * 4);
+        }
+    }
+    OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
+    return out;
+}
+
+template void train_full<float>(Engine&, TrainBatch&, const oppo_ppo_hparams&, bool, cudaStream_t);
+template void train_full<__nv_bfloat16>(Engine&, TrainBatch&, const oppo_ppo_hparams&, bool, cudaStream_t);
+
+}  // namespace oppo

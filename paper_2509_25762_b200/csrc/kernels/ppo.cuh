@@ -200,6 +200,15 @@ __global__ void ppo_clip(int n, const R* __restrict__ new_lp, const R* __restric
     }
 }
 
+// out[0] += sum of block partials (fixed order): accumulates the clipped
+// objective over the micro-batches of the full-parameter update.
+static __global__ void sum_partials_acc(const double* p, int n, double* out) {
+    if (threadIdx.x) return;
+    double s = 0;
+    for (int i = 0; i < n; ++i) s += p[i];
+    out[0] += s;
+}
+
 // Value-head regression on the critic's cached hidden states:
 // grad_w = (1/N) sum_t (V_t - R_t) h_t ; loss = (1/2N) sum_t (V_t - R_t)^2.
 // One CTA per 64-column slab of w, deterministic order over tokens.

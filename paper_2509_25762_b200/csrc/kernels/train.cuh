@@ -1,0 +1,474 @@
+// train.cuh — kernels of the full-parameter PPO update (K11 / K12): the
+// training forward that keeps per-layer activations, and the backward of
+// RMSNorm, RoPE, causal GQA attention and SwiGLU.  The projection GEMMs
+// (forward, dgrad, wgrad) run on the tcgen05 GEMM (gemm.cuh) / the SIMT GEMM
+// in fp32; everything here is the glue between them.
+//
+// Reference semantics: toy_rlhf_step's ascent theta += lr * grad
+// (ppo.cpp:288-290) with grad = clipped_objective_grad (ppo.cpp:138-177)
+// carried through the actor's lm_head and trunk, and the value fit toward
+// discounted returns (ppo.cpp:292-315) carried through the critic's head and
+// trunk.  The neural model itself has no reference counterpart;
+// oracle/gpt_np.py restates forward and backward in fp64.
+//
+// Training row layout: the micro-batch's sequences (prompt + response minus
+// its last token) are contiguous rows; a TBlk names a 32-row block of one
+// sequence (rows [row0 + q0, row0 + min(q0 + 32, len))).
+#pragma once
+
+#include "common.cuh"
+
+namespace oppo {
+namespace train {
+
+constexpr int kBlk = 32;  // query / key rows per attention block
+
+struct TBlk {
+    int32_t row0;  // first row of the sequence
+    int32_t len;   // rows of the sequence
+    int32_t q0;    // block start within the sequence
+    int32_t _pad;
+};
+
+// ------------------------------------------------------------------ rows
+// Per-row input token and position of each sequence of the micro-batch:
+// token q of sequence i is prompt[q] (q < P) or response token q - P + 1.
+struct TSeq {
+    int32_t slot, prompt_len, row0, len;  // len = prompt_len + target_len - 1
+};
+static __global__ void train_rows(const TSeq* __restrict__ seqs, const int32_t* __restrict__ prompt_buf,
+                           int prompt_stride, const int32_t* __restrict__ tok_buf, int tok_stride,
+                           int32_t* __restrict__ tok, int32_t* __restrict__ pos) {
+    const TSeq s = seqs[blockIdx.x];
+    for (int q = threadIdx.x; q < s.len; q += blockDim.x) {
+        tok[s.row0 + q] = q < s.prompt_len ? prompt_buf[static_cast<size_t>(s.slot) * prompt_stride + q]
+                                           : tok_buf[static_cast<size_t>(s.slot) * tok_stride + q - s.prompt_len + 1];
+        pos[s.row0 + q] = q;
+    }
+}
+
+// ------------------------------------------------------------------ RoPE
+// Rotate-half RoPE of the q and k heads of each row (in place), angle
+// pos * theta^(-2d/hd); inverse = the transpose (backward of the rotation).
+template <class T>
+__global__ void rope_rows(T* __restrict__ qkv, int ld, int rows, const int32_t* __restrict__ pos,
+                          int heads_qk, int hd, float theta, int inverse) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int half = hd / 2;
+    const float p = static_cast<float>(pos[r]);
+    T* row = qkv + static_cast<size_t>(r) * ld;
+    for (int i = threadIdx.x; i < heads_qk * half; i += blockDim.x) {
+        const int h = i / half, d = i % half;
+        const float inv = powf(theta, -2.0f * d / hd);
+        float sn, cs;
+        sincosf(p * inv, &sn, &cs);
+        if (inverse) sn = -sn;
+        T* x = row + h * hd;
+        const float x1 = tof(x[d]), x2 = tof(x[d + half]);
+        x[d] = fromf<T>(x1 * cs - x2 * sn);
+        x[d + half] = fromf<T>(x2 * cs + x1 * sn);
+    }
+}
+
+// ------------------------------------------------------------- attention
+// Causal GQA attention of the training forward, one CTA per (32-query block,
+// q head): online softmax over the sequence's key blocks.  Writes O and the
+// per-(row, head) log-sum-exp for the backward.  fp32 arithmetic (SIMT).
+template <int HD>
+struct AttnT {
+    static constexpr int P = HD + 1;                 // padded smem row
+    static constexpr int DPT = HD / 8;               // head dims per thread (8 threads per row)
+    static constexpr int SMEM_FWD = (3 * kBlk * P + kBlk * (kBlk + 1)) * 4;
+    static constexpr int SMEM_BWD = (4 * kBlk * P + 2 * kBlk * (kBlk + 1)) * 4;
+};
+
+template <class T, int HD>
+__device__ __forceinline__ void load_tile(float* dst, const T* __restrict__ src, size_t ld, int r0, int n, int col) {
+    constexpr int P = HD + 1;
+    for (int i = threadIdx.x; i < kBlk * HD; i += blockDim.x) {
+        const int r = i / HD, d = i % HD;
+        dst[r * P + d] = r < n ? tof(src[static_cast<size_t>(r0 + r) * ld + col + d]) : 0.f;
+    }
+}
+
+template <class T, int HD>
+__global__ void __launch_bounds__(256) attn_train_fwd(const TBlk* __restrict__ blks, const T* __restrict__ qkv,
+                                                      int ld, int H, int KV, T* __restrict__ out,
+                                                      float* __restrict__ lse) {
+    using A = AttnT<HD>;
+    extern __shared__ float sm[];
+    float* Qs = sm;
+    float* Ks = Qs + kBlk * A::P;
+    float* Vs = Ks + kBlk * A::P;
+    float* Ps = Vs + kBlk * A::P;  // [32][33]
+    const TBlk b = blks[blockIdx.x];
+    const int h = blockIdx.y, kvh = h / (H / KV);
+    const int nq = min(kBlk, b.len - b.q0);
+    const int t = threadIdx.x, i = t >> 3, sub = t & 7;
+    const float scale = rsqrtf(static_cast<float>(HD));
+    load_tile<T, HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    float acc[A::DPT];
+#pragma unroll
+    for (int k = 0; k < A::DPT; ++k) acc[k] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int k0 = 0; k0 < b.q0 + nq; k0 += kBlk) {
+        const int nk = min(kBlk, b.len - k0);
+        __syncthreads();
+        load_tile<T, HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+        load_tile<T, HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+        __syncthreads();
+        float s[4];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int j = sub * 4 + c;
+            float dot = 0.f;
+#pragma unroll 8
+            for (int d = 0; d < HD; ++d) dot = fmaf(Qs[i * A::P + d], Ks[j * A::P + d], dot);
+            const bool ok = j < nk && k0 + j <= b.q0 + i && i < nq;
+            s[c] = ok ? dot * scale : -INFINITY;
+            mx = fmaxf(mx, s[c]);
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float mn = fmaxf(m, mx);
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float p = mn == -INFINITY ? 0.f : __expf(s[c] - mn);
+            rs += p;
+            Ps[i * (kBlk + 1) + sub * 4 + c] = p;
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        const float corr = (m == -INFINITY) ? 0.f : __expf(m - mn);
+        l = l * corr + rs;
+        m = mn;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < A::DPT; ++k) {
+            const int d = sub + 8 * k;
+            float a = acc[k] * corr;
+            for (int j = 0; j < nk; ++j) a = fmaf(Ps[i * (kBlk + 1) + j], Vs[j * A::P + d], a);
+            acc[k] = a;
+        }
+    }
+    if (i < nq) {
+        const size_t r = static_cast<size_t>(b.row0 + b.q0 + i);
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int k = 0; k < A::DPT; ++k) out[r * (H * HD) + h * HD + sub + 8 * k] = fromf<T>(acc[k] * inv);
+        if (sub == 0) lse[r * H + h] = m + logf(l);
+    }
+}
+
+// D[r, h] = sum_d dO[r, h, d] * O[r, h, d]: one warp per (row, head).
+template <class T>
+__global__ void attn_dvec(const T* __restrict__ dout, const T* __restrict__ out, int rows, int H, int hd,
+                          float* __restrict__ dv) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows * H) return;
+    const size_t base = static_cast<size_t>(w) * hd;  // [r][h][d] == [(r*H+h)][d]
+    float s = 0.f;
+    for (int d = lane; d < hd; d += 32) s = fmaf(tof(dout[base + d]), tof(out[base + d]), s);
+    s = warp_sum(s);
+    if (lane == 0) dv[w] = s;
+}
+
+// dQ of one (query block, q head): loop over the causal key blocks.
+template <class T, int HD>
+__global__ void __launch_bounds__(256) attn_train_dq(const TBlk* __restrict__ blks, const T* __restrict__ qkv,
+                                                     int ld, int H, int KV, const T* __restrict__ dout,
+                                                     const float* __restrict__ lse, const float* __restrict__ dvec,
+                                                     float* __restrict__ dqkv, int ldd) {
+    using A = AttnT<HD>;
+    extern __shared__ float sm[];
+    float* Qs = sm;
+    float* Ks = Qs + kBlk * A::P;
+    float* Vs = Ks + kBlk * A::P;
+    float* dOs = Vs + kBlk * A::P;
+    float* Ss = dOs + kBlk * A::P;  // dS [32][33]
+    const TBlk b = blks[blockIdx.x];
+    const int h = blockIdx.y, kvh = h / (H / KV);
+    const int nq = min(kBlk, b.len - b.q0);
+    const int t = threadIdx.x, i = t >> 3, sub = t & 7;
+    const float scale = rsqrtf(static_cast<float>(HD));
+    load_tile<T, HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    load_tile<T, HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + b.q0, nq, h * HD);
+    const size_t ri = static_cast<size_t>(b.row0 + b.q0 + min(i, nq - 1));
+    const float lse_i = lse[ri * H + h], d_i = dvec[ri * H + h];
+    float acc[A::DPT];
+#pragma unroll
+    for (int k = 0; k < A::DPT; ++k) acc[k] = 0.f;
+    for (int k0 = 0; k0 < b.q0 + nq; k0 += kBlk) {
+        const int nk = min(kBlk, b.len - k0);
+        __syncthreads();
+        load_tile<T, HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+        load_tile<T, HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int j = sub * 4 + c;
+            float s = 0.f, dp = 0.f;
+#pragma unroll 8
+            for (int d = 0; d < HD; ++d) {
+                s = fmaf(Qs[i * A::P + d], Ks[j * A::P + d], s);
+                dp = fmaf(dOs[i * A::P + d], Vs[j * A::P + d], dp);
+            }
+            const bool ok = j < nk && k0 + j <= b.q0 + i && i < nq;
+            const float p = ok ? __expf(s * scale - lse_i) : 0.f;
+            Ss[i * (kBlk + 1) + j] = p * (dp - d_i);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < A::DPT; ++k) {
+            const int d = sub + 8 * k;
+            float a = acc[k];
+            for (int j = 0; j < nk; ++j) a = fmaf(Ss[i * (kBlk + 1) + j], Ks[j * A::P + d], a);
+            acc[k] = a;
+        }
+    }
+    if (i < nq) {
+        const size_t r = static_cast<size_t>(b.row0 + b.q0 + i);
+#pragma unroll
+        for (int k = 0; k < A::DPT; ++k) dqkv[r * ldd + h * HD + sub + 8 * k] = acc[k] * scale;
+    }
+}
+
+// dK, dV of one (key block, kv head): loop over the G query heads of the
+// group and the query blocks at or after the key block (causal).
+template <class T, int HD>
+__global__ void __launch_bounds__(256) attn_train_dkv(const TBlk* __restrict__ blks, const T* __restrict__ qkv,
+                                                      int ld, int H, int KV, const T* __restrict__ dout,
+                                                      const float* __restrict__ lse, const float* __restrict__ dvec,
+                                                      float* __restrict__ dqkv, int ldd) {
+    using A = AttnT<HD>;
+    extern __shared__ float sm[];
+    float* Ks = sm;
+    float* Vs = Ks + kBlk * A::P;
+    float* Qs = Vs + kBlk * A::P;
+    float* dOs = Qs + kBlk * A::P;
+    float* Ps = dOs + kBlk * A::P;    // P^T [key j][query i]
+    float* dSs = Ps + kBlk * (kBlk + 1);
+    const TBlk b = blks[blockIdx.x];  // q0 = key block start
+    const int kvh = blockIdx.y, G = H / KV;
+    const int k0 = b.q0, nk = min(kBlk, b.len - k0);
+    const int t = threadIdx.x, j = t >> 3, sub = t & 7;
+    const float scale = rsqrtf(static_cast<float>(HD));
+    load_tile<T, HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+    load_tile<T, HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+    float dk[A::DPT], dv[A::DPT];
+#pragma unroll
+    for (int k = 0; k < A::DPT; ++k) dk[k] = dv[k] = 0.f;
+    for (int g = 0; g < G; ++g) {
+        const int h = kvh * G + g;
+        for (int q0 = k0; q0 < b.len; q0 += kBlk) {
+            const int nq = min(kBlk, b.len - q0);
+            __syncthreads();
+            load_tile<T, HD>(Qs, qkv, ld, b.row0 + q0, nq, h * HD);
+            load_tile<T, HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + q0, nq, h * HD);
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int i = sub * 4 + c;
+                float s = 0.f, dp = 0.f;
+#pragma unroll 8
+                for (int d = 0; d < HD; ++d) {
+                    s = fmaf(Ks[j * A::P + d], Qs[i * A::P + d], s);
+                    dp = fmaf(Vs[j * A::P + d], dOs[i * A::P + d], dp);
+                }
+                const bool ok = i < nq && j < nk && k0 + j <= q0 + i;
+                const size_t ri = static_cast<size_t>(b.row0 + q0 + min(i, nq - 1));
+                const float p = ok ? __expf(s * scale - lse[ri * H + h]) : 0.f;
+                Ps[j * (kBlk + 1) + i] = p;
+                dSs[j * (kBlk + 1) + i] = ok ? p * (dp - dvec[ri * H + h]) : 0.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < A::DPT; ++k) {
+                const int d = sub + 8 * k;
+                float a = dv[k], c2 = dk[k];
+                for (int i = 0; i < nq; ++i) {
+                    a = fmaf(Ps[j * (kBlk + 1) + i], dOs[i * A::P + d], a);
+                    c2 = fmaf(dSs[j * (kBlk + 1) + i], Qs[i * A::P + d], c2);
+                }
+                dv[k] = a;
+                dk[k] = c2;
+            }
+        }
+    }
+    if (j < nk) {
+        const size_t r = static_cast<size_t>(b.row0 + k0 + j);
+#pragma unroll
+        for (int k = 0; k < A::DPT; ++k) {
+            dqkv[r * ldd + (H + kvh) * HD + sub + 8 * k] = dk[k] * scale;
+            dqkv[r * ldd + (H + KV + kvh) * HD + sub + 8 * k] = dv[k];
+        }
+    }
+}
+
+// ----------------------------------------------------------------- SwiGLU
+// gu [rows, 2F] interleaved (gate_i, up_i) -> ff [rows, F] = silu(g) * u
+template <class T>
+__global__ void swiglu_fwd(const T* __restrict__ gu, T* __restrict__ ff, int64_t n /* rows*F */) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const float g = tof(gu[2 * i]), u = tof(gu[2 * i + 1]);
+    ff[i] = fromf<T>(g / (1.f + __expf(-g)) * u);
+}
+// d(gu) from d(ff) (fp32)
+template <class T>
+__global__ void swiglu_bwd(const T* __restrict__ gu, const float* __restrict__ dff, T* __restrict__ dgu,
+                           int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const float g = tof(gu[2 * i]), u = tof(gu[2 * i + 1]), d = dff[i];
+    const float sg = 1.f / (1.f + __expf(-g));
+    dgu[2 * i] = fromf<T>(d * u * sg * (1.f + g * (1.f - sg)));
+    dgu[2 * i + 1] = fromf<T>(d * g * sg);
+}
+
+// --------------------------------------------------------------- RMSNorm
+// y = x * r * g, r = rsqrt(mean(x^2) + eps): dx += r * (dy*g - xh * mean(dy*g*xh)),
+// gscr[row] = dy * xh (the gamma gradient's per-row terms).  One warp per row.
+static __global__ void rms_bwd(const float* __restrict__ x, const float* __restrict__ g, const float* __restrict__ dy,
+                        int rows, int d, float eps, float* __restrict__ dx, float* __restrict__ gscr) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float* xr = x + static_cast<size_t>(w) * d;
+    const float* dr = dy + static_cast<size_t>(w) * d;
+    float ss = 0.f;
+    for (int c = lane; c < d; c += 32) ss = fmaf(xr[c], xr[c], ss);
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss / d + eps);
+    float dot = 0.f;
+    for (int c = lane; c < d; c += 32) dot = fmaf(dr[c] * g[c], xr[c] * r, dot);
+    dot = warp_sum(dot) / d;
+    float* o = dx + static_cast<size_t>(w) * d;
+    float* gs = gscr + static_cast<size_t>(w) * d;
+    for (int c = lane; c < d; c += 32) {
+        const float xh = xr[c] * r;
+        o[c] += r * (dr[c] * g[c] - xh * dot);
+        gs[c] = dr[c] * xh;
+    }
+}
+
+// --------------------------------------------------- column sums (deterministic)
+// stage 1: part[chunk][c] = sum of rows [chunk*per, (chunk+1)*per) of column c
+static __global__ void colsum_part(const float* __restrict__ x, int rows, int cols, int ld, int per,
+                            float* __restrict__ part) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+    float s = 0.f;
+    for (int r = r0; r < r1; ++r) s += x[static_cast<size_t>(r) * ld + c];
+    part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
+}
+// stage 2: out[c] += sum over chunks (fixed order)
+static __global__ void colsum_final(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    float s = 0.f;
+    for (int k = 0; k < chunks; ++k) s += part[static_cast<size_t>(k) * cols + c];
+    out[c] += s;
+}
+
+// ----------------------------------------------------------------- misc
+// out[c][r] = in[r][c] (rows padded to ld_out with zeros), with conversion
+template <class S, class D>
+__global__ void transpose_cvt(const S* __restrict__ in, int rows, int cols, int ld_in, int ld_out,
+                              D* __restrict__ out) {
+    __shared__ float tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < rows && c < cols) ? tof(in[static_cast<size_t>(r) * ld_in + c]) : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < ld_out) out[static_cast<size_t>(c) * ld_out + r] = fromf<D>(tile[threadIdx.x][i]);
+    }
+}
+
+// embedding gradient: g[tok[r]] += dx[r]
+static __global__ void embed_grad(const float* __restrict__ dx, const int32_t* __restrict__ tok, int rows, int d,
+                           float* __restrict__ g) {
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    float* dst = g + static_cast<size_t>(tok[r]) * d;
+    const float* src = dx + static_cast<size_t>(r) * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(dst + c, src[c]);
+}
+
+// response rows <-> training rows: map[k] = training row of response token k
+template <class T>
+__global__ void gather_rows_t(const T* __restrict__ src, const int32_t* __restrict__ map, int n, int d,
+                              T* __restrict__ dst) {
+    const int k = blockIdx.x;
+    if (k >= n) return;
+    const T* s = src + static_cast<size_t>(map[k]) * d;
+    T* o = dst + static_cast<size_t>(k) * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = s[c];
+}
+static __global__ void scatter_rows_f(const float* __restrict__ src, const int32_t* __restrict__ map, int n, int d,
+                               float* __restrict__ dst) {
+    const int k = blockIdx.x;
+    if (k >= n) return;
+    float* o = dst + static_cast<size_t>(map[k]) * d;
+    const float* s = src + static_cast<size_t>(k) * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = s[c];
+}
+
+// Critic regression head on the response rows: v_k = head_out[map[k]],
+// dv = (v - target) * inv_n; d_hf[map[k]] = dv * w; gscr[k] = dv * hf[map[k]]
+// (the head gradient's per-row terms); sq[k] = (v - target)^2.
+template <class T>
+__global__ void value_loss_grad(const float* __restrict__ head_out, const T* __restrict__ hf,
+                                const int32_t* __restrict__ map, int n, int d, const float* __restrict__ target,
+                                const float* __restrict__ w, float inv_n, float* __restrict__ d_hf,
+                                float* __restrict__ gscr, float* __restrict__ sq, float* __restrict__ v_out) {
+    const int k = blockIdx.x;
+    if (k >= n) return;
+    const int r = map[k];
+    const float e = head_out[r] - target[k];
+    const float dv = e * inv_n;
+    if (threadIdx.x == 0) {
+        sq[k] = e * e;
+        if (v_out) v_out[k] = head_out[r];
+    }
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        d_hf[static_cast<size_t>(r) * d + c] = dv * w[c];
+        gscr[static_cast<size_t>(k) * d + c] = dv * tof(hf[static_cast<size_t>(r) * d + c]);
+    }
+}
+
+// SGD on one tensor: p += scale * g (fp32 parameter / master), and the
+// compute copy w = round(p) when w is a separate (bf16) tensor.
+template <class T>
+__global__ void sgd_apply(float* __restrict__ p, const float* __restrict__ g, int64_t n, float scale,
+                          T* __restrict__ w) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const float v = p[i] + scale * g[i];
+    p[i] = v;
+    if (w) w[i] = fromf<T>(v);
+}
+
+static __global__ void sum_to_double(const float* __restrict__ x, int n, double* __restrict__ out) {
+    double s = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    s = warp_sum_d(s);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) t += sh[i];
+        *out += t;
+    }
+}
+
+}  // namespace train
+}  // namespace oppo
