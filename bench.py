@@ -5,12 +5,16 @@ Workload (configs[1]): 0.5B-shaped actor + 0.5B reward / critic / reference,
 bf16, 256 prompts of 128 tokens per GPU, lognormal(5.0, 1.0) response lengths
 capped at 1024, chunk 64, overcommit delta 26 (10%).  One step = refill ->
 run_step (lockstep actor decode || streamed scorer prefill) -> select the
-first B finishers -> PPO update (GAE, whitening, clipped loss, lm_head and
-value-head update).  Reported next to the same binary with overlap disabled
+first B finishers -> PPO update (GAE, whitening, clipped loss, full-parameter
+actor and critic update).  Reported next to the same binary with overlap disabled
 (RunConfig::baseline(): delta 0, sequential scoring) and next to the
 reference's own CPU path (oracle/_ref run_seed, toy policy) on the host cores.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+The PPO update trains every parameter of the actor and the critic
+(train_heads=2: training forward + backward through all layers, SGD on fp32
+masters), as the reference's toy_rlhf_step updates every policy parameter.
 """
 import argparse
 import ctypes as C
@@ -351,7 +355,7 @@ def ours(args):
             eng = Engine(wl["actor"], wl["scorer"], wl["scorer"], wl["scorer"], dtype=abi.DTYPE_BF16,
                          max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
                          max_response_len=wl["cap"], page_size=64, device=local,
-                         carry=cfg.carry_granularity, train_heads=1, sample_seed=2 + rank,
+                         carry=cfg.carry_granularity, train_heads=2, sample_seed=2 + rank,
                          weight_seed=1, scorer_sms=args.scorer_sms if not base else 0,
                          nccl_comm=comm, rank=rank, world=world)
             recs, wall = run_arm(eng, wl, cfg, 7, args.steps, args.warmup, rank, world, dist)

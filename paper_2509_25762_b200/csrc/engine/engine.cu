@@ -1911,7 +1911,8 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     for (int i = 0; i < n; ++i) meta_bytes += 16 * cdiv(e.slots[slots[i]].prompt_len + off[i + 1] - off[i], 32);
     const size_t need = static_cast<size_t>(Npad) * (4 * 14) + static_cast<size_t>(n + 1) * 20 * 4 +
                         static_cast<size_t>(Npad) * (Da + Dc) * sizeof(T) + 4096 * 8 + 1024 +
-                        meta_bytes + static_cast<size_t>(n) * 16 + 16384;
+                        meta_bytes + static_cast<size_t>(n) * 16 + 16384 +
+                        static_cast<size_t>(Npad + n * (e.Pmax + 1)) * 12;
     if (need > e.ppo_buf_bytes) {
         if (e.ppo_buf) cudaFree(e.ppo_buf);
         e.ppo_buf_bytes = need * 3 / 2;
@@ -2062,7 +2063,9 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
         // micro-batch metadata: sequences, 32-row attention blocks, response-row map
         size_t blocks = 0;
         for (int i = 0; i < n; ++i) blocks += cdiv(tb.P[i] + tb.L[i] - 1, 32);
-        tb.meta_cap = static_cast<size_t>(n) * 16 + blocks * 16 + static_cast<size_t>(N) * 4 + 4096;
+        size_t rows_all = 0;
+        for (int i = 0; i < n; ++i) rows_all += tb.P[i] + tb.L[i] - 1;
+        tb.meta_cap = static_cast<size_t>(n) * 16 + blocks * 16 + static_cast<size_t>(N) * 4 + rows_all * 12 + 8192;
         tb.meta_dev = take(tb.meta_cap);
         if (e.dtype == OPPO_DTYPE_F32) train_full<float>(e, tb, hp, dp, st);
         else train_full<__nv_bfloat16>(e, tb, hp, dp, st);
@@ -2514,7 +2517,14 @@ oppo_status oppo_get_tensor(oppo_engine* eh, int32_t model, const char* name, in
         if (model < 0 || model >= oppo::N_MODELS) oppo::input_error("bad model id");
         auto& m = e->models[model];
         const auto& d = m.dims;
-        const std::string nm(name);
+        std::string nm(name);
+        // "<tensor>:master": the fp32 master of a bf16 matrix trained by the
+        // full-parameter update (else the tensor itself)
+        bool want_master = false;
+        if (nm.size() > 7 && nm.compare(nm.size() - 7, 7, ":master") == 0) {
+            want_master = true;
+            nm.resize(nm.size() - 7);
+        }
         const void* ptr = nullptr;
         int64_t n = 0;
         bool is_f32 = false;
@@ -2535,6 +2545,11 @@ oppo_status oppo_get_tensor(oppo_engine* eh, int32_t model, const char* name, in
             else if (nm == "ln2") { ptr = L.ln2; n = D; is_f32 = true; }
             else oppo::input_error("unknown tensor " + nm);
         }
+        if (want_master)
+            if (const float* mp = oppo::train_master(*e, model, nm, layer)) {
+                ptr = mp;
+                is_f32 = true;
+            }
         *n_out = n;
         if (!ptr || n == 0 || !out) return;  // size query
         if (cap < n) oppo::input_error("buffer too small");

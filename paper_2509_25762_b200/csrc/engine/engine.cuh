@@ -255,6 +255,7 @@ template <class T>
 void train_full(Engine& e, TrainBatch& b, const oppo_ppo_hparams& hp, bool dp, cudaStream_t st);
 void train_free(Engine& e);
 std::vector<std::pair<void*, size_t>> train_tensors(Engine& e, cudaStream_t st);
+const float* train_master(Engine& e, int model, const std::string& name, int layer);
 // engine.cu
 void dp_allreduce_pub(Engine& e, void* buf, int64_t count, bool f64, cudaStream_t st);
 

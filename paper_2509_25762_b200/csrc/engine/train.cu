@@ -17,11 +17,15 @@
 // fp32 masters, from which the bf16 compute weights are re-rounded.
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
+#include <string>
+#include <type_traits>
 #include <vector>
 
 #include "engine.cuh"
 #include "kernels/ppo.cuh"
 #include "kernels/train.cuh"
+#include "kernels/attn_train_mma.cuh"
 
 namespace oppo {
 
@@ -234,10 +238,47 @@ void attn_launch(int which, const train::TBlk* blks, int nb, const T* qkv, int l
     else
         train::attn_train_dkv<T, HD><<<dim3(nb, KV), 256, A::SMEM_BWD, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
 }
+template <int HD>
+void attn_mma_launch(int which, const train::TBlk* blks, int nb, const __nv_bfloat16* qkv, int ld, int H, int KV,
+                     __nv_bfloat16* o, float* lse, const __nv_bfloat16* dO, const float* dvec, float* dqkv,
+                     cudaStream_t st) {
+    using M = train::MmaT<HD>;
+    static bool attr = false;
+    if (!attr) {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::attn_fwd_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             M::SMEM_FWD));
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::attn_dq_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             M::SMEM_DQ));
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::attn_dkv_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             M::SMEM_DKV));
+        attr = true;
+    }
+    if (which == 0)
+        train::attn_fwd_mma<HD><<<dim3(nb, H), 128, M::SMEM_FWD, st>>>(blks, qkv, ld, H, KV, o, lse);
+    else if (which == 1)
+        train::attn_dq_mma<HD><<<dim3(nb, H), 128, M::SMEM_DQ, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
+    else
+        train::attn_dkv_mma<HD><<<dim3(nb, KV), 128, M::SMEM_DKV, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
+}
+
+// tensor-core (mma.sync) attention for bf16 with head_dim 64 / 128 (64-row
+// blocks), the SIMT kernels otherwise (fp32 engine, head_dim 32; 32-row blocks)
+template <class T>
+constexpr bool use_mma_attn(int hd) {
+    return std::is_same_v<T, __nv_bfloat16> && (hd == 64 || hd == 128);
+}
+
 template <class T>
 void attn(int hd, int which, const train::TBlk* blks, int nb, const T* qkv, int ld, int H, int KV, T* o, float* lse,
           const T* dO, const float* dvec, float* dqkv, cudaStream_t st) {
     if (nb <= 0) return;
+    if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+        if (use_mma_attn<T>(hd) && std::getenv("OPPO_TRAIN_SIMT_ATTN") == nullptr) {
+            if (hd == 64) attn_mma_launch<64>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st);
+            else attn_mma_launch<128>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st);
+            return;
+        }
+    }
     switch (hd) {
     case 32: attn_launch<T, 32>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st); break;
     case 64: attn_launch<T, 64>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st); break;
@@ -247,7 +288,8 @@ void attn(int hd, int which, const train::TBlk* blks, int nb, const T* qkv, int 
 
 // Sizes the scratch for `rows` training rows of the largest trained model.
 template <class T>
-void ensure_scratch(Engine& e, TrainState& ts, int rows, int resp_rows) {
+void ensure_scratch(Engine& e, TrainState& ts, int rows) {
+    const int resp_rows = rows;  // a micro-batch never has more response rows than rows
     int L = 0, D = 0, qkv = 0, qw = 0, F = 0, H = 0, V = 0;
     for (int mid : {ACTOR, CRITIC}) {
         const Model& m = e.models[mid];
@@ -293,7 +335,7 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows, int resp_rows) {
     ts.dxc = ts.scr.take(R * D * es);
     ts.dxT = ts.scr.take(Rp * D * es);
     ts.aT = ts.scr.take(Rp * wide * es);
-    ts.bT = ts.scr.take(Rp * std::max(D, F) * es);
+    ts.bT = ts.scr.take(Rp * std::max({D, F, qw}) * es);
     ts.dO = ts.scr.take(R * qw * es);
     ts.dqkvc = ts.scr.take(R * qkv * es);
     ts.tok = static_cast<int32_t*>(ts.scr.take(R * 4));
@@ -344,10 +386,12 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
         std::vector<train::TBlk> blks;
         std::vector<int32_t> map;
         int row = 0;
+        const int blk = (use_mma_attn<T>(hd) && std::getenv("OPPO_TRAIN_SIMT_ATTN") == nullptr) ? train::kMBlk
+                                                                                              : train::kBlk;
         for (int i = s0; i < s1; ++i) {
             const int len = b.P[i] + b.L[i] - 1;
             seqs.push_back({b.slot[i], b.P[i], row, len});
-            for (int q0 = 0; q0 < len; q0 += train::kBlk) blks.push_back({row, len, q0, 0});
+            for (int q0 = 0; q0 < len; q0 += blk) blks.push_back({row, len, q0, 0});
             for (int j = 0; j < b.L[i]; ++j) map.push_back(row + b.P[i] - 1 + j);
             row += len;
         }
@@ -364,12 +408,40 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
         uint8_t* meta = static_cast<uint8_t*>(b.meta_dev);
         if (host.size() > b.meta_cap) internal_error("training metadata buffer too small");
         OPPO_CUDA_CHECK(cudaMemcpyAsync(meta, host.data(), host.size(), cudaMemcpyHostToDevice, st));
-        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // `host` is pageable and local
         const auto* d_seq = reinterpret_cast<const train::TSeq*>(meta + o_seq);
         const auto* d_blk = reinterpret_cast<const train::TBlk*>(meta + o_blk);
         const auto* d_map = reinterpret_cast<const int32_t*>(meta + o_map);
         const int nb = static_cast<int>(blks.size());
         train::train_rows<<<s1 - s0, 128, 0, st>>>(d_seq, e.d_prompt, e.Pmax, e.d_tok, e.tok_stride, ts.tok, ts.pos);
+        // rows grouped by input token (CSR) for the deterministic embedding gradient
+        std::vector<int32_t> toks(Tr);
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(toks.data(), ts.tok, Tr * 4, cudaMemcpyDeviceToHost, st));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // also: `host` (pageable, local) has been read
+        std::vector<int32_t> order(Tr);
+        for (int r = 0; r < Tr; ++r) order[r] = r;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return toks[a] < toks[c]; });
+        std::vector<int32_t> uniq, start;
+        for (int k = 0; k < Tr; ++k)
+            if (k == 0 || toks[order[k]] != toks[order[k - 1]]) {
+                uniq.push_back(toks[order[k]]);
+                start.push_back(k);
+            }
+        start.push_back(Tr);
+        std::vector<uint8_t> host2;
+        auto put2 = [&](const void* p, size_t bytes) {
+            const size_t o = (host2.size() + 255) & ~size_t(255);
+            host2.resize(o + bytes);
+            std::memcpy(host2.data() + o, p, bytes);
+            return o;
+        };
+        const size_t o_u = put2(uniq.data(), uniq.size() * 4), o_s = put2(start.data(), start.size() * 4),
+                     o_r = put2(order.data(), order.size() * 4);
+        const size_t base2 = (host.size() + 255) & ~size_t(255);
+        if (base2 + host2.size() > b.meta_cap) internal_error("training metadata buffer too small");
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(meta + base2, host2.data(), host2.size(), cudaMemcpyHostToDevice, st));
+        const auto* d_uniq = reinterpret_cast<const int32_t*>(meta + base2 + o_u);
+        const auto* d_start = reinterpret_cast<const int32_t*>(meta + base2 + o_s);
+        const auto* d_order = reinterpret_cast<const int32_t*>(meta + base2 + o_r);
 
         // ------------------------------------------------------- forward
         float* x = ts.x;
@@ -502,8 +574,10 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_in[l], Lw.ln1, ts.dh, Tr, D, kEps, dx, ts.gscr);
             colsum_into(ts, ts.gscr, Tr, D, Lt.ln1.grad, st);
         }
-        train::embed_grad<<<Tr, 128, 0, st>>>(dx, ts.tok, Tr, D, mt.embed.grad);
+        train::embed_grad_csr<<<static_cast<int>(uniq.size()), 128, 0, st>>>(dx, d_uniq, d_start, d_order, D,
+                                                                              mt.embed.grad);
         OPPO_CUDA_CHECK(cudaGetLastError());
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // host2 (pageable, local) has been read
         e.launches += 40 * Lyr + 20;
         s0 = s1;
     }
@@ -532,21 +606,7 @@ void train_full(Engine& e, TrainBatch& b, const oppo_ppo_hparams& hp, bool dp, c
     int max_seq = 0;
     for (size_t i = 0; i < b.slot.size(); ++i) max_seq = std::max(max_seq, b.P[i] + b.L[i] - 1);
     b.rows_max = std::max(b.rows_max, max_seq);
-    int max_resp = 0;  // response rows of the largest micro-batch
-    {
-        const int n = static_cast<int>(b.slot.size());
-        int s0 = 0;
-        while (s0 < n) {
-            int s1 = s0, rows = 0;
-            while (s1 < n && (rows + b.P[s1] + b.L[s1] - 1 <= b.rows_max || s1 == s0)) {
-                rows += b.P[s1] + b.L[s1] - 1;
-                ++s1;
-            }
-            max_resp = std::max(max_resp, b.off[s1] - b.off[s0]);
-            s0 = s1;
-        }
-    }
-    ensure_scratch<T>(e, ts, b.rows_max, std::max(max_resp, 8));
+    ensure_scratch<T>(e, ts, b.rows_max);
     if (hp.learning_rate != 0) {
         train_model<T>(e, b, ACTOR, st);
         train_apply<T>(e, ACTOR, static_cast<float>(hp.learning_rate), dp, st);  // ascent (ppo.cpp:288-290)
@@ -572,6 +632,23 @@ std::vector<std::pair<void*, size_t>> train_tensors(Engine& e, cudaStream_t st) 
     }
     OPPO_CUDA_CHECK(cudaStreamSynchronize(st));
     return out;
+}
+
+const float* train_master(Engine& e, int model, const std::string& name, int layer) {
+    auto* ts = static_cast<TrainState*>(e.train_state);
+    if (!ts || model < 0 || model >= N_MODELS || !ts->m[model].ready) return nullptr;
+    ModelT& m = ts->m[model];
+    PT* p = nullptr;
+    if (name == "embed") p = &m.embed;
+    else if (name == "lm_head") p = &m.lm_head;
+    else if (layer >= 0 && layer < static_cast<int>(m.layers.size())) {
+        auto& L = m.layers[layer];
+        if (name == "wqkv") p = &L.wqkv;
+        else if (name == "wo") p = &L.wo;
+        else if (name == "wgu") p = &L.wgu;
+        else if (name == "wdown") p = &L.wdown;
+    }
+    return p ? p->master : nullptr;
 }
 
 template void train_full<float>(Engine&, TrainBatch&, const oppo_ppo_hparams&, bool, cudaStream_t);

@@ -392,14 +392,20 @@ __global__ void transpose_cvt(const S* __restrict__ in, int rows, int cols, int 
     }
 }
 
-// embedding gradient: g[tok[r]] += dx[r]
-static __global__ void embed_grad(const float* __restrict__ dx, const int32_t* __restrict__ tok, int rows, int d,
-                           float* __restrict__ g) {
-    const int r = blockIdx.x;
-    if (r >= rows) return;
-    float* dst = g + static_cast<size_t>(tok[r]) * d;
-    const float* src = dx + static_cast<size_t>(r) * d;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(dst + c, src[c]);
+// Embedding gradient, deterministic: one CTA per distinct token u of the
+// micro-batch sums its rows (CSR: rows[start[u] .. start[u+1]), ascending) in
+// a fixed order, then g[uniq[u]] += sum.
+static __global__ void embed_grad_csr(const float* __restrict__ dx, const int32_t* __restrict__ uniq,
+                                      const int32_t* __restrict__ start, const int32_t* __restrict__ rows, int d,
+                                      float* __restrict__ g) {
+    const int u = blockIdx.x;
+    const int a = start[u], b = start[u + 1];
+    float* dst = g + static_cast<size_t>(uniq[u]) * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float s = 0.f;
+        for (int k = a; k < b; ++k) s += dx[static_cast<size_t>(rows[k]) * d + c];
+        dst[c] += s;
+    }
 }
 
 // response rows <-> training rows: map[k] = training row of response token k

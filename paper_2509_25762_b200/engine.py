@@ -172,12 +172,16 @@ class Engine:
                                       C.byref(n)))
         return buf
 
-    def export_weights(self, model):
-        """fp32 copies of every tensor of one model (0 actor .. 3 ref), for the oracle."""
+    def export_weights(self, model, masters=False):
+        """fp32 copies of every tensor of one model (0 actor .. 3 ref), for the
+        oracle; masters=True: the fp32 masters of the matrices the
+        full-parameter update trains (where they exist)."""
         d = [self.cfg.actor, self.cfg.reward, self.cfg.critic, self.cfg.ref][model]
-        w = {k: self.get_tensor(model, k) for k in ("embed", "lm_head", "final_norm", "head")}
+        mat = ("embed", "lm_head", "wqkv", "wo", "wgu", "wdown")
+        nm = lambda k: k + ":master" if masters and k in mat else k
+        w = {k: self.get_tensor(model, nm(k)) for k in ("embed", "lm_head", "final_norm", "head")}
         for k in ("ln1", "wqkv", "bqkv", "wo", "ln2", "wgu", "wdown"):
-            w[k] = [self.get_tensor(model, k, l) for l in range(d.n_layers)]
+            w[k] = [self.get_tensor(model, nm(k), l) for l in range(d.n_layers)]
         dd = {f: getattr(d, f) for f, _ in abi.ModelDims._fields_}
         return dd, w
 

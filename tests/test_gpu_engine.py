@@ -353,7 +353,8 @@ def test_policy_logprob_precompute_is_bit_identical():
     assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
-def test_engine_checkpoint_resume_is_bit_identical(tmp_path):
+@pytest.mark.parametrize("train", [1, 2])
+def test_engine_checkpoint_resume_is_bit_identical(tmp_path, train):
     """oppo_engine_save after a step with carried sequences (token carry: KV
     pages, partial tokens and log-probs of the stragglers, trained heads),
     oppo_engine_load into a fresh engine of the same configuration: the next
@@ -368,7 +369,7 @@ def test_engine_checkpoint_resume_is_bit_identical(tmp_path):
 
     def make(**kw):
         return Engine(shape, dtype=abi.DTYPE_BF16, max_slots=16, max_prompt_len=P, max_response_len=64,
-                      sample_seed=SAMPLE_SEED, train_heads=1, carry=abi.CARRY_TOKEN, **kw)
+                      sample_seed=SAMPLE_SEED, train_heads=train, carry=abi.CARRY_TOKEN, **kw)
 
     def fresh(ids, lens):
         return [S.seq_array([dict(id=i, prompt_len=P, target_len=L)])[0] for i, L in zip(ids, lens)]
@@ -398,8 +399,11 @@ def test_engine_checkpoint_resume_is_bit_identical(tmp_path):
         eng.admit(more)
         ents, ids, stats, ro = step(eng, [S.seq_array([e])[0] for e in entries] + more)
         res.append((ids, stats, ro, eng.get_tensor(0, "lm_head"), eng.get_tensor(2, "head"),
-                    [(e.id, e.generated, e.prefilled_tokens) for e in ents]))
-    (ia, sa, ra, la, ha, ea), (ib, sb, rb, lb, hb, eb) = res
+                    [(e.id, e.generated, e.prefilled_tokens) for e in ents],
+                    [eng.get_tensor(m, k, 1) for m in (0, 2) for k in ("wqkv:master", "wdown", "ln2")]))
+    (ia, sa, ra, la, ha, ea, ta), (ib, sb, rb, lb, hb, eb, tb) = res
+    for x, y in zip(ta, tb):  # trunk tensors (full-parameter update) and their masters
+        assert np.array_equal(x, y)
     assert ia == ib and sa == sb and ea == eb
     for x, y in zip(ra, rb):
         assert x["reward"] == y["reward"]
@@ -409,7 +413,7 @@ def test_engine_checkpoint_resume_is_bit_identical(tmp_path):
     a.close()
     b.close()
     c = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=64,
-               sample_seed=SAMPLE_SEED, train_heads=1, carry=abi.CARRY_TOKEN)
+               sample_seed=SAMPLE_SEED, train_heads=train, carry=abi.CARRY_TOKEN)
     with pytest.raises(Exception, match="configuration"):
         c.load(ck)
     c.close()

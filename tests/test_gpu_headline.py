@@ -75,7 +75,7 @@ def run_cfg2(steps=STEPS, scorer_sms=64, env=None, keep=None, weights=False):
         eng = Engine(wl["actor"], wl["scorer"], wl["scorer"], wl["scorer"], dtype=abi.DTYPE_BF16,
                      max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
                      max_response_len=wl["cap"], page_size=64, carry=cfg.carry_granularity,
-                     train_heads=1, sample_seed=SAMPLE_SEED, weight_seed=1, scorer_sms=scorer_sms)
+                     train_heads=2, sample_seed=SAMPLE_SEED, weight_seed=1, scorer_sms=scorer_sms)
     finally:
         for k, v in old.items():
             if v is None:

@@ -159,3 +159,56 @@ def test_full_update_every_tensor_vs_oracle_fp32():
     assert abs(stats.ppo_objective - obj) < 1e-4
     assert abs(stats.value_loss - vloss) <= 1e-4 * max(1.0, vloss)
     eng.close()
+
+
+W05 = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864, vocab=151936, tied=1)
+W15 = dict(n_layers=2, d_model=1536, n_heads=12, n_kv_heads=2, head_dim=128, d_ff=8960, vocab=151936, tied=1)
+
+
+@pytest.mark.parametrize("shape", [W05, W15], ids=["0.5b-width", "1.5b-width"])
+@pytest.mark.parametrize("simt", [0, 1], ids=["mma-attn", "simt-attn"])
+def test_full_update_bf16_vs_oracle(shape, simt, monkeypatch):
+    """bf16 engine (tcgen05 GEMMs, tensor-core or SIMT training attention,
+    fp32 masters) at the 0.5B / 1.5B layer geometry (head_dim 64 / 128) and
+    vocabulary (2 layers): every tensor's update agrees with the fp64 oracle
+    gradient in direction (cosine >= 0.99) and size (max error <= 10% of the
+    tensor's largest change; bf16 operands carry ~3 significant digits)."""
+    if simt:
+        monkeypatch.setenv("OPPO_TRAIN_SIMT_ATTN", "1")
+    P, C = 16, 16
+    lens = [40, 64, 23, 100]
+    eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=128,
+                 sample_seed=SAMPLE_SEED, train_heads=2)
+    st = [dict(id=i, prompt_len=P, target_len=L) for i, L in enumerate(lens)]
+    eng.admit(st)
+    eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+    dims_a, wa0 = snapshot(eng, 0)
+    dims_c, wc0 = snapshot(eng, 2)
+    hp = abi.PpoHparams(gamma=1.0, lambda_=0.95, clip_epsilon=0.2, learning_rate=0.5,
+                        value_learning_rate=0.05, kl_coef=0.05, whiten=1, value_target=abi.VALUE_MC_RETURN)
+    ids = [s["id"] for s in st]
+    da, dc, obj, vloss = oracle_update(eng, ids, P, hp, wa0, wc0, dims_a, dims_c)
+    eng.ppo_update(ids, hp)
+    # masters hold the un-rounded update: compare the fp32 masters' change
+    ma1 = eng_masters(eng, 0)
+    mc1 = eng_masters(eng, 2)
+    for who, m1, w0, dd in (("actor", ma1, wa0, da), ("critic", mc1, wc0, dc)):
+        for k in NAMES:
+            if k not in dd:
+                continue
+            o_list = dd[k] if isinstance(dd[k], list) else [dd[k]]
+            w_list = w0[k] if isinstance(w0[k], list) else [w0[k]]
+            m_list = m1[k] if isinstance(m1[k], list) else [m1[k]]
+            for li, (o, w, m) in enumerate(zip(o_list, w_list, m_list)):
+                e = (np.asarray(m) - np.asarray(w)).reshape(-1)
+                o = np.asarray(o).reshape(-1)
+                cos = float(e @ o / (np.linalg.norm(e) * np.linalg.norm(o) + 1e-30))
+                err = float(np.abs(e - o).max() / max(np.abs(o).max(), 1e-30))
+                assert cos >= 0.99 and err <= 0.10, (who, k, li, cos, err)
+    eng.close()
+
+
+def eng_masters(eng, model):
+    """fp32 masters (matrices) / fp32 parameters (vectors) after the update."""
+    d, w = eng.export_weights(model, masters=True)
+    return w
