@@ -95,7 +95,7 @@ struct TrainState {
     Scratch scr;
     int rows_cap = 0;  // training rows the scratch is sized for
     // per-layer saved activations
-    std::vector<float*> x_in, x_mid, lse;
+    std::vector<float*> x_in, x_mid, lse, rstd1, rstd2;
     std::vector<void*> qkv, o, gu;
     // transients
     float *x = nullptr, *dx = nullptr, *dh = nullptr, *dff = nullptr, *dqkv = nullptr, *dvec = nullptr,
@@ -212,6 +212,17 @@ void rmsnorm(Engine& e, float* x, const float* g, T* out, int rows, int D, cudaS
                                                    nullptr, 0, 0, -1, nullptr, 0, size_t(0));
 }
 
+const dim3 kTile(32, 8);
+template <class T>
+void cvt_t(const float* x, int rows, int cols, int ldT, void* y, void* yT, cudaStream_t st) {
+    train::cvt_t<T><<<dim3(cdiv(cols, 32), cdiv(ldT, 32)), kTile, 0, st>>>(x, rows, cols, ldT, static_cast<T*>(y),
+                                                                          static_cast<T*>(yT));
+}
+template <class T>
+void norm_t(const float* x, const float* rstd, const float* g, int rows, int d, int ldT, void* hT, cudaStream_t st) {
+    train::norm_t<T><<<dim3(cdiv(d, 32), cdiv(ldT, 32)), kTile, 0, st>>>(x, rstd, g, rows, d, ldT, static_cast<T*>(hT));
+}
+
 template <class T>
 void cvt_f32(const float* in, T* out, int64_t n, cudaStream_t st) {
     convert<float, T><<<cdiv(n, 256), 256, 0, st>>>(in, out, n);
@@ -306,6 +317,8 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
     ts.x_in.assign(L, nullptr);
     ts.x_mid.assign(L, nullptr);
     ts.lse.assign(L, nullptr);
+    ts.rstd1.assign(L, nullptr);
+    ts.rstd2.assign(L, nullptr);
     ts.qkv.assign(L, nullptr);
     ts.o.assign(L, nullptr);
     ts.gu.assign(L, nullptr);
@@ -314,6 +327,8 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
         ts.x_in[l] = static_cast<float*>(ts.scr.take(R * D * 4));
         ts.x_mid[l] = static_cast<float*>(ts.scr.take(R * D * 4));
         ts.lse[l] = static_cast<float*>(ts.scr.take(R * H * 4));
+        ts.rstd1[l] = static_cast<float*>(ts.scr.take(R * 4));
+        ts.rstd2[l] = static_cast<float*>(ts.scr.take(R * 4));
         ts.qkv[l] = ts.scr.take(R * qkv * es);
         ts.o[l] = ts.scr.take(R * qw * es);
         ts.gu[l] = ts.scr.take(R * 2 * F * es);
@@ -453,16 +468,16 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             T* o = static_cast<T*>(ts.o[l]);
             T* gu = static_cast<T*>(ts.gu[l]);
             OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_in[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
-            rmsnorm<T>(e, x, Lw.ln1, h, Tr, D, st);
+            train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln1, Tr, D, kEps, h, ts.rstd1[l]);
             mm(e, st, h, Tr, D, Lw.wqkv, qkvw, epi(EPI_STORE, qkv, qkvw, 1.f, Lw.bqkv));
             train::rope_rows<T><<<Tr, 128, 0, st>>>(qkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 0);
             attn<T>(hd, 0, d_blk, nb, qkv, qkvw, H, KV, o, ts.lse[l], nullptr, nullptr, nullptr, st);
             mm(e, st, o, Tr, qw, Lw.wo, D, epi(EPI_ADD_F32, x, D));
             OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_mid[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
-            rmsnorm<T>(e, x, Lw.ln2, h, Tr, D, st);
+            train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln2, Tr, D, kEps, h, ts.rstd2[l]);
             mm(e, st, h, Tr, D, Lw.wgu, 2 * F, epi(EPI_STORE, gu, 2 * F));
-            train::swiglu_fwd<T><<<cdiv(static_cast<int64_t>(Tr) * F, 256), 256, 0, st>>>(gu, static_cast<T*>(ts.ff),
-                                                                                          static_cast<int64_t>(Tr) * F);
+            train::swiglu_fwd4<T><<<cdiv(static_cast<int64_t>(Tr) * F / 4, 256), 256, 0, st>>>(
+                gu, static_cast<T*>(ts.ff), static_cast<int64_t>(Tr) * F);
             mm(e, st, ts.ff, Tr, F, Lw.wdown, D, epi(EPI_ADD_F32, x, D));
         }
         T* hf = static_cast<T*>(ts.hf);
@@ -535,26 +550,20 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             T* qkv = static_cast<T*>(ts.qkv[l]);
             T* o = static_cast<T*>(ts.o[l]);
             T* gu = static_cast<T*>(ts.gu[l]);
-            T* ff = static_cast<T*>(ts.ff);
             // down projection + SwiGLU
-            train::swiglu_fwd<T><<<cdiv(static_cast<int64_t>(Tr) * F, 256), 256, 0, st>>>(gu, ff, static_cast<int64_t>(Tr) * F);
-            cvt_f32<T>(dx, dxc, static_cast<int64_t>(Tr) * D, st);
-            transpose<T>(dx, Tr, D, Tp, ts.dxT, st, true);
-            transpose<T>(ff, Tr, F, Tp, ts.bT, st);
+            cvt_t<T>(dx, Tr, D, Tp, dxc, ts.dxT, st);
+            train::swiglu_t<T><<<dim3(cdiv(F, 32), cdiv(Tp, 32)), kTile, 0, st>>>(gu, Tr, F, Tp, static_cast<T*>(ts.bT));
             mm(e, st, ts.dxT, D, Tp, ts.bT, F, epi(EPI_ADD_F32, Lt.wdown.grad, F));
             mm(e, st, dxc, Tr, D, Lt.wdown.wT, F, epi(EPI_STORE_F32, ts.dff, F));
-            train::swiglu_bwd<T><<<cdiv(static_cast<int64_t>(Tr) * F, 256), 256, 0, st>>>(
-                gu, ts.dff, static_cast<T*>(ts.dgu), static_cast<int64_t>(Tr) * F);
-            transpose<T>(ts.dgu, Tr, 2 * F, Tp, ts.aT, st);
-            rmsnorm<T>(e, ts.x_mid[l], Lw.ln2, h, Tr, D, st);
-            transpose<T>(h, Tr, D, Tp, ts.bT, st);
+            train::swiglu_bwd_t<T><<<dim3(cdiv(F, 32), cdiv(Tp, 32)), kTile, 0, st>>>(
+                gu, ts.dff, Tr, F, Tp, static_cast<T*>(ts.dgu), static_cast<T*>(ts.aT));
+            norm_t<T>(ts.x_mid[l], ts.rstd2[l], Lw.ln2, Tr, D, Tp, ts.bT, st);
             mm(e, st, ts.aT, 2 * F, Tp, ts.bT, D, epi(EPI_ADD_F32, Lt.wgu.grad, D));
             mm(e, st, ts.dgu, Tr, 2 * F, Lt.wgu.wT, D, epi(EPI_STORE_F32, ts.dh, D));
             train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_mid[l], Lw.ln2, ts.dh, Tr, D, kEps, dx, ts.gscr);
             colsum_into(ts, ts.gscr, Tr, D, Lt.ln2.grad, st);
             // O projection + attention
-            cvt_f32<T>(dx, dxc, static_cast<int64_t>(Tr) * D, st);
-            transpose<T>(dx, Tr, D, Tp, ts.dxT, st, true);
+            cvt_t<T>(dx, Tr, D, Tp, dxc, ts.dxT, st);
             transpose<T>(o, Tr, qw, Tp, ts.bT, st);
             mm(e, st, ts.dxT, D, Tp, ts.bT, qw, epi(EPI_ADD_F32, Lt.wo.grad, qw));
             T* dO = static_cast<T*>(ts.dO);
@@ -565,10 +574,8 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             train::rope_rows<float><<<Tr, 128, 0, st>>>(ts.dqkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 1);
             colsum_into(ts, ts.dqkv, Tr, qkvw, Lt.bqkv.grad, st);
             T* dqc = static_cast<T*>(ts.dqkvc);
-            cvt_f32<T>(ts.dqkv, dqc, static_cast<int64_t>(Tr) * qkvw, st);
-            transpose<T>(ts.dqkv, Tr, qkvw, Tp, ts.aT, st, true);
-            rmsnorm<T>(e, ts.x_in[l], Lw.ln1, h, Tr, D, st);
-            transpose<T>(h, Tr, D, Tp, ts.bT, st);
+            cvt_t<T>(ts.dqkv, Tr, qkvw, Tp, dqc, ts.aT, st);
+            norm_t<T>(ts.x_in[l], ts.rstd1[l], Lw.ln1, Tr, D, Tp, ts.bT, st);
             mm(e, st, ts.aT, qkvw, Tp, ts.bT, D, epi(EPI_ADD_F32, Lt.wqkv.grad, D));
             mm(e, st, dqc, Tr, qkvw, Lt.wqkv.wT, D, epi(EPI_STORE_F32, ts.dh, D));
             train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_in[l], Lw.ln1, ts.dh, Tr, D, kEps, dx, ts.gscr);

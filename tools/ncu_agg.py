@@ -4,7 +4,7 @@ import sys
 from collections import defaultdict
 
 
-def main(path, top=40):
+def main(path, top=40, by_grid=False):
     rows = list(csv.reader(open(path)))
     hdr = None
     agg = defaultdict(lambda: [0, 0.0])
@@ -18,6 +18,8 @@ def main(path, top=40):
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
         name = d["Kernel Name"].split("(")[0][:90]
+        if by_grid and "gemm" in name:
+            name += " grid" + d.get("Grid Size", "?")
         v = float(d["Metric Value"].replace(",", ""))
         unit = d.get("Metric Unit", "nsecond")
         us = v / 1e3 if unit.startswith("n") else (v if unit.startswith("u") else v * 1e3)
@@ -30,4 +32,4 @@ def main(path, top=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40, len(sys.argv) > 3)
