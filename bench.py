@@ -106,46 +106,61 @@ def host_prompts(ids, P, V, seed):
 
 
 def run_arm(eng, wl, cfg, seed, steps, warmup, rank, world, dist):
-    """The data-parallel step loop (paper_2509_25762_b200.dp.run_rank, i.e.
-    driver.cpp:103-195 per rank) through the C ABI: host prompts copied in at
-    admission, step results read back every step.  Returns the timed steps."""
-    from paper_2509_25762_b200 import dp
+    """The step loop in the engine's C++ host (oppo_run_seed_ex = driver.cpp:
+    103-195 per rank, data parallel when world > 1): host prompts copied in
+    at admission through the prompt-source hook, each step's record and
+    ledger read back.  The per-step hook puts the warm-up boundary (device
+    synchronize + barrier) before the timed steps.  Returns the timed steps."""
     import torch
 
     V = eng.cfg.actor.vocab
     P = cfg.prompt_len
-    ex = dp.GpuExecutor(eng, prompt_fn=lambda ids: host_prompts(ids, P, V, 1234))
-    marks = {}
+    marks = {"prompts": [0] * (warmup + steps + 1)}
+    state = {"step": 0}
+
+    def prompt_fn(sid, plen):
+        marks["prompts"][state["step"]] += plen * 4
+        return host_prompts([sid], plen, V, 1234)[0]
 
     def on_step(rec):
-        if rec["step"] == warmup - 1 or (warmup == 0 and rec["step"] == 0 and "t0" not in marks):
-            if warmup > 0:
-                if dist:
-                    dist.barrier()
-                torch.cuda.synchronize()
+        state["step"] = rec.step + 1
+        if rec.step == warmup - 1:
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
             marks["t0"] = time.perf_counter()
+        return False
 
     if warmup == 0:
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
         marks["t0"] = time.perf_counter()
-    recs = dp.run_rank(cfg, seed, rank, world, ex, steps=warmup + steps, on_step=on_step)
+    run_cfg = abi_copy(cfg)
+    run_cfg.steps = warmup + steps
+    recs, sel, leds = eng.run_seed_ex(run_cfg, seed, prompt_fn=prompt_fn, on_step=on_step)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     wall = time.perf_counter() - marks["t0"]
+    if len(recs) != warmup + steps:
+        raise RuntimeError(f"step loop ended after {len(recs)} steps")
+    from paper_2509_25762_b200 import abi
     out = []
-    for r in recs[warmup:]:
-        led, st = r["ledger"], r["stats"] or abi_stats()
-        out.append(dict(samples=len(r["ids"]), step_us=led.step_us, update_us=st.update_us,
-                        wall_s=r["wall_s"], loop_us=led.decode_loop_us,
-                        loop_bytes=led.decode_weight_bytes + led.decode_kv_bytes,
-                        decode_us=led.decode_us, score_us=led.score_us, iters=led.decode_iters,
-                        decode_tokens=led.decode_tokens, prefill_tokens=led.prefill_tokens,
-                        launches=led.kernel_launches, h2d=r["h2d"], d2h=r["d2h"] + int(st.n_tokens) * 4,
-                        tokens=int(st.n_tokens), reward=r["mean_reward"], obj=st.ppo_objective))
+    for r, led in list(zip(recs, leds))[warmup:]:
+        out.append(dict(samples=r.finished, step_us=led.step_us, update_us=r.update_us, loop_us=led.decode_loop_us,
+                        loop_bytes=led.decode_weight_bytes + led.decode_kv_bytes, decode_us=led.decode_us,
+                        score_us=led.score_us, iters=led.decode_iters, decode_tokens=led.decode_tokens,
+                        prefill_tokens=led.prefill_tokens, launches=led.kernel_launches,
+                        h2d=marks["prompts"][r.step] + r.finished * C.sizeof(abi.SeqState),
+                        d2h=C.sizeof(abi.StepRecord) + C.sizeof(abi.Ledger) + int(r.batch_tokens) * 4 + r.finished * 4,
+                        tokens=int(r.batch_tokens), reward=r.mean_reward, obj=r.ppo_loss))
     return out, wall
+
+
+def abi_copy(cfg):
+    from paper_2509_25762_b200 import abi
+    return abi.RunConfig.from_buffer_copy(cfg)
 
 
 def abi_stats():
@@ -457,7 +472,7 @@ def reference(args):
             tot += time.perf_counter() - t
         v = fin / tot
         line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "samples/s",
-                "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps,
+                "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference toy policy)",
@@ -470,6 +485,46 @@ def reference(args):
     except Exception as ex:
         line = {"impl": "reference", "unavailable": str(ex)[:200]}
     print(json.dumps(line), flush=True)
+
+
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: one process per GPU, launched here
+    with the torchrun environment (RANK / LOCAL_RANK / WORLD_SIZE /
+    MASTER_ADDR=127.0.0.1 / MASTER_PORT); rank 0's stdout is the JSON line."""
+    port = free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    codes = [p.wait() for p in procs]
+    return max(codes, key=abs)
+
+
+def dry_run_ranks(args):
+    """--dry-run-ranks: the launch plumbing without a GPU: every rank joins a
+    gloo group from the environment and rank 0 prints what it saw."""
+    import torch
+    import torch.distributed as td
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    t = torch.tensor([rank, int(os.environ.get("LOCAL_RANK", -1))], dtype=torch.int64)
+    got = [torch.zeros_like(t) for _ in range(world)]
+    td.all_gather(got, t)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "ranks": [g.tolist() for g in got],
+                          "global_batch": WORKLOADS[args.workload]["batch"] * world}), flush=True)
+    td.destroy_process_group()
 
 
 def main():
@@ -485,7 +540,13 @@ def main():
                     help="fixed SM partition for the scorer stream in the overlapped arm (0: shared)")
     ap.add_argument("--config", default=None,
                     help="reference-schema JSON run config (+ model/gpu blocks) instead of --workload")
+    ap.add_argument("--dry-run-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(spawn_ranks(args.gpus))
+    if args.dry_run_ranks:
+        dry_run_ranks(args)
+        return
     if args.config:
         wl = workload_from_config(args.config)
         WORKLOADS["config"] = wl

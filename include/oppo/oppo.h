@@ -213,6 +213,10 @@ typedef struct oppo_step_record {
     int64_t batch_tokens;
 } oppo_step_record;
 
+/* Per-step callback of the step loop (run after selection, update and the
+ * controller step of each step); a non-zero return ends the loop. */
+typedef int32_t (*oppo_step_fn)(void* ctx, const oppo_step_record* rec);
+
 /* ------------------------------------------------ host scheduler (no GPU) */
 
 /* Defaults identical to RunConfig{} (config.hpp:28-77). */
@@ -267,6 +271,16 @@ int32_t oppo_abi_sizes(int64_t* out, int32_t cap);
 /* Scheduler-only run of the step loop (driver.cpp:103-195) with the logical
  * executor; no GPU.  Records one oppo_step_record per step and, if sel_ids is
  * non-NULL, the selected ids of each step (batch_size slots per step, -1 pad). */
+/* The logical loop as rank `rank` of `world` (CPU; the data-parallel
+ * decisions without a GPU): sums go through `allreduce` (in place, n doubles),
+ * and in simulate mode the controller's reward is batch_reward(selected ids)
+ * when given (else the reference's proxy). */
+typedef int32_t (*oppo_host_allreduce_fn)(void* ctx, double* v, int32_t n);
+typedef double (*oppo_batch_reward_fn)(void* ctx, const int64_t* ids, int32_t n);
+oppo_status oppo_run_seed_logical_dp(const oppo_run_config* cfg, uint64_t seed, int32_t rank, int32_t world,
+                                     oppo_host_allreduce_fn allreduce, void* allreduce_ctx,
+                                     oppo_batch_reward_fn batch_reward, void* reward_ctx,
+                                     oppo_step_record* records, int32_t* n_records, int64_t* sel_ids);
 oppo_status oppo_run_seed_logical(const oppo_run_config* cfg, uint64_t seed,
                                   oppo_step_record* records, int32_t* n_records,
                                   int64_t* sel_ids);
@@ -382,6 +396,26 @@ oppo_status oppo_read_rollout(oppo_engine* e, int64_t id, int32_t* tokens, float
  * replaced by oppo_run_step and fill_values/toy_rlhf_step by oppo_ppo_update. */
 oppo_status oppo_run_seed(oppo_engine* e, const oppo_run_config* cfg, uint64_t seed,
                           oppo_step_record* records, int32_t* n_records, int64_t* sel_ids);
+
+/* The reference's PromptSource seam (overcommit.hpp:16-20): prompt tokens of
+ * sequence `id` (prompt_len of them) into tokens_out; non-zero = failure. */
+typedef int32_t (*oppo_prompt_fn)(void* ctx, int64_t id, int32_t prompt_len, int32_t* tokens_out);
+typedef struct oppo_loop_hooks {
+    oppo_prompt_fn prompt;  /* NULL: synthetic prompt stream keyed by (sample_seed, id) */
+    void* prompt_ctx;
+    oppo_step_fn on_step;   /* NULL: none */
+    void* step_ctx;
+    oppo_ledger* ledgers;   /* NULL or [cfg->steps]: each step's ledger */
+} oppo_loop_hooks;
+/* run_seed with host hooks.  Data parallel when the engine was created with
+ * world > 1: rank r serves prompt ids = r (mod world), draws its
+ * lengths from Rng::derive(seed ^ r, "lengths"), the Delta controller is fed
+ * the global mean reward and the tuner the max step time over the ranks.
+ * Refill defers a sequence while the engine lacks a slot or KV pages for it
+ * (admission control; the reference's refill never defers). */
+oppo_status oppo_run_seed_ex(oppo_engine* e, const oppo_run_config* cfg, uint64_t seed,
+                             const oppo_loop_hooks* hooks, oppo_step_record* records, int32_t* n_records,
+                             int64_t* sel_ids);
 
 /* Data-parallel plumbing: one NCCL communicator over the GPUs of
  * the box; pass it as oppo_engine_cfg.nccl_comm with rank/world.  The engine

@@ -105,6 +105,8 @@ def _declare(L):
         "oppo_abi_sizes": (i32, [P(i64), i32]),
         "oppo_run_seed_logical": (i32, [P(abi.RunConfig), u64, P(abi.StepRecord), P(i32),
                                         P(i64)]),
+        "oppo_run_seed_logical_dp": (i32, [P(abi.RunConfig), u64, i32, i32, vp, vp, vp, vp,
+                                           P(abi.StepRecord), P(i32), P(i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -124,6 +126,8 @@ def _declare(L):
                                     P(C.c_float), P(C.c_float), i32, P(i32)]),
         "oppo_run_seed": (i32, [vp, P(abi.RunConfig), u64, P(abi.StepRecord), P(i32),
                                 P(i64)]),
+        "oppo_run_seed_ex": (i32, [vp, P(abi.RunConfig), u64, P(abi.LoopHooks), P(abi.StepRecord),
+                                   P(i32), P(i64)]),
         "oppo_k_ppo_token": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, dbl, dbl, dbl, i32, vp,
                                    vp, vp, vp, vp]),
         "oppo_k_gemm": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, vp]),

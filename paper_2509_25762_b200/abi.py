@@ -134,3 +134,15 @@ def struct_sizes():
         ("ledger", Ledger), ("latency", Latency), ("length_dist", LengthDist),
         ("ppo_hparams", PpoHparams), ("run_config", RunConfig), ("step_record", StepRecord),
         ("model_dims", ModelDims), ("engine_cfg", EngineCfg), ("ppo_stats", PpoStats)]}
+
+
+# host callbacks of the step loop (include/oppo/oppo.h)
+PROMPT_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32))
+STEP_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(StepRecord))
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32)
+BATCH_REWARD_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.POINTER(C.c_int64), C.c_int32)
+
+
+class LoopHooks(C.Structure):
+    _fields_ = [("prompt", C.c_void_p), ("prompt_ctx", C.c_void_p), ("on_step", C.c_void_p),
+                ("step_ctx", C.c_void_p), ("ledgers", C.POINTER(Ledger))]

@@ -1969,7 +1969,10 @@ void ppo_update_impl(Engine& e, const std::vector<int>& slots, const oppo_ppo_hp
     // call: whitening uses the global moments, the token mean of the
     // objective / gradients the global token count, and every rank's Delta
     // controller the global mean reward.
-    const bool dp = e.cfg.world > 1 && (e.nccl != nullptr || e.cfg.allreduce != nullptr);
+    // data-parallel collectives: world > 1, or a communicator given explicitly
+    // (world 1 with NCCL runs every collective on one GPU: the hardware check
+    // of the NCCL call sites, tests/test_gpu_dp.py)
+    const bool dp = (e.cfg.world > 1 && e.cfg.allreduce != nullptr) || e.nccl != nullptr;
     const int mb = std::min(1024, std::max(1, cdiv(N, 256)));
     double* stats = nullptr;
     double n_glob = N, score_glob = 0, samples_glob = n;
@@ -2354,11 +2357,52 @@ void release_slot(Engine& e, int64_t id) {
 struct EngineHooks final : LoopHooks {
     Engine& e;
     oppo_ppo_hparams hp;
+    oppo_prompt_fn prompt = nullptr;
+    void* prompt_ctx = nullptr;
+    int reserved_slots = 0, reserved_pages = 0;
     explicit EngineHooks(Engine& en, const oppo_ppo_hparams& h) : e(en), hp(h) {}
     void admit(const std::vector<oppo_seq_state>& fresh) override {
         if (fresh.empty()) return;
-        if (e.dtype == OPPO_DTYPE_F32) admit_impl<float>(e, fresh.data(), static_cast<int>(fresh.size()), nullptr);
-        else admit_impl<__nv_bfloat16>(e, fresh.data(), static_cast<int>(fresh.size()), nullptr);
+        std::vector<int32_t> tok;
+        if (prompt) {  // the caller's prompt source (PromptSource::next, overcommit.hpp:16-20)
+            for (const auto& s : fresh) {
+                const size_t o = tok.size();
+                tok.resize(o + s.prompt_len);
+                if (prompt(prompt_ctx, s.id, s.prompt_len, tok.data() + o) != 0)
+                    input_error("prompt source failed for sequence " + std::to_string(s.id));
+            }
+        }
+        const int32_t* p = prompt ? tok.data() : nullptr;
+        if (e.dtype == OPPO_DTYPE_F32) admit_impl<float>(e, fresh.data(), static_cast<int>(fresh.size()), p);
+        else admit_impl<__nv_bfloat16>(e, fresh.data(), static_cast<int>(fresh.size()), p);
+    }
+    int rank() const override { return e.cfg.world > 1 ? e.cfg.rank : 0; }
+    int world() const override { return std::max(1, e.cfg.world); }
+    bool dp() const { return e.cfg.world > 1 && (e.nccl != nullptr || e.cfg.allreduce != nullptr); }
+    // oppo_ppo_update allreduces the reward statistics itself when data parallel
+    bool reward_is_global() const override { return e.cfg.world <= 1 || dp(); }
+    void allreduce_sum(double* v, int n) override {
+        if (e.cfg.world <= 1) return;
+        if (!dp()) config_error("world > 1 without a communicator (nccl_comm or allreduce hook)");
+        double* d = nullptr;
+        OPPO_CUDA_CHECK(cudaMalloc(&d, n * sizeof(double)));
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(d, v, n * sizeof(double), cudaMemcpyHostToDevice, e.su));
+        dp_allreduce(e, d, n, true, e.su);
+        OPPO_CUDA_CHECK(cudaMemcpyAsync(v, d, n * sizeof(double), cudaMemcpyDeviceToHost, e.su));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(e.su));
+        cudaFree(d);
+    }
+    // KV admission control: a sequence is admitted only with a free slot and
+    // KV pages for prompt + target length (else refill defers it)
+    void begin_refill() override { reserved_slots = reserved_pages = 0; }
+    bool fits(const oppo_seq_state& s) override {
+        const int need = cdiv(s.prompt_len + s.target_len + 1, e.page_size);
+        if (reserved_slots + 1 > static_cast<int>(e.free_slots.size()) ||
+            reserved_pages + need > static_cast<int>(e.free_pages.size()))
+            return false;
+        ++reserved_slots;
+        reserved_pages += need;
+        return true;
     }
     void execute(const std::vector<oppo_seq_state>& active, int chunk, int mode, int stop,
                  std::vector<oppo_seq_outcome>& out, oppo_ledger& ledger) override {
@@ -2569,13 +2613,27 @@ oppo_status oppo_get_tensor(oppo_engine* eh, int32_t model, const char* name, in
 
 oppo_status oppo_run_seed(oppo_engine* eh, const oppo_run_config* cfg, uint64_t seed,
                           oppo_step_record* records, int32_t* n_records, int64_t* sel_ids) {
+    return oppo_run_seed_ex(eh, cfg, seed, nullptr, records, n_records, sel_ids);
+}
+
+oppo_status oppo_run_seed_ex(oppo_engine* eh, const oppo_run_config* cfg, uint64_t seed,
+                             const oppo_loop_hooks* lh, oppo_step_record* records, int32_t* n_records,
+                             int64_t* sel_ids) {
     Engine* e = reinterpret_cast<Engine*>(eh);
     std::string err;
     const oppo_status st = oppo::eguard(e, [&] {
         oppo::EngineHooks hooks(*e, cfg->ppo);
         if (cfg->carry_granularity != e->cfg.carry_granularity)
             oppo::config_error("run config and engine disagree on carry_granularity");
-        *n_records = oppo::run_seed_loop(*cfg, seed, hooks, records, sel_ids, &err);
+        oppo::LoopExtras ex;
+        if (lh) {
+            hooks.prompt = lh->prompt;
+            hooks.prompt_ctx = lh->prompt_ctx;
+            ex.on_step = lh->on_step;
+            ex.step_ctx = lh->step_ctx;
+            ex.ledgers = lh->ledgers;
+        }
+        *n_records = oppo::run_seed_loop(*cfg, seed, hooks, records, sel_ids, &err, ex);
         // sequences still buffered at the end keep their slots; free them
         std::vector<int64_t> left;
         for (auto& kv : e->slot_of) left.push_back(kv.first);

@@ -36,7 +36,29 @@ struct LogicalHooks final : oppo::LoopHooks {
         return 0.0;
     }
     void release(const std::vector<oppo_seq_state>&) override {}
+    int rank() const override { return rank_; }
+    int world() const override { return world_; }
+    void allreduce_sum(double* v, int n) override {
+        if (world_ <= 1) return;
+        if (!ar || ar(ar_ctx, v, n) != 0) oppo::internal_error("host allreduce failed");
+    }
+    double sim_reward(const oppo_run_config& cfg, int step, const std::vector<oppo_seq_state>& batch,
+                      bool& is_local) override {
+        if (!rw) {
+            is_local = false;
+            return oppo::proxy_reward(cfg, step);
+        }
+        std::vector<int64_t> ids;
+        for (const auto& s : batch) ids.push_back(s.id);
+        is_local = true;
+        return rw(rw_ctx, ids.data(), static_cast<int32_t>(ids.size()));
+    }
     int carry = OPPO_CARRY_CHUNK;
+    int rank_ = 0, world_ = 1;
+    oppo_host_allreduce_fn ar = nullptr;
+    void* ar_ctx = nullptr;
+    oppo_batch_reward_fn rw = nullptr;
+    void* rw_ctx = nullptr;
 };
 }  // namespace
 
@@ -154,6 +176,30 @@ oppo_status oppo_tuner_replay(const int32_t* candidates, int32_t n_cand, int32_t
             chosen[i] = t.current;
         }
     });
+}
+
+oppo_status oppo_run_seed_logical_dp(const oppo_run_config* cfg, uint64_t seed, int32_t rank, int32_t world,
+                                     oppo_host_allreduce_fn allreduce, void* allreduce_ctx,
+                                     oppo_batch_reward_fn batch_reward, void* reward_ctx,
+                                     oppo_step_record* records, int32_t* n_records, int64_t* sel_ids) {
+    std::string err;
+    const oppo_status st = guarded([&] {
+        LogicalHooks hooks;
+        hooks.carry = cfg->carry_granularity;
+        hooks.rank_ = rank;
+        hooks.world_ = world;
+        hooks.ar = allreduce;
+        hooks.ar_ctx = allreduce_ctx;
+        hooks.rw = batch_reward;
+        hooks.rw_ctx = reward_ctx;
+        *n_records = oppo::run_seed_loop(*cfg, seed, hooks, records, sel_ids, &err);
+    });
+    if (st != OPPO_OK) return st;
+    if (!err.empty()) {
+        g_error = err;
+        return OPPO_ERR_INTERNAL;
+    }
+    return OPPO_OK;
 }
 
 oppo_status oppo_run_seed_logical(const oppo_run_config* cfg, uint64_t seed,

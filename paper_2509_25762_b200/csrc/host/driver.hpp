@@ -3,6 +3,7 @@
 // GPU engine.
 #pragma once
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,16 +26,50 @@ struct LoopHooks {
                           oppo_step_record& rec) = 0;
     // selected sequences leave the buffer for good
     virtual void release(const std::vector<oppo_seq_state>& batch) = 0;
+
+    // ---- data parallelism and admission control; the defaults
+    // are the single-rank, unbounded-memory reference behaviour
+    virtual int rank() const { return 0; }
+    virtual int world() const { return 1; }
+    // in-place sum over the ranks (host doubles)
+    virtual void allreduce_sum(double* v, int n) { (void)v; (void)n; }
+    // true when update() already returns the mean reward over all ranks
+    virtual bool reward_is_global() const { return true; }
+    // simulate / tune modes: the reward fed to the controller (the reference's
+    // proxy, driver.cpp:21-32, unless a hook supplies one from the batch)
+    virtual double sim_reward(const oppo_run_config& cfg, int step, const std::vector<oppo_seq_state>& batch,
+                              bool& is_local) {
+        (void)batch;
+        is_local = false;
+        return proxy_reward(cfg, step);
+    }
+    // KV admission control: called before each refill, then once per
+    // candidate in admission order; false defers the candidate
+    virtual void begin_refill() {}
+    virtual bool fits(const oppo_seq_state& s) { (void)s; return true; }
+};
+
+// Optional per-run host callbacks of the loop (C ABI: oppo_loop_hooks).
+struct LoopExtras {
+    oppo_step_fn on_step = nullptr;
+    void* step_ctx = nullptr;
+    oppo_ledger* ledgers = nullptr;  // [cfg.steps] each step's ledger
 };
 
 // Returns the number of records; throws oppo::Error on configuration errors.
 // Runtime failures are caught like run_seed does (driver.cpp:196-199): the
 // partial log is kept and *error receives the message.
 inline int run_seed_loop(const oppo_run_config& cfg, uint64_t seed, LoopHooks& hooks,
-                         oppo_step_record* records, int64_t* sel_ids, std::string* error) {
+                         oppo_step_record* records, int64_t* sel_ids, std::string* error,
+                         const LoopExtras& extras = LoopExtras{}) {
     validate(cfg);
-    Stream lengths = Stream::derive(seed, "lengths");
+    const int rank = hooks.rank(), world = hooks.world();
+    if (world < 1 || rank < 0 || rank >= world) config_error("rank / world out of range");
+    // rank r draws its own lengths; rank 0 of 1 is the reference stream
+    Stream lengths = Stream::derive(seed ^ static_cast<uint64_t>(rank), "lengths");
     PromptStream source{cfg.prompt_len, cfg.prompt_count};
+    source.rank = rank;
+    source.world = world;
     Buffer buffer;
     buffer.batch_size = cfg.batch_size;
     buffer.delta = cfg.delta_init;
@@ -61,7 +96,9 @@ inline int run_seed_loop(const oppo_run_config& cfg, uint64_t seed, LoopHooks& h
                 throw std::runtime_error("injected failure (debug.fail_after_step)");
             buffer.delta = delta;  // capacity change takes effect at refill
             const size_t before = buffer.entries.size();
-            refill(buffer, source, step, cfg.lengths, lengths);
+            hooks.begin_refill();
+            refill_fit(buffer, source, step, cfg.lengths, lengths,
+                       [&](const oppo_seq_state& s) { return hooks.fits(s); });
             if (buffer.entries.empty()) break;  // source exhausted
             hooks.admit(std::vector<oppo_seq_state>(buffer.entries.begin() + before,
                                                     buffer.entries.end()));
@@ -88,11 +125,18 @@ inline int run_seed_loop(const oppo_run_config& cfg, uint64_t seed, LoopHooks& h
             oppo_step_record& rec = records[n];
             std::memset(&rec, 0, sizeof(rec));
             double reward = 0.0;
+            bool local = false;
             if (training) {
                 if (!sel.batch.empty()) reward = hooks.update(sel.batch, true, rec);
+                local = !hooks.reward_is_global();
             } else {
                 hooks.update(sel.batch, false, rec);
-                reward = proxy_reward(cfg, step);
+                reward = hooks.sim_reward(cfg, step, sel.batch, local);
+            }
+            if (world > 1 && local) {  // the controller sees the global mean
+                double v[2] = {reward * static_cast<double>(sel.batch.size()), static_cast<double>(sel.batch.size())};
+                hooks.allreduce_sum(v, 2);
+                reward = v[1] > 0 ? v[0] / v[1] : 0.0;
             }
             hooks.release(sel.batch);
             ctl.history.push_back(reward);
@@ -121,11 +165,20 @@ inline int run_seed_loop(const oppo_run_config& cfg, uint64_t seed, LoopHooks& h
             ++n;
             if (tuning && explored) {
                 // the tuner's measurement: the reference's tick wall (driver.cpp:187-192);
-                // on the GPU the measured step time in us replaces it
-                const double m = ledger.step_us > 0.0 ? ledger.step_us : double(ledger.wall);
+                // on the GPU the measured step time in us replaces it,
+                // the max over the ranks so every rank picks the same chunk size
+                double m = ledger.step_us > 0.0 ? ledger.step_us : double(ledger.wall);
+                if (world > 1) {
+                    std::vector<double> v(world, 0.0);
+                    v[rank] = m;
+                    hooks.allreduce_sum(v.data(), world);
+                    m = *std::max_element(v.begin(), v.end());
+                }
                 tuner.fold(*explored, m);
             }
             delta = up.delta;
+            if (extras.ledgers) extras.ledgers[n - 1] = ledger;
+            if (extras.on_step && extras.on_step(extras.step_ctx, &rec) != 0) break;
         }
     } catch (const Error& e) {
         if (e.code == OPPO_ERR_CONFIG) throw;

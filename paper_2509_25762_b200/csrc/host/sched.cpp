@@ -187,7 +187,8 @@ StepPlan plan_step(const std::vector<oppo_seq_state>& active, int chunk_size, in
 bool PromptStream::next(int step, oppo_seq_state& out) {
     if (total >= 0 && issued >= total) return false;
     out = {};
-    out.id = issued++;
+    out.id = issued * world + rank;
+    ++issued;
     out.prompt_len = prompt_len;
     out.arrival_step = step;
     return true;

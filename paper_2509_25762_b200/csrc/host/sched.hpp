@@ -84,9 +84,21 @@ struct PromptStream {  // StreamPromptSource (overcommit.hpp:23-37)
     int prompt_len;
     int64_t total;
     int64_t issued = 0;
+    // data parallel: rank r of N serves prompt ids = r (mod N)
+    int rank = 0, world = 1;
+    // KV admission control: a prompt drawn (with its length) that did not fit
+    // waits here and is admitted first at the next refill
+    bool has_pending = false;
+    oppo_seq_state pending{};
     bool next(int step, oppo_seq_state& out);
 };
 int refill(Buffer& b, PromptStream& src, int step, const oppo_length_dist& d, Stream& rng);
+// refill with admission control: a candidate (length already drawn) enters
+// only if fits(candidate) — the engine has a slot and KV pages for it; else
+// it is held in src.pending and refill stops (the reference's refill is this
+// with fits == always true, overcommit.cpp:11-28)
+template <class Fits>
+int refill_fit(Buffer& b, PromptStream& src, int step, const oppo_length_dist& d, Stream& rng, Fits&& fits);
 
 struct Selection {
     std::vector<oppo_seq_state> batch;  // earliest score-ready first
@@ -123,6 +135,35 @@ struct Tuner {
 void config_defaults(oppo_run_config& c);
 oppo_run_config config_baseline(const oppo_run_config& c);
 void validate(const oppo_run_config& c);
+int draw_length(const oppo_length_dist& d, Stream& rng);
+
+template <class Fits>
+int refill_fit(Buffer& b, PromptStream& src, int step, const oppo_length_dist& d, Stream& rng, Fits&& fits) {
+    if (b.batch_size < 1) config_error("batch size must be >= 1");
+    if (static_cast<int>(b.entries.size()) > b.capacity()) internal_error("buffer over capacity at refill");
+    int added = 0;
+    while (static_cast<int>(b.entries.size()) < b.capacity()) {
+        oppo_seq_state s;
+        if (src.has_pending) {
+            s = src.pending;
+            src.has_pending = false;
+        } else {
+            if (!src.next(step, s)) break;
+            s.target_len = draw_length(d, rng);  // length drawn at admission (overcommit.cpp:22)
+            s.admitted_at = step;
+        }
+        if (!fits(s)) {
+            if (b.entries.empty()) input_error("a single sequence needs more KV pages / slots than the engine has");
+            src.pending = s;
+            src.has_pending = true;
+            break;
+        }
+        b.entries.push_back(s);
+        ++added;
+    }
+    return added;
+}
+
 double proxy_reward(const oppo_run_config& c, int step);
 
 }  // namespace oppo

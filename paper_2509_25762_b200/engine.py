@@ -185,6 +185,39 @@ class Engine:
         dd = {f: getattr(d, f) for f, _ in abi.ModelDims._fields_}
         return dd, w
 
+    def run_seed_ex(self, cfg, seed, prompt_fn=None, on_step=None):
+        """oppo_run_seed_ex: the C++ step loop (driver.cpp:69-202) on this
+        engine.  prompt_fn(id, prompt_len) -> tokens (host prompt source);
+        on_step(record) -> truthy to stop.  Returns (records, selected ids per
+        step, ledgers)."""
+        def _pf(ctx, sid, plen, out):
+            try:
+                toks = prompt_fn(sid, plen)
+                for i in range(plen):
+                    out[i] = int(toks[i])
+                return 0
+            except Exception:
+                return 1
+
+        def _sf(ctx, rec):
+            try:
+                return 1 if on_step(rec.contents) else 0
+            except Exception:
+                return 1
+
+        pf = abi.PROMPT_FN(_pf) if prompt_fn else None
+        sf = abi.STEP_FN(_sf) if on_step else None
+        leds = (abi.Ledger * cfg.steps)()
+        hooks = abi.LoopHooks(C.cast(pf, C.c_void_p) if pf else None, None,
+                              C.cast(sf, C.c_void_p) if sf else None, None, leds)
+        recs = (abi.StepRecord * cfg.steps)()
+        sel = (C.c_int64 * (cfg.steps * cfg.batch_size))()
+        n = C.c_int32()
+        self._check(lib().oppo_run_seed_ex(self.h, C.byref(cfg), seed, C.byref(hooks), recs, C.byref(n), sel))
+        b = cfg.batch_size
+        return (list(recs[:n.value]), [list(sel[i * b:(i + 1) * b]) for i in range(n.value)],
+                list(leds[:n.value]))
+
     def run_seed(self, cfg, seed):
         recs = (abi.StepRecord * cfg.steps)()
         sel = (C.c_int64 * (cfg.steps * cfg.batch_size))()

@@ -156,3 +156,33 @@ def run_seed_logical(cfg, seed):
     check(lib().oppo_run_seed_logical(C.byref(cfg), seed, recs, C.byref(n), sel))
     b = cfg.batch_size
     return list(recs[:n.value]), [list(sel[i * b:(i + 1) * b]) for i in range(n.value)]
+
+
+def run_seed_logical_dp(cfg, seed, rank, world, allreduce_sum=None, batch_reward=None):
+    """The C++ step loop (driver.hpp) as rank `rank` of `world` on the logical
+    executor: allreduce_sum(list[float]) -> list[float] sums over the ranks;
+    batch_reward(ids) -> the selected batch's mean reward (simulate mode).
+    Returns (records, selected ids per step)."""
+    def _ar(ctx, v, n):
+        try:
+            out = allreduce_sum([v[i] for i in range(n)])
+            for i in range(n):
+                v[i] = out[i]
+            return 0
+        except Exception:
+            return 1
+
+    def _rw(ctx, ids, n):
+        return float(batch_reward([ids[i] for i in range(n)]))
+
+    ar = abi.HOST_ALLREDUCE_FN(_ar) if allreduce_sum else None
+    rw = abi.BATCH_REWARD_FN(_rw) if batch_reward else None
+    recs = (abi.StepRecord * cfg.steps)()
+    sel = (C.c_int64 * (cfg.steps * cfg.batch_size))()
+    n = C.c_int32()
+    check(lib().oppo_run_seed_logical_dp(C.byref(cfg), seed, rank, world,
+                                         C.cast(ar, C.c_void_p) if ar else None, None,
+                                         C.cast(rw, C.c_void_p) if rw else None, None,
+                                         recs, C.byref(n), sel))
+    b = cfg.batch_size
+    return list(recs[:n.value]), [list(sel[i * b:(i + 1) * b]) for i in range(n.value)]

@@ -38,3 +38,16 @@ def test_reference_default_config_matches_product_default():
     a, b = R.default_config(batch_size=256, chunk_size=64), S.default_config(batch_size=256, chunk_size=64)
     assert bytes(a) == bytes(b)
     assert bytes(R.baseline_config(a)) == bytes(S.baseline(b))
+
+
+def test_gpus_flag_spawns_one_rank_per_gpu():
+    """`bench.py --gpus N` outside torchrun launches N ranks itself with the
+    torchrun environment (127.0.0.1 rendezvous); rank 0 reports n_gpus=N and
+    global_batch=N*B."""
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "3", "--dry-run-ranks"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=300,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 3 and line["global_batch"] == 3 * 256
+    assert sorted(tuple(r) for r in line["ranks"]) == [(0, 0), (1, 1), (2, 2)]

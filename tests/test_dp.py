@@ -95,3 +95,54 @@ def test_single_rank_matches_oracle_world1():
     recs = dp.run_rank(cfg, 5, 0, 1, dp.LogicalExecutor(cfg.carry_granularity, _reward))
     oracle = dp.run_lockstep_oracle(cfg, 5, 1, _reward)
     assert [r["ids"] for r in recs] == [ids for ids, _ in oracle[0]]
+
+
+def _worker_cpp(rank, world, port, q):
+    """The same rank through the C++ step loop (driver.hpp, oppo_run_seed_logical_dp)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_25762_b200 import scheduler as S
+
+    def allreduce_sum(vals):
+        t = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.tolist()
+
+    def batch_reward(ids):
+        return sum(_reward(i) for i in ids) / len(ids) if ids else 0.0
+
+    cfg = _cfg()
+    recs, sel = S.run_seed_logical_dp(cfg, 11, rank, world, allreduce_sum, batch_reward)
+    q.put((rank, [(ids, r.delta, r.mean_reward) for ids, r in zip(sel, recs)]))
+    dist.destroy_process_group()
+
+
+def test_two_rank_cpp_loop_matches_lockstep_oracle():
+    """The production loop in C++ (rank/world, seed ^ rank lengths, prompt ids
+    = r mod N, global mean reward into every rank's controller): identical
+    selections and Delta trajectories to the in-process lockstep oracle."""
+    from paper_2509_25762_b200 import dp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_cpp, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = _cfg()
+    oracle = dp.run_lockstep_oracle(cfg, 11, world, _reward)
+    assert len({tuple(d for _, d, _ in got[r]) for r in range(world)}) == 1
+    for r in range(world):
+        assert [[i for i in ids if i >= 0] for ids, _, _ in got[r]] == [ids for ids, _ in oracle[r]]
+        # StepRecord.delta is the step's capacity; the oracle logs the updated one
+        assert [d for _, d, _ in got[r]][1:] == [d for _, d in oracle[r]][:-1]
+        assert all(i % world == r for ids, _, _ in got[r] for i in ids if i >= 0)
+    # global mean reward: both ranks record the same value each step
+    assert [m for _, _, m in got[0]] == [m for _, _, m in got[1]]

@@ -595,3 +595,43 @@ def test_engine_input_errors_map_to_reference_exceptions():
     eng.close()
     with pytest.raises(ConfigError):
         Engine("tiny", dtype=7)
+
+
+def test_run_seed_ex_prompt_source_and_kv_admission_control():
+    """The C++ step loop with the host prompt source (oppo_run_seed_ex, the
+    reference's PromptSource seam): decisions equal the logical loop's and the
+    engine holds exactly the host's prompts.  With a KV pool smaller than the
+    B + delta worst case, refill defers sequences instead of failing, and the
+    run still completes with every sequence selected at most once."""
+    cfg = S.default_config(mode=abi.RUN_SIMULATE, steps=6, batch_size=8, prompt_len=8, delta_init=4,
+                           delta_max=4, controller=abi.DELTA_FIXED, chunk_size=16,
+                           lengths_kind=abi.LEN_LOGNORMAL, lengths_mu_log=3.5, lengths_sigma_log=0.6,
+                           lengths_cap=64, latency_decode_per_token=1, latency_prefill_per_token=0,
+                           latency_reward_residual=0, latency_placement=1)
+    seen = {}
+
+    def pf(i, plen):
+        t = [(i * 7 + q * 13) % 512 for q in range(plen)]
+        seen[i] = t
+        return t
+
+    checked = []
+
+    def on_step(rec):  # prompts of the step's sequences are the host's
+        return False
+
+    eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=16, max_prompt_len=8, max_response_len=64,
+                 sample_seed=SAMPLE_SEED)
+    recs, sel, leds = eng.run_seed_ex(cfg, 1, prompt_fn=pf, on_step=on_step)
+    _, lsel = S.run_seed_logical(cfg, 1)
+    assert sel == lsel
+    assert len(recs) == 6 and all(l.decode_iters > 0 for l in leds)
+    eng.close()
+    # admission control: 14 pages of 64 tokens; a sequence needs 1-2 pages
+    eng = Engine("tiny", dtype=abi.DTYPE_F32, max_slots=16, max_prompt_len=8, max_response_len=64,
+                 sample_seed=SAMPLE_SEED, kv_pages=14)
+    recs, sel, _ = eng.run_seed_ex(cfg, 1, prompt_fn=pf)
+    got = [i for s in sel for i in s if i >= 0]
+    assert len(recs) == 6 and len(got) == len(set(got)) and len(got) >= 24
+    assert sel != lsel  # the deferrals changed the schedule (the test is not vacuous)
+    eng.close()
