@@ -37,19 +37,41 @@ CFG2 = dict(name="cfg2", actor="0.5b", scorer="0.5b", batch=256, prompt_len=128,
 # BASELINE configs[2] shape on one GPU: 1.5B actor + 0.5B scorers (chunk 64, 10% overcommit)
 CFG3 = dict(name="cfg3", actor="1.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
             sigma=1.0, cap=1024, chunk=64, delta=26)
+# BASELINE configs[3] per GPU: 7B actor + 1.5B scorers, 512 prompts over 8 GPUs = 64 per GPU,
+# LN(5.5, 1.0) cap 2048, 10% overcommit (6 per GPU); the update in 4096-row micro-batches
+CFG4 = dict(name="cfg4", actor="7b", scorer="1.5b", batch=64, prompt_len=128, mu=5.5,
+            sigma=1.0, cap=2048, chunk=64, delta=6, train_rows=4096)
 WORKLOADS = {}
 TINY = dict(name="cfg1", actor="tiny", scorer="tiny", batch=8, prompt_len=8, mu=3.5, sigma=0.6,
             cap=64, chunk=16, delta=2)
-WORKLOADS.update(cfg1=TINY, cfg2=CFG2, cfg3=CFG3)
+WORKLOADS.update(cfg1=TINY, cfg2=CFG2, cfg3=CFG3, cfg4=CFG4)
+
+
+def workload(args):
+    """The --workload entry with the --chunk / --delta / --batch overrides."""
+    wl = dict(WORKLOADS[args.workload])
+    for k in ("chunk", "delta", "batch"):
+        if getattr(args, k, None) is not None:
+            wl[k] = getattr(args, k)
+            wl["name"] += f" {k}={wl[k]}"
+    return wl
+
+
+def kv_bytes_per_token(shape):
+    """K + V bytes (bf16) one token adds to a model's cache over all layers."""
+    from paper_2509_25762_b200.engine import SHAPES
+    d = SHAPES[shape]
+    return 2 * d["n_layers"] * d["n_kv_heads"] * d["head_dim"] * 2
 
 
 def peaks():
+    """(HBM GB/s, bf16 TFLOP/s burst, bf16 TFLOP/s sustained, source)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, 1590.0, "fallback"
 
 
 # ------------------------------------------------------------------ clocks
@@ -149,6 +171,8 @@ def run_arm(eng, wl, cfg, seed, steps, warmup, rank, world, dist):
     out = []
     for r, led in list(zip(recs, leds))[warmup:]:
         out.append(dict(samples=r.finished, step_us=led.step_us, update_us=r.update_us, loop_us=led.decode_loop_us,
+                        decode_flops=led.decode_flops, prefill_flops=led.prefill_flops,
+                        prefill_bytes=led.prefill_bytes, loop_kv_bytes=led.decode_kv_bytes,
                         loop_bytes=led.decode_weight_bytes + led.decode_kv_bytes, decode_us=led.decode_us,
                         score_us=led.score_us, iters=led.decode_iters, decode_tokens=led.decode_tokens,
                         prefill_tokens=led.prefill_tokens, launches=led.kernel_launches,
@@ -217,35 +241,90 @@ def make_cfg(wl, baseline=False, ref_side=False):
     return base_fn(cfg) if baseline else cfg
 
 
-def decode_roofline(recs, hbm_peak, peak_src):
+def decode_roofline(recs, hbm_peak, peak_src, actor):
     """The dominant unit of the step: one actor decode iteration (a CUDA graph
-    of ~200 launches: 24 layers x {RMSNorm, qkv GEMM, RoPE/KV append, paged
-    attention, O GEMM, RMSNorm, gate|up GEMM, down GEMM} + lm_head/sampling),
-    timed live with CUDA events on the actor stream over the timed steps'
-    decode loops.  Algorithmic bytes per iteration (SURVEY 8d B_dec): the
-    actor's weights once (non-embedding + lm_head, 0.988 GB) + per active row
-    the KV positions it reads and the row it appends (12,288 B per position)."""
+    of ~7 launches per layer: RMSNorm, q|k|v GEMM, fused RoPE/KV-append/paged
+    attention, O GEMM, RMSNorm, gate|up+SwiGLU GEMM, down GEMM, + lm_head /
+    sampling), timed live with CUDA events on the actor stream over the timed
+    steps' decode loops.  Algorithmic bytes per iteration (SURVEY 8d B_dec):
+    the actor's weights once (non-embedding + lm_head) + per active row the KV
+    positions it reads and the row it appends.  `traffic` is the ncu DRAM
+    bytes of one iteration of the same build and actor shape
+    (tools/capture_roofline.sh), at the captured row count nearest the step's
+    mean active rows; its own algorithmic bytes are given beside it."""
+    from paper_2509_25762_b200.engine import SHAPES
     loop_us = sum(r["loop_us"] for r in recs)
     loop_b = sum(r["loop_bytes"] for r in recs)
     iters = sum(r["iters"] for r in recs)
     if loop_us <= 0 or iters <= 0:
         return None
     ach = loop_b / (loop_us * 1e-6) / 1e9
-    out = {"kernel": "actor decode iteration (CUDA graph: 24 layers + lm_head/sampling)",
+    rows = sum(r["decode_tokens"] for r in recs) / iters
+    out = {"kernel": f"actor decode iteration (CUDA graph: {SHAPES[actor]['n_layers']} layers + "
+                     f"lm_head/sampling, {actor} actor, mean {rows:.0f} active rows)",
            "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
            "frac": round(ach / hbm_peak, 4), "traffic": None,
            "algorithmic_bytes_per_launch": round(loop_b / iters),
            "avg_launch_us": round(loop_us / iters, 2),
            "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
            "timing": "CUDA events on the actor stream around each step's decode loop"}
-    try:  # DRAM bytes of one decode iteration from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "r01_decode_iter_traffic.json")) as f:
+    caps = []
+    for m in (64, 128, 256):
+        path = os.path.join(ROOT, "profiles", f"r02_decode_traffic_{actor}_M{m}.json")
+        if os.path.exists(path):
+            caps.append((abs(m - rows), m, path))
+    if caps:
+        _, m, path = min(caps)
+        with open(path) as f:
             t = json.load(f)
         out["traffic"] = t["dram_bytes_per_iteration"]
-        out["traffic_source"] = t["source"]
-    except Exception:
-        pass
+        out["traffic_capture"] = {"rows": m, "file": os.path.relpath(path, ROOT),
+                                  "algorithmic_bytes": t.get("algorithmic_bytes_per_iteration"),
+                                  "traffic_over_algorithmic": t.get("traffic_over_algorithmic"),
+                                  "source": t["source"]}
     return out
+
+
+def step_roofline(recs, wl, hbm_peak, tf_sustained):
+    """Step roofline: T_roof = max(F / peak_bf16, B / BW_HBM) over the
+    step's algorithmic work -- actor decode (ledger: 2 P_dec + attention per
+    sampled token; weights per iteration + KV), scorer prefill (ledger: linear
+    + causal attention + the reference model's lm_head rows; weights per pass
+    + KV), and the full-parameter update (6 P per training row for the actor
+    and critic trunks, 6 V d per response token for the actor's lm_head;
+    bytes: bf16 weights read twice, fp32 gradient written and read, fp32
+    master read and written, bf16 weights rewritten = 22 B per parameter, plus
+    the saved activations written once and read once).  Training attention is
+    omitted (< 5% of the update's flops at these lengths).  frac = T_roof / T."""
+    from paper_2509_25762_b200.engine import SHAPES
+    a, c = SHAPES[wl["actor"]], SHAPES[wl["scorer"]]
+
+    def nonemb(d):
+        qkv = (d["n_heads"] + 2 * d["n_kv_heads"]) * d["head_dim"]
+        return d["n_layers"] * (qkv * d["d_model"] + d["n_heads"] * d["head_dim"] * d["d_model"]
+                                + 3 * d["d_model"] * d["d_ff"])
+
+    def act_bytes(d):  # saved activations per training row (write + read), bf16 / fp32
+        qkv = (d["n_heads"] + 2 * d["n_kv_heads"]) * d["head_dim"]
+        per = 2 * d["d_model"] * 4 + 2 * d["d_model"] * 2 + qkv * 2 + d["n_heads"] * d["head_dim"] * 2 \
+            + 3 * d["d_ff"] * 2
+        return 2 * d["n_layers"] * per
+
+    F = B = T = 0.0
+    for r in recs:
+        rows = r["tokens"] + r["samples"] * (wl["prompt_len"] - 1)
+        f_tr = 6.0 * (nonemb(a) + nonemb(c)) * rows + 6.0 * a["vocab"] * a["d_model"] * r["tokens"]
+        p_tr = nonemb(a) + nonemb(c) + a["vocab"] * a["d_model"] * (1 if a["tied"] else 2)
+        b_tr = 22.0 * p_tr + rows * (act_bytes(a) + act_bytes(c))
+        F += r["decode_flops"] + r["prefill_flops"] + f_tr
+        B += r["loop_bytes"] + r["prefill_bytes"] + b_tr
+        T += (r["step_us"] + r["update_us"]) * 1e-6
+    t_f, t_b = F / (tf_sustained * 1e12), B / (hbm_peak * 1e9)
+    t_roof = max(t_f, t_b)
+    return {"flops_per_step": round(F / len(recs)), "bytes_per_step": round(B / len(recs)),
+            "t_roof_ms": round(t_roof / len(recs) * 1e3, 2), "t_measured_ms": round(T / len(recs) * 1e3, 2),
+            "bound": "tensor" if t_f >= t_b else "hbm", "frac": round(t_roof / T, 4),
+            "peaks": {"bf16_tflops_sustained": tf_sustained, "hbm_gbs": hbm_peak}}
 
 
 def gemm_microbench(hbm_peak):
@@ -277,10 +356,11 @@ def prefill_gemm_microbench(tf_peak):
             "frac": round(ach / tf_peak, 4), "avg_launch_us": round(us.value, 3)}
 
 
-def cpu_baseline(wl, budget_s=12.0):
-    """The reference's own path (oracle/_ref = /root/reference core compiled here):
-    run_seed in train mode (tabular policy, V=16) at this workload's B / delta /
-    chunk / length distribution, one seed per host core."""
+def toy_reference(wl, budget_s=8.0):
+    """The reference's own CPU path (oracle/_ref = /root/reference core compiled
+    here): run_seed in train mode with its tabular toy policy (V=16) at this
+    workload's B / delta / chunk / length distribution, one seed per host
+    core.  Reported beside the neural port for scale (not the same workload)."""
     try:
         from oracle import ref as R
         if not R.available():
@@ -300,8 +380,7 @@ def cpu_baseline(wl, budget_s=12.0):
         t = time.perf_counter()
         fin = R.run_seeds_parallel(cfg, list(range(1, cores + 1)))
         dt = time.perf_counter() - t
-        return {"value": round(fin / dt, 1), "unit": "samples/s", "cores": cores,
-                "kind": "reference",
+        return {"value": round(fin / dt, 1), "unit": "samples/s", "cores": cores, "kind": "reference",
                 "sample": f"rlpipe::run_seed train mode (toy tabular policy V=16), B={wl['batch']}, "
                           f"delta={wl['delta']}, C={wl['chunk']}, LN({wl['mu']},{wl['sigma']}) cap "
                           f"{wl['cap']}, {cfg.steps} steps x {cores} seeds in {dt:.1f}s"}
@@ -309,36 +388,53 @@ def cpu_baseline(wl, budget_s=12.0):
         return {"value": None, "error": str(ex)[:200]}
 
 
-def neural_port_baseline(wl, tokens=8):
-    """The same neural workload on the host: the C oracle's fp64 forward
-    (oracle/oppo_oracle.c, single thread) of the 0.5B-shaped model over a
-    bounded sample of `tokens` tokens, projected to samples/s for this
-    workload: each sample needs its prompt + mean response through the actor
-    (decode with a KV cache costs one forward pass of the sequence) and the
-    three scorers.  Weight values do not change the timing (zeros)."""
+def port_step_counts(wl, seed=7, steps=12):
+    """Per-step counts of the workload for the CPU port: decode iterations per
+    step from the reference's own run_seed (oracle/_ref, simulate mode, the
+    lockstep latency model: one tick per decode iteration), and the token
+    counts of a steady-state step (B samples, each response decoded once,
+    each prompt + response prefilled once per scorer and trained once)."""
+    from oracle import ref as R
+    from paper_2509_25762_b200 import abi
+    cfg = make_cfg(wl, ref_side=True)
+    cfg.mode = abi.RUN_SIMULATE
+    cfg.steps = steps
+    cfg.carry_granularity = 0
+    recs, _ = R.run_seed(cfg, seed)
+    iters = float(np.mean([r.wall_ticks for r in recs[2:]]))
+    lens = np.asarray(R.sample_lengths(cfg.lengths, seed, 100000), dtype=np.float64)
+    B, P = wl["batch"], wl["prompt_len"]
+    mean_len = lens.mean()
+    dec_tokens = B * mean_len
+    ctx = P + (lens * (lens + 1) / 2).sum() / lens.sum()  # mean context of a decoded token
+    return dict(iters=iters, rows=dec_tokens / iters, ctx=ctx, prefill_tokens=B * (P + mean_len),
+                train_rows=B * (P - 1 + mean_len), samples=B)
+
+
+def cpu_port(wl, counts=None):
+    """the same neural workload on the host cores -- the fp32
+    all-cores numpy port of the engine's step (oracle/cpu_step.py: batched
+    decode iteration, scorer prefill, training forward + backward), each
+    timed on a bounded sample and projected to one step of this workload."""
     try:
-        from oracle import oracle as O
+        from oracle import cpu_step as P
         from paper_2509_25762_b200.engine import SHAPES
-        d = dict(SHAPES[wl["actor"]])
-        L, D, F, V = d["n_layers"], d["d_model"], d["d_ff"], d["vocab"]
-        qkv = (d["n_heads"] + 2 * d["n_kv_heads"]) * d["head_dim"]
-        q = d["n_heads"] * d["head_dim"]
-        z = np.zeros
-        w = {"embed": z((V, D), np.float32), "lm_head": z((V, D), np.float32),
-             "final_norm": z(D, np.float32), "ln1": [z(D, np.float32)] * L,
-             "wqkv": [z((qkv, D), np.float32)] * L, "bqkv": [z(qkv, np.float32)] * L,
-             "wo": [z((D, q), np.float32)] * L, "ln2": [z(D, np.float32)] * L,
-             "wgu": [z((2 * F, D), np.float32)] * L, "wdown": [z((D, F), np.float32)] * L}
-        g = O.GptOracle(d, w)
+        c = counts or port_step_counts(wl)
+        rows, ctx = max(1, round(c["rows"])), max(2, round(c["ctx"]))
+        seq = int(min(wl["cap"], round(c["train_rows"] / c["samples"]))) + 1
+        resp = max(1, seq - wl["prompt_len"])
         t = time.perf_counter()
-        g.forward(np.arange(tokens, dtype=np.int32) % V)
-        per_tok = (time.perf_counter() - t) / tokens
-        mean_len = float(np.exp(wl["mu"] + wl["sigma"] ** 2 / 2))  # lognormal mean (cap ignored)
-        per_sample = 4 * (wl["prompt_len"] + min(mean_len, wl["cap"])) * per_tok
-        return {"value": round(1.0 / per_sample, 6), "unit": "samples/s", "cores": 1, "kind": "port",
-                "sample": f"oracle_gpt_forward (fp64, scalar C) of the {wl['actor']} model over {tokens} "
-                          f"tokens: {per_tok * 1e3:.1f} ms/token, projected x4 models x "
-                          f"{wl['prompt_len']}+{min(mean_len, wl['cap']):.0f} tokens per sample"}
+        t_dec, t_pf, t_tr = P.measure(SHAPES[wl["actor"]], SHAPES[wl["scorer"]], rows, ctx, seq, resp)
+        dt = time.perf_counter() - t
+        step, v = P.project(t_dec, t_pf, t_tr, c["iters"], c["prefill_tokens"], c["train_rows"], c["samples"])
+        return {"value": round(v, 5), "unit": "samples/s", "cores": P.cores(), "kind": "port",
+                "sample": f"oracle/cpu_step.py fp32 numpy, BLAS on all cores: one {wl['actor']} decode iteration "
+                          f"at {rows} rows x ctx {ctx} ({t_dec:.2f} s), {wl['scorer']} prefill of 2 x {seq} "
+                          f"tokens ({t_pf * 1e3:.2f} ms/token), training fwd+bwd of {seq} rows "
+                          f"({t_tr * 1e3:.2f} ms/row), measured in {dt:.1f} s; projected to a step of "
+                          f"{c['iters']:.0f} iterations, 3 x {c['prefill_tokens']:.0f} prefill tokens, "
+                          f"2 x {c['train_rows']:.0f} training rows = {step:.0f} s for {c['samples']} samples",
+                "step_s": round(step, 1)}
     except Exception as ex:
         return {"value": None, "error": str(ex)[:200]}
 
@@ -359,14 +455,22 @@ def ours(args):
     from paper_2509_25762_b200.engine import Engine, param_count, SHAPES, nccl_comm_from_torch
     comm = nccl_comm_from_torch(rank, world, local) if world > 1 else None
 
-    wl = WORKLOADS[args.workload]
-    hbm, tflops, peak_src = peaks()
+    wl = workload(args)
+    if wl.get("train_rows"):
+        os.environ.setdefault("OPPO_TRAIN_ROWS", str(wl["train_rows"]))
+    hbm, tflops, tf_sust, peak_src = peaks()
     res = {}
+    # overlap ablations: intra-step only = streamed scoring with
+    # delta 0; inter-step only = overcommit with sequential (after-generation) scoring
     arms = [("oppo", False)] + ([] if args.no_sequential else [("sequential", True)])
     clocks = ClockSampler(local)
     with clocks:
         for name, base in arms:
             cfg = make_cfg(wl, base)
+            if not base and args.overlap == "intra":
+                cfg.delta_init = cfg.delta_min = cfg.delta_max = 0
+            elif not base and args.overlap == "inter":
+                cfg.schedule_mode = abi.MODE_SEQUENTIAL
             eng = Engine(wl["actor"], wl["scorer"], wl["scorer"], wl["scorer"], dtype=abi.DTYPE_BF16,
                          max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
                          max_response_len=wl["cap"], page_size=64, device=local,
@@ -401,7 +505,9 @@ def ours(args):
         "config": {"workload": f"{wl['name']}: {wl['actor']} actor + 3x {wl['scorer']} scorers "
                                f"(reward/critic/ref), B={wl['batch']}/GPU, prompt {wl['prompt_len']}, "
                                f"LN({wl['mu']},{wl['sigma']}) cap {wl['cap']}, chunk {wl['chunk']}, "
-                               f"delta {wl['delta']}, token-granular carry",
+                               f"delta {wl['delta']}, token-granular carry"
+                               + ("" if args.overlap == "both" else f", overlapped arm: {args.overlap}-step "
+                                  "overlap only"),
                    "global_batch": wl["batch"] * world, "parallelism": f"dp{world}",
                    "params_per_model": param_count(SHAPES[wl["actor"]]),
                    "l2": "working set > L2 (4 models x ~1 GB bf16 weights + paged KV)",
@@ -430,13 +536,24 @@ def ours(args):
         "tokens_per_step": int(np.mean([r["tokens"] for r in rec])),
         "prefill_tokens_per_step": int(np.mean([r["prefill_tokens"] for r in rec])),
     }
-    line["roofline"] = decode_roofline(rec, hbm, peak_src)
+    line["roofline"] = decode_roofline(rec, hbm, peak_src, wl["actor"])
+    line["step_roofline"] = step_roofline(rec, wl, hbm, tf_sust)
     line["kernels"] = {"decode_gemm_gate_up": gemm_microbench(hbm), "prefill_gemm_gate_up": prefill_gemm_microbench(tflops)}
-    line["cpu_baseline"] = cpu_baseline(wl) if not args.no_cpu else None
-    if line["cpu_baseline"] is not None and not args.no_cpu:
-        # the reference's CPU path runs its toy tabular policy; the same neural
-        # workload on the host cores, for scale (reported, not the target)
-        line["cpu_baseline"]["neural_port"] = neural_port_baseline(wl)
+    if not args.no_cpu:
+        # the same neural workload on the host cores (the reference has no
+        # neural path), with this run's own step counts; the reference's toy
+        # tabular path beside it for scale (reported baselines, not targets)
+        counts = dict(iters=float(np.mean([r["iters"] for r in rec])),
+                      rows=float(np.sum([r["decode_tokens"] for r in rec]) / np.sum([r["iters"] for r in rec])),
+                      ctx=float(np.sum([r["loop_kv_bytes"] for r in rec]) /
+                                (kv_bytes_per_token(wl["actor"]) * np.sum([r["decode_tokens"] for r in rec]))),
+                      prefill_tokens=float(np.mean([r["prefill_tokens"] for r in rec])),
+                      train_rows=float(np.mean([r["tokens"] + r["samples"] * (wl["prompt_len"] - 1) for r in rec])),
+                      samples=int(np.mean([r["samples"] for r in rec])))
+        line["cpu_baseline"] = cpu_port(wl, counts)
+        line["cpu_baseline"]["reference_toy"] = toy_reference(wl)
+    else:
+        line["cpu_baseline"] = None
     line["clocks"] = clocks.summary()
     line["gpu_launches"] = int(sum(r["launches"] for r in rec))
     print(json.dumps(line), flush=True)
@@ -445,42 +562,44 @@ def ours(args):
 
 
 def reference(args):
-    """--impl reference: the reference's own CPU implementation of the path
-    (oracle/_ref, the unmodified /root/reference core) on the host cores."""
+    """--impl reference: the CPU implementation of this workload on the host
+    cores.  The reference has no neural path (its actor is a tabular toy,
+    ppo.hpp:21-35), so each step is the all-cores port of the engine's step
+    (oracle/cpu_step.py) on a bounded sample, projected to one step whose
+    decode-iteration count comes from the reference's own run_seed
+    (oracle/_ref, lockstep latency model); the reference's toy path at the
+    same B / delta / chunk / lengths is reported beside it."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    wl = WORKLOADS[args.workload]
+    wl = workload(args)
     try:
         from oracle import ref as R
-        from paper_2509_25762_b200 import scheduler as S
         if not R.available():
             raise FileNotFoundError("oracle/_ref/librlpipe_ref.so not built")
-        cores = os.cpu_count() or 1
-        cfg = make_cfg(wl, ref_side=True)
-        S.set_field(cfg, "vocab", 16)
-        S.set_field(cfg, "ppo_learning_rate", 0.1)
-        S.set_field(cfg, "ppo_value_learning_rate", 0.2)
-        cfg.carry_granularity = 0
-        cfg.steps = 1
+        counts = port_step_counts(wl)
         for _ in range(args.warmup):
-            R.run_seeds_parallel(cfg, list(range(1, cores + 1)))
-        tot, fin = 0.0, 0
-        for k in range(args.steps):
-            t = time.perf_counter()
-            fin += R.run_seeds_parallel(cfg, list(range(100 + k * cores, 100 + (k + 1) * cores)))
-            tot += time.perf_counter() - t
-        v = fin / tot
-        line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "samples/s",
+            cpu_port(wl, counts)
+        vals, last = [], None
+        for _ in range(args.steps):
+            last = cpu_port(wl, counts)
+            if last.get("value") is None:
+                raise RuntimeError(last.get("error", "cpu port failed"))
+            vals.append(last["value"])
+        v = float(np.median(vals))
+        step_s = wl["batch"] / v
+        line = {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "samples/s",
                 "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (reference toy policy)",
-                "config": {"workload": f"{wl['name']} scheduling shape, reference toy policy V=16"},
-                "cpu_baseline": {"value": round(v, 2), "unit": "samples/s", "cores": cores,
-                                 "kind": "reference",
-                                 "sample": f"one rlpipe::run_seed step per seed x {cores} seeds per step"},
-                "e2e": {"value": round(v, 2), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (constant weights; timing only)",
+                "config": {"workload": f"{wl['name']}: {wl['actor']} actor + 3x {wl['scorer']} scorers, "
+                                       f"B={wl['batch']}, prompt {wl['prompt_len']}, LN({wl['mu']},{wl['sigma']}) "
+                                       f"cap {wl['cap']}, chunk {wl['chunk']}, delta {wl['delta']}"},
+                "cpu_baseline": {"value": round(v, 5), "unit": "samples/s", "cores": last["cores"],
+                                 "kind": "port", "sample": last["sample"]},
+                "reference_toy": toy_reference(wl),
+                "e2e": {"value": round(v, 5), "unit": "samples/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
     except Exception as ex:
         line = {"impl": "reference", "unavailable": str(ex)[:200]}
@@ -541,6 +660,12 @@ def main():
     ap.add_argument("--config", default=None,
                     help="reference-schema JSON run config (+ model/gpu blocks) instead of --workload")
     ap.add_argument("--dry-run-ranks", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--chunk", type=int, default=None, help="override the workload's chunk size")
+    ap.add_argument("--delta", type=int, default=None, help="override the workload's overcommit delta")
+    ap.add_argument("--batch", type=int, default=None, help="override the workload's per-GPU batch")
+    ap.add_argument("--overlap", default="both", choices=["both", "intra", "inter"],
+                    help="overlapped arm: both overlaps, intra-step only (delta 0), inter-step only "
+                         "(sequential scoring)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
         sys.exit(spawn_ranks(args.gpus))

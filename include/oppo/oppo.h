@@ -102,6 +102,13 @@ typedef struct oppo_ledger {
     double decode_loop_us;
     double decode_weight_bytes;
     double decode_kv_bytes;
+    /* algorithmic work of the step: decode flops (2 P_dec + 4 L H hd ctx
+     * per sampled token), scorer prefill flops (linear layers, causal attention and
+     * the reference model's lm_head rows) and bytes (each pass's weights of the
+     * three scorers + the KV they append and read) */
+    double decode_flops;
+    double prefill_flops;
+    double prefill_bytes;
 } oppo_ledger;
 
 enum { OPPO_MODE_STREAMED = 0, OPPO_MODE_SEQUENTIAL = 1 };      /* ScheduleMode */
@@ -328,7 +335,8 @@ typedef struct oppo_engine_cfg {
     int32_t rank;
     int32_t world;
     int32_t use_graphs;       /* capture the decode iteration in a CUDA graph */
-    int32_t train_heads;      /* PPO update trains lm_head (actor) + value head (critic) */
+    int32_t train_heads;      /* PPO update: 0 none, 1 lm_head (actor) + value head (critic)
+                                 only, 2 every parameter of actor and critic (K11/K12) */
     int32_t scorer_sms;       /* fixed SM partition: SMs for the scorer stream (green
                                  contexts, multiple of 8), the rest run the actor; 0 = shared */
     void* nccl_comm;          /* ncclComm_t or NULL (single GPU)       */
@@ -460,6 +468,15 @@ oppo_status oppo_k_ppo_token(int32_t is_f64, int32_t n_seq, const int32_t* d_off
 oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* d_x,
                         const void* d_w, const void* d_bias, void* d_y, int32_t epilogue,
                         void* stream);
+
+/* The same GEMM with either operand MN-major (stored transposed: A as
+ * d_a[K][M] with leading dimension lda, B as d_b[K][N] with ldb; K-major
+ * operands are d_a[M][K] / d_b[N][K]), as the full-parameter update reads dY,
+ * X and W in place for its wgrad / dgrad GEMMs.  epilogue 0 store (dtype),
+ * 1 add to f32 out, 5 store f32; d_y is [M][N]. */
+oppo_status oppo_k_gemm_t(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* d_a, int32_t a_mn,
+                          int32_t lda, const void* d_b, int32_t b_mn, int32_t ldb, void* d_y, int32_t epilogue,
+                          void* stream);
 
 /* Decode-shaped GEMM (swap-AB tcgen05, M <= 512 tokens) behind the actor's
  * decode iteration.  mode 0: fp32 split-K partials into d_ws[splits][M][N]

@@ -132,6 +132,7 @@ def _declare(L):
                                    vp, vp, vp, vp]),
         "oppo_k_gemm": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, i32, vp]),
         "oppo_k_gemm_bench": (i32, [i32, i32, i32, i32, i32, i32, P(C.c_float)]),
+        "oppo_k_gemm_t": (i32, [i32, i32, i32, i32, vp, i32, i32, vp, i32, i32, vp, i32, vp]),
         "oppo_k_gemm_dec": (i32, [i32, i32, i32, vp, vp, vp, vp, i32, vp, i64, P(i32), vp]),
         "oppo_nccl_unique_id": (i32, [vp]),
         "oppo_nccl_comm_create": (i32, [vp, i32, i32, i32, P(vp)]),

@@ -50,7 +50,8 @@ class Ledger(C.Structure):
                 ("decode_iters", C.c_int64), ("decode_tokens", C.c_int64),
                 ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64),
                 ("decode_loop_us", C.c_double), ("decode_weight_bytes", C.c_double),
-                ("decode_kv_bytes", C.c_double)]
+                ("decode_kv_bytes", C.c_double), ("decode_flops", C.c_double),
+                ("prefill_flops", C.c_double), ("prefill_bytes", C.c_double)]
 
 
 class Latency(C.Structure):

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <numeric>
 
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include "engine.cuh"
@@ -99,6 +100,37 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
         cap = pinned_cap = 0;
     }
 };
+
+// Stream memory operations (driver API) for the K13 chunk-ready flags.
+PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
+PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+void stream_memops_init() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+    });
+    if (!g_wait32 || !g_write32) throw Error(OPPO_ERR_CUDA, "cuStreamWaitValue32 / cuStreamWriteValue32 unavailable");
+}
+void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t v) {
+    stream_memops_init();
+    const CUresult r = g_wait32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
+                                CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw Error(OPPO_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
+}
+void stream_write(cudaStream_t st, uint32_t* flag, uint32_t v) {
+    stream_memops_init();
+    const CUresult r = g_write32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
+                                 CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) throw Error(OPPO_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(r) + ")");
+}
 
 // Host thread that enqueues the scorer waves on the scorer stream.  A wave is
 // hundreds of launches; enqueued from the driver thread they can fill the
@@ -968,6 +1000,9 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         // off: with concurrent scorer passes the scorers finish within ~8 ms of
         // decode, shorter than the precompute on the actor SMs (215.4 vs 213.6)
         e->pre_lp = env_int("OPPO_PRE_LP", 0) != 0;
+        e->chunk_flags = env_int("OPPO_CHUNK_FLAGS", 1) != 0;
+        OPPO_CUDA_CHECK(cudaMalloc(&e->d_ready, Engine::kReadyRing * sizeof(uint32_t)));
+        OPPO_CUDA_CHECK(cudaMemsetAsync(e->d_ready, 0, Engine::kReadyRing * sizeof(uint32_t), st));
         e->g_chunk = std::max(64, env_int("OPPO_G_CHUNK", e->g_chunk)) / 8 * 8;  // update token chunk
         // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
         // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
@@ -1023,7 +1058,8 @@ void engine_free(Engine* e) {
                     static_cast<void*>(e->d_mega_bar), static_cast<void*>(e->d_mega_aws),
                     static_cast<void*>(e->d_mega_acnt), e->pre_hf, static_cast<void*>(e->pre_tok),
                     static_cast<void*>(e->pre_new), static_cast<void*>(e->pre_lse), static_cast<void*>(e->pre_meta),
-                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt)})
+                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt),
+                    static_cast<void*>(e->d_ready)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) free_work(*w);
@@ -1595,6 +1631,14 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     for (int i = 0; i < n; ++i) p_cur[i] = active[i].prefilled_tokens;
     std::vector<WavePlan> waves;
     int64_t wave_tokens = 0;
+    double pf_flops = 0, pf_bytes = 0, scorer_params[N_MODELS] = {0}, kv_bytes_tok[N_MODELS] = {0};
+    for (int mi : {REWARD, CRITIC, REF}) {  // non-embedding parameters; K+V bytes per token
+        const auto& d = e.models[mi].dims;
+        scorer_params[mi] = static_cast<double>(d.n_layers) *
+            ((static_cast<double>(d.n_heads + 2 * d.n_kv_heads) * d.head_dim + d.n_heads * d.head_dim) * d.d_model +
+             3.0 * d.d_model * d.d_ff);
+        kv_bytes_tok[mi] = 2.0 * d.n_layers * d.n_kv_heads * d.head_dim * e.esz;
+    }
     auto make_wave = [&](int at_iter, auto&& target_p) {
         std::vector<SegReq> reqs;
         for (int i : order) {  // deterministic order
@@ -1613,6 +1657,21 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
         WavePlan wv;
         wv.at_iter = at_iter;
         build_passes(e, reqs, wv, A);
+        // algorithmic work of the wave (SURVEY 8d F_pf / B_pf)
+        for (const auto& r : reqs) {
+            const double n = r.n, ctx = n * r.pos0 + n * (n + 1) / 2;  // sum of causal context lengths
+            const double resp = std::max(0, r.pos0 + r.n - std::max(r.pos0, r.prompt_len));  // ref lm_head rows
+            for (int mi : {REWARD, CRITIC, REF}) {
+                const auto& d = e.models[mi].dims;
+                pf_flops += 2.0 * scorer_params[mi] * n + 4.0 * d.n_layers * d.n_heads * d.head_dim * ctx;
+                pf_bytes += kv_bytes_tok[mi] * (n + r.pos0 + n);  // append n rows, read the context once
+            }
+            pf_flops += 2.0 * e.models[REF].dims.vocab * e.models[REF].dims.d_model * resp;
+        }
+        for (size_t k = 0; k < wv.passes.size(); ++k)
+            for (int mi : {REWARD, CRITIC, REF}) pf_bytes += scorer_params[mi] * e.esz;
+        pf_bytes += e.esz * static_cast<double>(e.models[REF].dims.vocab) * e.models[REF].dims.d_model *
+                    wv.passes.size();  // the reference model's lm_head per pass
         waves.push_back(std::move(wv));
     };
     auto whole_by = [&](int i, int64_t t) -> int {  // chunk-complete tokens after iteration t
@@ -1670,8 +1729,33 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
             }
         }
     } drain_guard{worker};
+    const bool flags = e.chunk_flags;
+    std::vector<uint32_t> wave_seq(waves.size());
+    for (size_t k = 0; flags && k < waves.size(); ++k) wave_seq[k] = ++e.ready_seq;
+    // The scorer stream's copy of wave k is enqueued one wave ahead (when wave
+    // k-1's flag is written), gated on the device by wave k's flag: the launch
+    // queue never holds more than ~two waves of work that waits on the actor,
+    // so the actor's own launches are never stuck behind them.
+    auto post_wave = [&](size_t k) {
+        uint32_t* flag = e.d_ready + (wave_seq[k] % Engine::kReadyRing);
+        const uint32_t want = wave_seq[k];
+        const WavePlan* wave = &waves[k];
+        worker.post([&e, &A, &prefill_tokens, flag, want, wave] {
+            stream_wait_geq(e.ss, flag, want);
+            int64_t tok = 0;
+            for (const auto& p : wave->passes) run_scorer_pass<T>(e, p, A, e.ss, tok);
+            prefill_tokens += tok;
+        });
+    };
+    if (flags && !waves.empty()) post_wave(0);
     auto fire_waves_at = [&](int64_t it) {
         while (wi < waves.size() && waves[wi].at_iter == it) {
+            if (flags) {  // actor-stream order: after iteration `it`, the wave's chunks are complete
+                stream_write(e.sa, e.d_ready + (wave_seq[wi] % Engine::kReadyRing), wave_seq[wi]);
+                if (wi + 1 < waves.size()) post_wave(wi + 1);
+                ++wi;
+                continue;
+            }
             cudaEvent_t ev = e.ev_pool[wi + 1];
             OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));  // actor-stream order: after iteration `it`
             const WavePlan* wave = &waves[wi];
@@ -1697,7 +1781,9 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
               3.0 * ad.d_model * ad.d_ff) +
          static_cast<double>(ad.vocab) * ad.d_model);
     const double kvb = 2.0 * ad.n_layers * ad.n_kv_heads * ad.head_dim * e.esz;  // K+V per token
-    double loop_w = 0, loop_kv = 0;
+    double loop_w = 0, loop_kv = 0, loop_f = 0;
+    const double p_dec = w_bytes / e.esz;  // non-embedding + lm_head parameters
+    const double att_f = 4.0 * ad.n_layers * ad.n_heads * ad.head_dim;  // per (token, context position)
     OPPO_CUDA_CHECK(cudaEventRecord(e.ev_loop0, e.sa));
     for (int64_t it = 1; it <= t_end; ++it) {
         while (active_n > 0 && rem_sorted[active_n - 1] < it) --active_n;
@@ -1706,6 +1792,7 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
         for (size_t r = 0; r < active_n; ++r) {
             const DecodeSeq& q = dseq[r];
             loop_kv += kvb * static_cast<double>(q.prompt_len + q.generated + it);  // ctx + appended row
+            loop_f += 2.0 * p_dec + att_f * static_cast<double>(q.prompt_len + q.generated + it);
         }
         // bucketed batch: rows [active_n, bucket) decode into the scratch slot
         const int bucket = e.cfg.use_graphs ? std::min(cdiv(active_n, 16) * 16, e.S + 16)
@@ -1761,6 +1848,9 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     ledger.decode_loop_us = ms * 1e3;
     ledger.decode_weight_bytes = loop_w;
     ledger.decode_kv_bytes = loop_kv;
+    ledger.decode_flops = loop_f;
+    ledger.prefill_flops = pf_flops;
+    ledger.prefill_bytes = pf_bytes;
     ledger.decode_iters = t_end;
     ledger.decode_tokens = decode_tokens;
     ledger.prefill_tokens = prefill_tokens;
@@ -2706,6 +2796,22 @@ oppo_status oppo_k_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
     try {
         oppo::gemm_standalone(dtype, M, N, K, d_x, d_w, static_cast<const float*>(d_bias), d_y,
                               epilogue, static_cast<cudaStream_t>(stream));
+        OPPO_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        return OPPO_OK;
+    } catch (const oppo::Error& x) {
+        oppo_set_global_error(x.what());
+        return x.code;
+    }
+}
+
+oppo_status oppo_k_gemm_t(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* d_a, int32_t a_mn,
+                          int32_t lda, const void* d_b, int32_t b_mn, int32_t ldb, void* d_y, int32_t epilogue,
+                          void* stream) {
+    try {
+        if (epilogue != oppo::EPI_STORE && epilogue != oppo::EPI_ADD_F32 && epilogue != oppo::EPI_STORE_F32)
+            oppo::input_error("oppo_k_gemm_t: epilogue must be 0 (store), 1 (add f32) or 5 (store f32)");
+        oppo::gemm_standalone_t(dtype, M, N, K, d_a, a_mn, lda, d_b, b_mn, ldb, d_y, epilogue,
+                                static_cast<cudaStream_t>(stream));
         OPPO_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
         return OPPO_OK;
     } catch (const oppo::Error& x) {

@@ -173,6 +173,17 @@ struct Engine {
     cudaStream_t sa = nullptr, ss = nullptr;
     cudaStream_t su = nullptr;  // admission prefill + PPO update: whole GPU (== sa without a partition)
     std::vector<cudaEvent_t> ev_pool;
+    // K13 chunk hand-off on the device: after the decode iteration that
+    // completes a wave's chunks the actor stream writes the wave's sequence
+    // number into a ring of per-chunk ready flags (cuStreamWriteValue32); the
+    // scorer stream waits for it (cuStreamWaitValue32, GEQ) -- no event or
+    // host round trip between the actor and the scorers, and every wave of a
+    // step is enqueued on the scorer stream up front.  OPPO_CHUNK_FLAGS=0
+    // falls back to per-wave events.
+    static constexpr int kReadyRing = 256;
+    uint32_t* d_ready = nullptr;  // [kReadyRing] flags (monotone sequence numbers)
+    uint32_t ready_seq = 0;       // last sequence number issued
+    bool chunk_flags = true;
     cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr,
                 ev_loop0 = nullptr;
     bool step_open = false;
@@ -264,6 +275,13 @@ void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, 
               const void* wt, int N, int ldw, const EpiParams& ep);
 void gemm_standalone(int dtype, int M, int N, int K, const void* x, const void* w,
                      const float* bias, void* y, int epi, cudaStream_t st);
+// Y[M,N] = A . B^T with either operand MN-major (stored transposed, a: [K][M]
+// ld lda, b: [K][N] ld ldb) -- the update's wgrad / dgrad GEMMs read dY, X
+// and W in place instead of transposed copies.
+void gemm_run_t(Engine& e, Work& w, cudaStream_t st, const void* a, int a_mn, int lda, const void* b, int b_mn,
+                int ldb, int M, int N, int K, const EpiParams& ep);
+void gemm_standalone_t(int dtype, int M, int N, int K, const void* a, int a_mn, int lda, const void* b, int b_mn,
+                       int ldb, void* y, int epi, cudaStream_t st);
 int gemm_dec_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,
                  const void* wt, int N, int ldw, int mode, void* y, int ldy, const float* bias);
 int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int ldx, const void* wt,

@@ -121,19 +121,22 @@ static const int g_tc2sm = [] {  // 0 off, 1 everywhere, 2 scorer stream only, 3
 
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
                       const void* wt, int N, int ldw, const EpiParams& ep_in, int dtype,
-                      int num_sms, float* ws, size_t ws_floats, int* cnt, int cnt_n) {
+                      int num_sms, float* ws, size_t ws_floats, int* cnt, int cnt_n, int a_mn = 0,
+                      int b_mn = 0) {
     if (M <= 0 || N <= 0) return;
     EpiParams ep = ep_in;
     ep.M = M;
     ep.N = N;
     ep.n_tiles = gemm_logit_tiles(dtype, N);
-    GemmShape sh{M, N, K, 1, 0, nullptr, nullptr};
+    GemmShape sh{M, N, K, 1, 0, nullptr, nullptr, a_mn, b_mn, ldx, ldw};
     const int m_tiles = (M + 127) / 128;
     const bool rope = ep.mode == EPI_ROPE_APPEND;
+    const bool mn = a_mn || b_mn;
     if (rope && (dtype != OPPO_DTYPE_BF16 || (ep.kv.head_dim != 64 && ep.kv.head_dim != 128)))
         throw Error(OPPO_ERR_INTERNAL, "rope-append epilogue: bf16, head_dim 64 or 128 only");
+    if (mn && (ep.mode == EPI_LOGITS || rope))
+        throw Error(OPPO_ERR_INTERNAL, "MN-major operands: store / add / softmax-grad epilogues only");
     if (dtype == OPPO_DTYPE_F32) {
-        if (ldx != K || ldw != K) throw Error(OPPO_ERR_INTERNAL, "SIMT GEMM needs packed rows");
         launch(e && e->pdl, gemm_simt<float>, dim3(m_tiles, (N + kSampleBlock - 1) / kSampleBlock),
                dim3(128), 0, st, static_cast<const float*>(x), static_cast<const float*>(wt), sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
@@ -148,7 +151,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // mainloop and the 2-CTA/SM kernel (8 epilogue warps per SM) wins
     // (bench: update 60 -> 69 ms on the persistent kernel; O / down no gain).
     const bool light = ep.mode == EPI_STORE || ep.mode == EPI_SWIGLU || ep.mode == EPI_ROPE_APPEND;
-    if (m_tiles >= 8 && light && dtype == OPPO_DTYPE_BF16 && persist_enabled()) {
+    if (m_tiles >= 8 && light && !mn && dtype == OPPO_DTYPE_BF16 && persist_enabled()) {
         // 128-wide tiles where a 256-wide last tile would waste > 5% (N = 896, 1152)
         const int pad256 = (N + 255) / 256 * 256 - N;
         const int BNp = (N % 128 == 0 && pad256 * 20 > N) ? 128 : 256;
@@ -181,7 +184,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     }
     // Token-rich prefill GEMMs (>= 8 token tiles, not the logits epilogue, the
     // output wide enough to fill the SMs): 256x256 tiles, one CTA per SM.
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && g_tc256 &&
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && g_tc256 &&
         ((M + 255) / 256) * ((N + 255) / 256) >= num_sms) {
         static std::once_flag attr256;
         std::call_once(attr256, [] {
@@ -202,7 +205,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // Token-rich prefill GEMMs: CTA-pair 256x256 tiles (cta_group::2)
     const bool scorer_stream = e && st == e->ss;
     const bool use2 = g_tc2sm == 1 || (g_tc2sm == 2 && scorer_stream) || (g_tc2sm == 3 && !scorer_stream);
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && use2) {
+    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && use2) {
         static std::once_flag attr2;
         std::call_once(attr2, [] {
             OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm,
@@ -253,7 +256,15 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     const int kb = (K + 63) / 64;
     const int tiles = n_tiles * m_tiles;
     int splits = 1;
-    if (ws && cnt && ep.mode != EPI_LOGITS && tiles * 2 <= num_sms && kb >= 4) {
+    // long-K GEMMs with few output tiles (the update's weight gradients, K =
+    // tokens; its vocabulary dgrad, K = V): split K until both CTA slots of
+    // every SM are busy (133 tiles of dW_down ran at 45% of the slots)
+    const bool long_k = m_tiles > 4 && kb >= 64;
+    if (ws && cnt && ep.mode != EPI_LOGITS && long_k && tiles * 4 <= 3 * 2 * num_sms) {
+        splits = std::max(1, std::min((2 * num_sms) / tiles, 8));
+        while (splits > 1 && (static_cast<size_t>(splits) * tiles * 128 * BN > ws_floats || tiles > cnt_n))
+            --splits;
+    } else if (ws && cnt && ep.mode != EPI_LOGITS && tiles * 2 <= num_sms && kb >= 4) {
         splits = std::max(1, std::min(std::min(kb / 2, (num_sms + tiles - 1) / tiles), 4));
         while (splits > 1 && (static_cast<size_t>(splits) * tiles * 128 * BN > ws_floats ||
                               tiles > cnt_n))
@@ -266,8 +277,9 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     sh.workspace = ws;
     sh.counters = cnt;
     CUtensorMap s1, s2;
-    const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
-    const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, BN, s2);
+    // MN-major operands are stored [K][M] / [K][N]: [64 k][64] boxes
+    const CUtensorMap& mx = a_mn ? cached_map(e, x, K, M, ldx, 64, s1) : cached_map(e, x, M, K, ldx, 128, s1);
+    const CUtensorMap& mw = b_mn ? cached_map(e, wt, K, N, ldw, 64, s2) : cached_map(e, wt, N, K, ldw, BN, s2);
     const dim3 grid(m_tiles, n_tiles, splits);
     switch (BN) {
     case 64:
@@ -398,6 +410,26 @@ void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, 
     gemm_impl(&e, &w, st, x, M, K, ldx, wt, N, ldw, ep, e.dtype, w.sms, w.gemm_ws,
               w.gemm_ws_floats, w.gemm_cnt, w.gemm_cnt_n);
     e.launches += 1;
+}
+
+void gemm_run_t(Engine& e, Work& w, cudaStream_t st, const void* a, int a_mn, int lda, const void* b, int b_mn,
+                int ldb, int M, int N, int K, const EpiParams& ep) {
+    gemm_impl(&e, &w, st, a, M, K, lda, b, N, ldb, ep, e.dtype, w.sms, w.gemm_ws, w.gemm_ws_floats, w.gemm_cnt,
+              w.gemm_cnt_n, a_mn, b_mn);
+    e.launches += 1;
+}
+
+void gemm_standalone_t(int dtype, int M, int N, int K, const void* a, int a_mn, int lda, const void* b, int b_mn,
+                       int ldb, void* y, int epi, cudaStream_t st) {
+    EpiParams ep{};
+    ep.mode = epi;
+    ep.y = y;
+    ep.ldy = N;
+    ep.scale = 1.0f;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gemm_impl(nullptr, nullptr, st, a, M, K, lda, b, N, ldb, ep, dtype, sms, nullptr, 0, nullptr, 0, a_mn, b_mn);
 }
 
 void gemm_standalone(int dtype, int M, int N, int K, const void* x, const void* w,

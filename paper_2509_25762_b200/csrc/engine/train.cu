@@ -10,8 +10,15 @@
 // pre-activation; the loss head (actor: lm_head + log-softmax + clipped
 // surrogate, dObj/dlogits through the softmax-grad GEMM epilogue; critic:
 // value head + squared error to the returns); then the backward, layer by
-// layer, with dgrad GEMMs against transposed weight copies and wgrad GEMMs
-// (dY^T X over the token dimension) accumulating into fp32 gradient buffers.
+// layer.  The dgrad GEMMs (dX = dY W) and wgrad GEMMs (dW += dY^T X over the
+// token dimension, into fp32 gradient buffers) read W, dY and X in place:
+// the tcgen05 GEMM takes either operand MN-major (K-outer storage, TMA boxes of
+// [64 k][64 mn], transposed UMMA descriptors), so no transposed copy of a
+// weight or activation is ever materialised.  SwiGLU runs in the gate|up
+// GEMM's epilogue (forward: product + saved pre-activations; backward: the
+// dgrad GEMM of the down projection writes d(gate, up) directly), and the
+// RMSNorm backward emits the bf16 copy of the residual gradient the next
+// GEMMs read.
 // After the last micro-batch the gradients are allreduced across the
 // data-parallel ranks (one NCCL call per tensor) and applied by SGD to the
 // fp32 masters, from which the bf16 compute weights are re-rounded.
@@ -47,7 +54,6 @@ struct PT {
     void* w = nullptr;        // compute tensor (T matrix or fp32 vector)
     float* master = nullptr;  // fp32 master (bf16 matrices), else null (w is fp32)
     float* grad = nullptr;    // fp32 gradient, same layout as w
-    void* wT = nullptr;       // transposed compute copy [cols][rows] (dgrad operand)
     int64_t rows = 0, cols = 1;
     bool matrix = false;
     int64_t n() const { return rows * cols; }
@@ -94,15 +100,16 @@ struct TrainState {
     ModelT m[N_MODELS];
     Scratch scr;
     int rows_cap = 0;  // training rows the scratch is sized for
-    // per-layer saved activations
+    // per-layer saved activations: residual inputs (fp32), normed inputs of
+    // the attention / MLP blocks, post-RoPE q|k|v, attention output + lse,
+    // (gate, up) pre-activations and the SwiGLU product
     std::vector<float*> x_in, x_mid, lse, rstd1, rstd2;
-    std::vector<void*> qkv, o, gu;
+    std::vector<void*> h1, h2, qkv, o, gu, ff;
     // transients
-    float *x = nullptr, *dx = nullptr, *dh = nullptr, *dff = nullptr, *dqkv = nullptr, *dvec = nullptr,
-          *gscr = nullptr, *colp = nullptr, *head_out = nullptr, *dhf_c = nullptr;
-    void *h = nullptr, *hf = nullptr, *ff = nullptr, *dgu = nullptr, *dxc = nullptr, *dxT = nullptr,
-         *aT = nullptr, *bT = nullptr, *dO = nullptr, *dqkvc = nullptr, *hf_resp = nullptr, *hfT = nullptr,
-         *G = nullptr, *Gt = nullptr;
+    float *x = nullptr, *dx = nullptr, *dh = nullptr, *dqkv = nullptr, *dvec = nullptr, *gscr = nullptr,
+          *colp = nullptr, *head_out = nullptr, *dhf_c = nullptr;
+    void *hf = nullptr, *dgu = nullptr, *dxc = nullptr, *dO = nullptr, *dqkvc = nullptr, *hf_resp = nullptr,
+         *Gt = nullptr;
     int32_t *tok = nullptr, *pos = nullptr;
     int g_rows = 0;  // lm_head gradient chunk (rows)
 };
@@ -114,7 +121,6 @@ void train_free(Engine& e) {
     for (auto& m : ts->m)
         for (PT* p : m.all()) {
             if (p->grad) cudaFree(p->grad);
-            if (p->wT) cudaFree(p->wT);
             if (p->master && !(p == &m.embed && p->master == e.models[ACTOR].lm_master)) cudaFree(p->master);
         }
     delete ts;
@@ -123,8 +129,7 @@ void train_free(Engine& e) {
 
 namespace {
 
-PT make_pt(Engine& e, void* w, int64_t rows, int64_t cols, bool matrix, float* master_existing, bool want_T,
-           cudaStream_t st) {
+PT make_pt(Engine& e, void* w, int64_t rows, int64_t cols, bool matrix, float* master_existing, cudaStream_t st) {
     PT p;
     p.w = w;
     p.rows = rows;
@@ -140,7 +145,6 @@ PT make_pt(Engine& e, void* w, int64_t rows, int64_t cols, bool matrix, float* m
                                                                              p.master, p.n());
         }
     }
-    if (want_T) p.wT = dalloc(p.n() * e.esz);
     return p;
 }
 
@@ -152,40 +156,36 @@ void setup_model(Engine& e, TrainState& ts, int mid, cudaStream_t st) {
     const int64_t D = d.d_model, V = d.vocab, F = d.d_ff, qkv = m.qkv_width(), qw = m.q_width();
     const bool actor = mid == ACTOR;
     float* lm_master = actor ? m.lm_master : nullptr;
-    mt.embed = make_pt(e, m.embed, V, D, true, d.tied ? lm_master : nullptr, actor && d.tied, st);
-    if (!d.tied && actor) mt.lm_head = make_pt(e, m.lm_head, V, D, true, lm_master, true, st);
+    mt.embed = make_pt(e, m.embed, V, D, true, d.tied ? lm_master : nullptr, st);
+    if (!d.tied && actor) mt.lm_head = make_pt(e, m.lm_head, V, D, true, lm_master, st);
     else mt.lm_head = mt.embed;
-    mt.final_norm = make_pt(e, m.final_norm, D, 1, false, nullptr, false, st);
-    if (m.head) mt.head = make_pt(e, m.head, D, 1, false, nullptr, false, st);
+    mt.final_norm = make_pt(e, m.final_norm, D, 1, false, nullptr, st);
+    if (m.head) mt.head = make_pt(e, m.head, D, 1, false, nullptr, st);
     mt.layers.resize(d.n_layers);
     for (int l = 0; l < d.n_layers; ++l) {
         auto& L = m.layers[l];
         auto& T = mt.layers[l];
-        T.wqkv = make_pt(e, L.wqkv, qkv, D, true, nullptr, true, st);
-        T.bqkv = make_pt(e, L.bqkv, qkv, 1, false, nullptr, false, st);
-        T.wo = make_pt(e, L.wo, D, qw, true, nullptr, true, st);
-        T.wgu = make_pt(e, L.wgu, 2 * F, D, true, nullptr, true, st);
-        T.wdown = make_pt(e, L.wdown, D, F, true, nullptr, true, st);
-        T.ln1 = make_pt(e, L.ln1, D, 1, false, nullptr, false, st);
-        T.ln2 = make_pt(e, L.ln2, D, 1, false, nullptr, false, st);
+        T.wqkv = make_pt(e, L.wqkv, qkv, D, true, nullptr, st);
+        T.bqkv = make_pt(e, L.bqkv, qkv, 1, false, nullptr, st);
+        T.wo = make_pt(e, L.wo, D, qw, true, nullptr, st);
+        T.wgu = make_pt(e, L.wgu, 2 * F, D, true, nullptr, st);
+        T.wdown = make_pt(e, L.wdown, D, F, true, nullptr, st);
+        T.ln1 = make_pt(e, L.ln1, D, 1, false, nullptr, st);
+        T.ln2 = make_pt(e, L.ln2, D, 1, false, nullptr, st);
     }
     mt.ready = true;
-}
-
-template <class T>
-void transpose(const void* in, int rows, int cols, int ld_out, void* out, cudaStream_t st, bool in_f32 = false) {
-    const dim3 grid(cdiv(cols, 32), cdiv(std::max(rows, ld_out), 32)), block(32, 8);
-    if (in_f32)
-        train::transpose_cvt<float, T><<<grid, block, 0, st>>>(static_cast<const float*>(in), rows, cols, cols,
-                                                               ld_out, static_cast<T*>(out));
-    else
-        train::transpose_cvt<T, T><<<grid, block, 0, st>>>(static_cast<const T*>(in), rows, cols, cols, ld_out,
-                                                           static_cast<T*>(out));
 }
 
 // Y[M, N] (epilogue ep) = A[M, K] . B[N, K]^T, packed rows
 void mm(Engine& e, cudaStream_t st, const void* A, int M, int K, const void* B, int N, EpiParams ep) {
     gemm_run(e, e.ws, st, A, M, K, K, B, N, K, ep);
+}
+// The same with operands read in place: K-major (kK, stored [M][K] / [N][K])
+// or MN-major (kMN, stored [K][M] / [K][N]), leading dimension ld.
+constexpr int kK = 0, kMN = 1;
+void mmt(Engine& e, cudaStream_t st, const void* A, int a_mn, int lda, const void* B, int b_mn, int ldb, int M,
+         int N, int K, EpiParams ep) {
+    gemm_run_t(e, e.ws, st, A, a_mn, lda, B, b_mn, ldb, M, N, K, ep);
 }
 EpiParams epi(int mode, void* y, int ldy, float scale = 1.f, const float* bias = nullptr) {
     EpiParams p{};
@@ -210,17 +210,6 @@ void rmsnorm(Engine& e, float* x, const float* g, T* out, int rows, int D, cudaS
              const float* head_w = nullptr, float* head_out = nullptr) {
     rmsnorm_rows<T><<<cdiv(rows, 4), 128, 0, st>>>(x, g, out, rows, D, kEps, head_w, head_out, nullptr, nullptr,
                                                    nullptr, 0, 0, -1, nullptr, 0, size_t(0));
-}
-
-const dim3 kTile(32, 8);
-template <class T>
-void cvt_t(const float* x, int rows, int cols, int ldT, void* y, void* yT, cudaStream_t st) {
-    train::cvt_t<T><<<dim3(cdiv(cols, 32), cdiv(ldT, 32)), kTile, 0, st>>>(x, rows, cols, ldT, static_cast<T*>(y),
-                                                                          static_cast<T*>(yT));
-}
-template <class T>
-void norm_t(const float* x, const float* rstd, const float* g, int rows, int d, int ldT, void* hT, cudaStream_t st) {
-    train::norm_t<T><<<dim3(cdiv(d, 32), cdiv(ldT, 32)), kTile, 0, st>>>(x, rstd, g, rows, d, ldT, static_cast<T*>(hT));
 }
 
 template <class T>
@@ -314,43 +303,34 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
     }
     if (rows <= ts.rows_cap) return;
     ts.scr.release();
-    ts.x_in.assign(L, nullptr);
-    ts.x_mid.assign(L, nullptr);
-    ts.lse.assign(L, nullptr);
-    ts.rstd1.assign(L, nullptr);
-    ts.rstd2.assign(L, nullptr);
-    ts.qkv.assign(L, nullptr);
-    ts.o.assign(L, nullptr);
-    ts.gu.assign(L, nullptr);
-    const size_t R = rows, Rp = (R + 31) / 32 * 32, es = sizeof(T);
+    for (auto* v : {&ts.x_in, &ts.x_mid, &ts.lse, &ts.rstd1, &ts.rstd2}) v->assign(L, nullptr);
+    for (auto* v : {&ts.h1, &ts.h2, &ts.qkv, &ts.o, &ts.gu, &ts.ff}) v->assign(L, nullptr);
+    const size_t R = rows, es = sizeof(T);
     for (int l = 0; l < L; ++l) {
         ts.x_in[l] = static_cast<float*>(ts.scr.take(R * D * 4));
         ts.x_mid[l] = static_cast<float*>(ts.scr.take(R * D * 4));
         ts.lse[l] = static_cast<float*>(ts.scr.take(R * H * 4));
         ts.rstd1[l] = static_cast<float*>(ts.scr.take(R * 4));
         ts.rstd2[l] = static_cast<float*>(ts.scr.take(R * 4));
+        ts.h1[l] = ts.scr.take(R * D * es);
+        ts.h2[l] = ts.scr.take(R * D * es);
         ts.qkv[l] = ts.scr.take(R * qkv * es);
         ts.o[l] = ts.scr.take(R * qw * es);
         ts.gu[l] = ts.scr.take(R * 2 * F * es);
+        ts.ff[l] = ts.scr.take(R * F * es);
     }
     const size_t wide = std::max<size_t>({static_cast<size_t>(D), static_cast<size_t>(qkv), static_cast<size_t>(2 * F)});
     ts.x = static_cast<float*>(ts.scr.take(R * D * 4));
     ts.dx = static_cast<float*>(ts.scr.take(R * D * 4));
     ts.dh = static_cast<float*>(ts.scr.take(R * D * 4));
-    ts.dff = static_cast<float*>(ts.scr.take(R * F * 4));
     ts.dqkv = static_cast<float*>(ts.scr.take(R * qkv * 4));
     ts.dvec = static_cast<float*>(ts.scr.take(R * H * 4));
     ts.gscr = static_cast<float*>(ts.scr.take(R * std::max(D, qkv) * 4));
     ts.colp = static_cast<float*>(ts.scr.take(64 * wide * 4));
     ts.head_out = static_cast<float*>(ts.scr.take(R * 4));
-    ts.h = ts.scr.take(R * D * es);
     ts.hf = ts.scr.take(R * D * es);
-    ts.ff = ts.scr.take(R * F * es);
     ts.dgu = ts.scr.take(R * 2 * F * es);
     ts.dxc = ts.scr.take(R * D * es);
-    ts.dxT = ts.scr.take(Rp * D * es);
-    ts.aT = ts.scr.take(Rp * wide * es);
-    ts.bT = ts.scr.take(Rp * std::max({D, F, qw}) * es);
     ts.dO = ts.scr.take(R * qw * es);
     ts.dqkvc = ts.scr.take(R * qkv * es);
     ts.tok = static_cast<int32_t*>(ts.scr.take(R * 4));
@@ -358,10 +338,7 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
     ts.hf_resp = ts.scr.take(static_cast<size_t>(resp_rows) * D * es);
     ts.dhf_c = static_cast<float*>(ts.scr.take(static_cast<size_t>(resp_rows) * D * 4));
     ts.g_rows = std::min(resp_rows, 4096);
-    const size_t gp = (ts.g_rows + 7) / 8 * 8;
-    ts.hfT = ts.scr.take(gp * D * es);
-    ts.G = ts.scr.take(gp * V * es);
-    ts.Gt = ts.scr.take(gp * V * es);
+    ts.Gt = ts.scr.take(static_cast<size_t>(ts.g_rows) * V * es);
     ts.rows_cap = rows;
 }
 
@@ -380,11 +357,7 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
     const int D = d.d_model, H = d.n_heads, KV = d.n_kv_heads, hd = d.head_dim, F = d.d_ff, V = d.vocab;
     const int qkvw = m.qkv_width(), qw = m.q_width(), Lyr = d.n_layers;
     const bool actor = mid == ACTOR;
-    // weight transposes (dgrad operands) and zeroed gradients
     for (PT* p : mt.all()) OPPO_CUDA_CHECK(cudaMemsetAsync(p->grad, 0, p->n() * 4, st));
-    for (PT* p : mt.all())
-        if (p->wT) transpose<T>(p->w, static_cast<int>(p->rows), static_cast<int>(p->cols), static_cast<int>(p->rows),
-                                p->wT, st);
     // micro-batches of whole sequences
     const int n = static_cast<int>(b.slot.size());
     int s0 = 0;
@@ -394,7 +367,7 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             rows += b.P[s1] + b.L[s1] - 1;
             ++s1;
         }
-        const int Tr = rows, Tp = (Tr + 7) / 8 * 8;
+        const int Tr = rows;
         const int r0 = b.off[s0], Nr = b.off[s1] - r0;  // response tokens of this micro-batch
         // metadata: sequences, attention blocks, response-row map
         std::vector<train::TSeq> seqs;
@@ -461,24 +434,25 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
         // ------------------------------------------------------- forward
         float* x = ts.x;
         embed_rows<T><<<Tr, 128, 0, st>>>(static_cast<const T*>(m.embed), ts.tok, x, Tr, D);
-        T* h = static_cast<T*>(ts.h);
         for (int l = 0; l < Lyr; ++l) {
             auto& Lw = m.layers[l];
             T* qkv = static_cast<T*>(ts.qkv[l]);
             T* o = static_cast<T*>(ts.o[l]);
-            T* gu = static_cast<T*>(ts.gu[l]);
+            T* h1 = static_cast<T*>(ts.h1[l]);
+            T* h2 = static_cast<T*>(ts.h2[l]);
             OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_in[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
-            train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln1, Tr, D, kEps, h, ts.rstd1[l]);
-            mm(e, st, h, Tr, D, Lw.wqkv, qkvw, epi(EPI_STORE, qkv, qkvw, 1.f, Lw.bqkv));
+            train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln1, Tr, D, kEps, h1, ts.rstd1[l]);
+            mm(e, st, h1, Tr, D, Lw.wqkv, qkvw, epi(EPI_STORE, qkv, qkvw, 1.f, Lw.bqkv));
             train::rope_rows<T><<<Tr, 128, 0, st>>>(qkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 0);
             attn<T>(hd, 0, d_blk, nb, qkv, qkvw, H, KV, o, ts.lse[l], nullptr, nullptr, nullptr, st);
             mm(e, st, o, Tr, qw, Lw.wo, D, epi(EPI_ADD_F32, x, D));
             OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_mid[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
-            train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln2, Tr, D, kEps, h, ts.rstd2[l]);
-            mm(e, st, h, Tr, D, Lw.wgu, 2 * F, epi(EPI_STORE, gu, 2 * F));
-            train::swiglu_fwd4<T><<<cdiv(static_cast<int64_t>(Tr) * F / 4, 256), 256, 0, st>>>(
-                gu, static_cast<T*>(ts.ff), static_cast<int64_t>(Tr) * F);
-            mm(e, st, ts.ff, Tr, F, Lw.wdown, D, epi(EPI_ADD_F32, x, D));
+            train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln2, Tr, D, kEps, h2, ts.rstd2[l]);
+            EpiParams eg = epi(EPI_SWIGLU, ts.ff[l], F);  // SwiGLU product + saved (gate, up)
+            eg.y2 = ts.gu[l];
+            eg.ldy2 = 2 * F;
+            mm(e, st, h2, Tr, D, Lw.wgu, 2 * F, eg);
+            mm(e, st, ts.ff[l], Tr, F, Lw.wdown, D, epi(EPI_ADD_F32, x, D));
         }
         T* hf = static_cast<T*>(ts.hf);
         rmsnorm<T>(e, x, m.final_norm, hf, Tr, D, st, actor ? nullptr : m.head, ts.head_out);
@@ -513,22 +487,19 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             // and the hidden-state dgrad
             const PT& lm = mt.lm_head;
             for (int c0 = 0; c0 < Nr; c0 += ts.g_rows) {
-                const int cn = std::min(ts.g_rows, Nr - c0), cp = (cn + 7) / 8 * 8;
-                EpiParams ep{};
+                const int cn = std::min(ts.g_rows, Nr - c0);
+                EpiParams ep{};  // G = dObj/dlogits [cn][V], row-major
                 ep.mode = EPI_SOFTMAX_GRAD;
-                ep.y = ts.G;
-                ep.ldy = cp;
                 ep.y2 = ts.Gt;
                 ep.ldy2 = V;
                 ep.lse = b.lse + r0 + c0;
                 ep.coef = b.dobj + r0 + c0;
                 ep.targets = b.tok + r0 + c0;
-                if (cp != cn) OPPO_CUDA_CHECK(cudaMemsetAsync(ts.G, 0, static_cast<size_t>(V) * cp * sizeof(T), st));
                 const T* hc = hr + static_cast<size_t>(c0) * D;
                 mm(e, st, hc, cn, D, m.lm_head, V, ep);
-                transpose<T>(hc, cn, D, cp, ts.hfT, st);
-                mm(e, st, ts.G, V, cp, ts.hfT, D, epi(EPI_ADD_F32, lm.grad, D));
-                mm(e, st, ts.Gt, cn, V, lm.wT, D, epi(EPI_STORE_F32, ts.dhf_c, D));
+                // dW_lm += G^T H (both MN-major over the chunk's tokens); dH = G W_lm (W MN-major)
+                mmt(e, st, ts.Gt, kMN, V, hc, kMN, D, V, D, cn, epi(EPI_ADD_F32, lm.grad, D));
+                mmt(e, st, ts.Gt, kK, V, m.lm_head, kMN, D, cn, D, V, epi(EPI_STORE_F32, ts.dhf_c, D));
                 train::scatter_rows_f<<<cn, 128, 0, st>>>(ts.dhf_c, d_map + c0, cn, D, d_hf);
             }
         } else {
@@ -540,52 +511,50 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
 
         // ------------------------------------------------------- backward
         float* dx = ts.dx;
+        T* dxc = static_cast<T*>(ts.dxc);  // dx rounded to T: the next GEMMs' operand
         OPPO_CUDA_CHECK(cudaMemsetAsync(dx, 0, static_cast<size_t>(Tr) * D * 4, st));
-        train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(x, m.final_norm, d_hf, Tr, D, kEps, dx, ts.gscr);
+        train::rms_bwd<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, m.final_norm, d_hf, Tr, D, kEps, dx, ts.gscr, dxc);
         colsum_into(ts, ts.gscr, Tr, D, mt.final_norm.grad, st);
-        T* dxc = static_cast<T*>(ts.dxc);
+        T* dgu = static_cast<T*>(ts.dgu);
         for (int l = Lyr - 1; l >= 0; --l) {
             auto& Lw = m.layers[l];
             auto& Lt = mt.layers[l];
             T* qkv = static_cast<T*>(ts.qkv[l]);
-            T* o = static_cast<T*>(ts.o[l]);
-            T* gu = static_cast<T*>(ts.gu[l]);
-            // down projection + SwiGLU
-            cvt_t<T>(dx, Tr, D, Tp, dxc, ts.dxT, st);
-            train::swiglu_t<T><<<dim3(cdiv(F, 32), cdiv(Tp, 32)), kTile, 0, st>>>(gu, Tr, F, Tp, static_cast<T*>(ts.bT));
-            mm(e, st, ts.dxT, D, Tp, ts.bT, F, epi(EPI_ADD_F32, Lt.wdown.grad, F));
-            mm(e, st, dxc, Tr, D, Lt.wdown.wT, F, epi(EPI_STORE_F32, ts.dff, F));
-            train::swiglu_bwd_t<T><<<dim3(cdiv(F, 32), cdiv(Tp, 32)), kTile, 0, st>>>(
-                gu, ts.dff, Tr, F, Tp, static_cast<T*>(ts.dgu), static_cast<T*>(ts.aT));
-            norm_t<T>(ts.x_mid[l], ts.rstd2[l], Lw.ln2, Tr, D, Tp, ts.bT, st);
-            mm(e, st, ts.aT, 2 * F, Tp, ts.bT, D, epi(EPI_ADD_F32, Lt.wgu.grad, D));
-            mm(e, st, ts.dgu, Tr, 2 * F, Lt.wgu.wT, D, epi(EPI_STORE_F32, ts.dh, D));
-            train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_mid[l], Lw.ln2, ts.dh, Tr, D, kEps, dx, ts.gscr);
+            // down projection (x += ff Wd^T, Wd [D][F]) and SwiGLU: the dgrad
+            // GEMM's epilogue turns d ff into d(gate, up) from the saved pre-activations
+            mmt(e, st, dxc, kMN, D, ts.ff[l], kMN, F, D, F, Tr, epi(EPI_ADD_F32, Lt.wdown.grad, F));
+            EpiParams es = epi(EPI_SWIGLU_BWD, dgu, 2 * F);
+            es.aux = ts.gu[l];
+            mmt(e, st, dxc, kK, D, Lw.wdown, kMN, F, Tr, F, D, es);
+            // gate|up projection (gu = h2 Wgu^T, Wgu [2F][D])
+            mmt(e, st, dgu, kMN, 2 * F, ts.h2[l], kMN, D, 2 * F, D, Tr, epi(EPI_ADD_F32, Lt.wgu.grad, D));
+            mmt(e, st, dgu, kK, 2 * F, Lw.wgu, kMN, D, Tr, D, 2 * F, epi(EPI_STORE_F32, ts.dh, D));
+            train::rms_bwd<T><<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_mid[l], Lw.ln2, ts.dh, Tr, D, kEps, dx, ts.gscr, dxc);
             colsum_into(ts, ts.gscr, Tr, D, Lt.ln2.grad, st);
-            // O projection + attention
-            cvt_t<T>(dx, Tr, D, Tp, dxc, ts.dxT, st);
-            transpose<T>(o, Tr, qw, Tp, ts.bT, st);
-            mm(e, st, ts.dxT, D, Tp, ts.bT, qw, epi(EPI_ADD_F32, Lt.wo.grad, qw));
+            // O projection (x += o Wo^T, Wo [D][qw]) + attention
+            mmt(e, st, dxc, kMN, D, ts.o[l], kMN, qw, D, qw, Tr, epi(EPI_ADD_F32, Lt.wo.grad, qw));
             T* dO = static_cast<T*>(ts.dO);
-            mm(e, st, dxc, Tr, D, Lt.wo.wT, qw, epi(EPI_STORE, dO, qw));
-            train::attn_dvec<T><<<cdiv(static_cast<int64_t>(Tr) * H * 32, 256), 256, 0, st>>>(dO, o, Tr, H, hd, ts.dvec);
+            mmt(e, st, dxc, kK, D, Lw.wo, kMN, qw, Tr, qw, D, epi(EPI_STORE, dO, qw));
+            train::attn_dvec<T><<<cdiv(static_cast<int64_t>(Tr) * H * 32, 256), 256, 0, st>>>(
+                dO, static_cast<const T*>(ts.o[l]), Tr, H, hd, ts.dvec);
             attn<T>(hd, 1, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
             attn<T>(hd, 2, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
             train::rope_rows<float><<<Tr, 128, 0, st>>>(ts.dqkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 1);
             colsum_into(ts, ts.dqkv, Tr, qkvw, Lt.bqkv.grad, st);
             T* dqc = static_cast<T*>(ts.dqkvc);
-            cvt_t<T>(ts.dqkv, Tr, qkvw, Tp, dqc, ts.aT, st);
-            norm_t<T>(ts.x_in[l], ts.rstd1[l], Lw.ln1, Tr, D, Tp, ts.bT, st);
-            mm(e, st, ts.aT, qkvw, Tp, ts.bT, D, epi(EPI_ADD_F32, Lt.wqkv.grad, D));
-            mm(e, st, dqc, Tr, qkvw, Lt.wqkv.wT, D, epi(EPI_STORE_F32, ts.dh, D));
-            train::rms_bwd<<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_in[l], Lw.ln1, ts.dh, Tr, D, kEps, dx, ts.gscr);
+            cvt_f32<T>(ts.dqkv, dqc, static_cast<int64_t>(Tr) * qkvw, st);
+            // q|k|v projection (qkv = h1 Wqkv^T + b, Wqkv [qkv][D])
+            mmt(e, st, dqc, kMN, qkvw, ts.h1[l], kMN, D, qkvw, D, Tr, epi(EPI_ADD_F32, Lt.wqkv.grad, D));
+            mmt(e, st, dqc, kK, qkvw, Lw.wqkv, kMN, D, Tr, D, qkvw, epi(EPI_STORE_F32, ts.dh, D));
+            train::rms_bwd<T><<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_in[l], Lw.ln1, ts.dh, Tr, D, kEps, dx, ts.gscr,
+                                                            l > 0 ? dxc : static_cast<T*>(nullptr));
             colsum_into(ts, ts.gscr, Tr, D, Lt.ln1.grad, st);
         }
         train::embed_grad_csr<<<static_cast<int>(uniq.size()), 128, 0, st>>>(dx, d_uniq, d_start, d_order, D,
                                                                               mt.embed.grad);
         OPPO_CUDA_CHECK(cudaGetLastError());
         OPPO_CUDA_CHECK(cudaStreamSynchronize(st));  // host2 (pageable, local) has been read
-        e.launches += 40 * Lyr + 20;
+        e.launches += 26 * Lyr + 20;
         s0 = s1;
     }
 }

@@ -308,32 +308,14 @@ __global__ void __launch_bounds__(256) attn_train_dkv(const TBlk* __restrict__ b
     }
 }
 
-// ----------------------------------------------------------------- SwiGLU
-// gu [rows, 2F] interleaved (gate_i, up_i) -> ff [rows, F] = silu(g) * u
-template <class T>
-__global__ void swiglu_fwd(const T* __restrict__ gu, T* __restrict__ ff, int64_t n /* rows*F */) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const float g = tof(gu[2 * i]), u = tof(gu[2 * i + 1]);
-    ff[i] = fromf<T>(g / (1.f + __expf(-g)) * u);
-}
-// d(gu) from d(ff) (fp32)
-template <class T>
-__global__ void swiglu_bwd(const T* __restrict__ gu, const float* __restrict__ dff, T* __restrict__ dgu,
-                           int64_t n) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const float g = tof(gu[2 * i]), u = tof(gu[2 * i + 1]), d = dff[i];
-    const float sg = 1.f / (1.f + __expf(-g));
-    dgu[2 * i] = fromf<T>(d * u * sg * (1.f + g * (1.f - sg)));
-    dgu[2 * i + 1] = fromf<T>(d * g * sg);
-}
-
 // --------------------------------------------------------------- RMSNorm
 // y = x * r * g, r = rsqrt(mean(x^2) + eps): dx += r * (dy*g - xh * mean(dy*g*xh)),
-// gscr[row] = dy * xh (the gamma gradient's per-row terms).  One warp per row.
-static __global__ void rms_bwd(const float* __restrict__ x, const float* __restrict__ g, const float* __restrict__ dy,
-                        int rows, int d, float eps, float* __restrict__ dx, float* __restrict__ gscr) {
+// gscr[row] = dy * xh (the gamma gradient's per-row terms), and dxc (if set) =
+// the updated dx rounded to T (the next dgrad / wgrad GEMM operand).  One warp per row.
+template <class T>
+__global__ void rms_bwd(const float* __restrict__ x, const float* __restrict__ g, const float* __restrict__ dy,
+                        int rows, int d, float eps, float* __restrict__ dx, float* __restrict__ gscr,
+                        T* __restrict__ dxc) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= rows) return;
     const float* xr = x + static_cast<size_t>(w) * d;
@@ -347,9 +329,12 @@ static __global__ void rms_bwd(const float* __restrict__ x, const float* __restr
     dot = warp_sum(dot) / d;
     float* o = dx + static_cast<size_t>(w) * d;
     float* gs = gscr + static_cast<size_t>(w) * d;
+    T* oc = dxc ? dxc + static_cast<size_t>(w) * d : nullptr;
     for (int c = lane; c < d; c += 32) {
         const float xh = xr[c] * r;
-        o[c] += r * (dr[c] * g[c] - xh * dot);
+        const float v = o[c] + r * (dr[c] * g[c] - xh * dot);
+        o[c] = v;
+        if (oc) oc[c] = fromf<T>(v);
         gs[c] = dr[c] * xh;
     }
 }
@@ -375,23 +360,6 @@ static __global__ void colsum_final(const float* __restrict__ part, int chunks, 
 }
 
 // ----------------------------------------------------------------- misc
-// out[c][r] = in[r][c] (rows padded to ld_out with zeros), with conversion
-template <class S, class D>
-__global__ void transpose_cvt(const S* __restrict__ in, int rows, int cols, int ld_in, int ld_out,
-                              D* __restrict__ out) {
-    __shared__ float tile[32][33];
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int r = r0 + i, c = c0 + threadIdx.x;
-        tile[i][threadIdx.x] = (r < rows && c < cols) ? tof(in[static_cast<size_t>(r) * ld_in + c]) : 0.f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int c = c0 + i, r = r0 + threadIdx.x;
-        if (c < cols && r < ld_out) out[static_cast<size_t>(c) * ld_out + r] = fromf<D>(tile[threadIdx.x][i]);
-    }
-}
-
 // Embedding gradient, deterministic: one CTA per distinct token u of the
 // micro-batch sums its rows (CSR: rows[start[u] .. start[u+1]), ascending) in
 // a fixed order, then g[uniq[u]] += sum.
@@ -477,29 +445,6 @@ static __global__ void sum_to_double(const float* __restrict__ x, int n, double*
 }
 
 // ----------------------------------------------------- fused backward glue
-// The wgrad GEMMs reduce over tokens, so their operands are needed
-// feature-major ([features][tokens], tokens padded to ldT with zeros); these
-// kernels produce them straight from the producers' inputs through a 32x32
-// shared-memory tile (coalesced reads and writes), fusing the elementwise op.
-
-// (gate, up) pair of an interleaved gu row, one 4- / 8-byte access
-__device__ __forceinline__ void load_pair(const __nv_bfloat16* p, float& a, float& b) {
-    const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(p);
-    a = __low2float(v);
-    b = __high2float(v);
-}
-__device__ __forceinline__ void load_pair(const float* p, float& a, float& b) {
-    const float2 v = *reinterpret_cast<const float2*>(p);
-    a = v.x;
-    b = v.y;
-}
-__device__ __forceinline__ void store_pair(__nv_bfloat16* p, float a, float b) {
-    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
-}
-__device__ __forceinline__ void store_pair(float* p, float a, float b) {
-    *reinterpret_cast<float2*>(p) = make_float2(a, b);
-}
-
 // Training forward RMSNorm: out = x * r * g (T), rstd[row] = r.  One warp per row.
 template <class T>
 __global__ void rms_fwd_train(const float* __restrict__ x, const float* __restrict__ g, int rows, int d, float eps,
@@ -514,110 +459,6 @@ __global__ void rms_fwd_train(const float* __restrict__ x, const float* __restri
     T* o = out + static_cast<size_t>(w) * d;
     for (int c = lane; c < d; c += 32) o[c] = fromf<T>(xr[c] * r * g[c]);
     if (lane == 0) rstd[w] = r;
-}
-
-// hT[c][r] = round(x[r][c] * rstd[r] * g[c]) (the normed rows, feature-major)
-template <class T>
-__global__ void norm_t(const float* __restrict__ x, const float* __restrict__ rstd, const float* __restrict__ g,
-                       int rows, int d, int ldT, T* __restrict__ hT) {
-    __shared__ float tile[32][33];
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int r = r0 + i, c = c0 + threadIdx.x;
-        tile[i][threadIdx.x] = (r < rows && c < d) ? tof(fromf<T>(x[static_cast<size_t>(r) * d + c] * rstd[r] * g[c])) : 0.f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int c = c0 + i, r = r0 + threadIdx.x;
-        if (c < d && r < ldT) hT[static_cast<size_t>(c) * ldT + r] = fromf<T>(tile[threadIdx.x][i]);
-    }
-}
-
-// fp32 [rows][cols] -> T row-major copy + T feature-major copy (the dgrad and
-// wgrad operands of a gradient)
-template <class T>
-__global__ void cvt_t(const float* __restrict__ x, int rows, int cols, int ldT, T* __restrict__ y,
-                      T* __restrict__ yT) {
-    __shared__ float tile[32][33];
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int r = r0 + i, c = c0 + threadIdx.x;
-        float v = 0.f;
-        if (r < rows && c < cols) {
-            v = x[static_cast<size_t>(r) * cols + c];
-            y[static_cast<size_t>(r) * cols + c] = fromf<T>(v);
-        }
-        tile[i][threadIdx.x] = v;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int c = c0 + i, r = r0 + threadIdx.x;
-        if (c < cols && r < ldT) yT[static_cast<size_t>(c) * ldT + r] = fromf<T>(tile[threadIdx.x][i]);
-    }
-}
-
-// ffT[f][r] = silu(g) * u of gu[r][(2f, 2f+1)] (SwiGLU recomputed, feature-major)
-template <class T>
-__global__ void swiglu_t(const T* __restrict__ gu, int rows, int F, int ldT, T* __restrict__ ffT) {
-    __shared__ float tile[32][33];
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int r = r0 + i, c = c0 + threadIdx.x;
-        float v = 0.f;
-        if (r < rows && c < F) {
-            float gg, uu;
-            load_pair(gu + static_cast<size_t>(r) * 2 * F + 2 * c, gg, uu);
-            v = tof(fromf<T>(gg / (1.f + __expf(-gg)) * uu));
-        }
-        tile[i][threadIdx.x] = v;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int c = c0 + i, r = r0 + threadIdx.x;
-        if (c < F && r < ldT) ffT[static_cast<size_t>(c) * ldT + r] = fromf<T>(tile[threadIdx.x][i]);
-    }
-}
-
-// SwiGLU backward: dgu[r][2f], dgu[r][2f+1] from dff[r][f] (fp32) and gu,
-// written row-major (the dgrad operand) and feature-major (the wgrad operand).
-template <class T>
-__global__ void swiglu_bwd_t(const T* __restrict__ gu, const float* __restrict__ dff, int rows, int F, int ldT,
-                             T* __restrict__ dgu, T* __restrict__ dguT) {
-    __shared__ float tile[32][65];
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;  // c: ff column
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int r = r0 + i, c = c0 + threadIdx.x;
-        float a = 0.f, b = 0.f;
-        if (r < rows && c < F) {
-            const size_t o = static_cast<size_t>(r) * 2 * F + 2 * c;
-            float gg, uu;
-            load_pair(gu + o, gg, uu);
-            const float d = dff[static_cast<size_t>(r) * F + c];
-            const float sg = 1.f / (1.f + __expf(-gg));
-            a = d * uu * sg * (1.f + gg * (1.f - sg));
-            b = d * gg * sg;
-            store_pair(dgu + o, a, b);
-        }
-        tile[i][2 * threadIdx.x] = a;
-        tile[i][2 * threadIdx.x + 1] = b;
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 64; i += blockDim.y) {  // 64 gu columns x 32 rows
-        const int c = 2 * c0 + i, r = r0 + threadIdx.x;
-        if (c < 2 * F && r < ldT) dguT[static_cast<size_t>(c) * ldT + r] = fromf<T>(tile[threadIdx.x][i]);
-    }
-}
-
-// SwiGLU forward, 4 outputs per thread (gu interleaved pairs)
-template <class T>
-__global__ void swiglu_fwd4(const T* __restrict__ gu, T* __restrict__ ff, int64_t n /* rows*F, multiple of 4 */) {
-    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4;
-    if (i >= n) return;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float g = tof(gu[2 * (i + k)]), u = tof(gu[2 * (i + k) + 1]);
-        ff[i + k] = fromf<T>(g / (1.f + __expf(-g)) * u);
-    }
 }
 
 }  // namespace train

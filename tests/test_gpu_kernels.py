@@ -54,6 +54,35 @@ def test_gemm_bf16_tcgen05_vs_torch(M, N, K):
     assert err <= tol, (err, tol)
 
 
+@pytest.mark.parametrize("dtype", [1, 0])
+@pytest.mark.parametrize("a_mn,b_mn", [(1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(896, 896, 1000), (1152, 4864, 640), (200, 136, 64), (4096, 896, 336)])
+def test_gemm_mn_major_operands(dtype, a_mn, b_mn, M, N, K):
+    """Operands read in place from their transposed storage (the update's
+    wgrad dW = dY^T X with both MN-major over the token dimension, and dgrad
+    dX = dY W with W MN-major): bit-identical to the K-major kernel on
+    explicitly transposed copies (same tiles, same K order), and vs torch."""
+    if dtype == 0 and M * N * K > 2e8:
+        pytest.skip("SIMT path: small shapes only")
+    tdt = torch.bfloat16 if dtype == 1 else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + 7 * K + a_mn + 2 * b_mn)
+    a = torch.randn(M, K, device="cuda", generator=g).to(tdt)          # logical A [M][K]
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(tdt)  # logical B [N][K]
+    a_st = a.t().contiguous() if a_mn else a  # stored [K][M] when MN-major
+    b_st = b.t().contiguous() if b_mn else b
+    y = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    st = _lib().oppo_k_gemm_t(dtype, M, N, K, _ptr(a_st), a_mn, M if a_mn else K, _ptr(b_st), b_mn,
+                              N if b_mn else K, _ptr(y), EPI_STORE_F32, _stream())
+    assert st == 0, _lib().oppo_last_error_global()
+    y_k = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    assert _lib().oppo_k_gemm_t(dtype, M, N, K, _ptr(a), 0, K, _ptr(b), 0, K, _ptr(y_k), EPI_STORE_F32,
+                                _stream()) == 0
+    assert torch.equal(y, y_k)
+    ref = a.double() @ b.double().T
+    rel = ((y.double() - ref).abs().max() / ref.abs().max()).item()
+    assert rel < 2e-4, rel
+
+
 def test_gemm_bf16_store_f32_long_k():
     # fp32 output isolates the tensor-core fp32 accumulation error over a long K
     M, N, K = 32, 256, 8192

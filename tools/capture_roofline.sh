@@ -1,0 +1,30 @@
+#!/bin/bash
+# Roofline evidence for bench.py (run under gpurun, one GPU):
+#  * ncu DRAM traffic of one actor decode iteration of the CURRENT build for
+#    each bench actor shape at 64 / 128 / 256 rows (tools/decode_iter.py,
+#    6 iterations per row count) -> profiles/r02_decode_traffic_<shape>_M<rows>.json
+#  * ncu time + DRAM bytes of the per-token PPO kernels of one update at the
+#    cfg2 shape -> profiles/r02_ppo_kernels.json
+# ncu numbers are serialised and cache-flushed per kernel: shares and bytes,
+# never bench values.
+set -u
+OUT=gpurun_out/roof
+mkdir -p $OUT
+PEAK=$(python -c "import json;print(json.load(open('MEASURED_PEAKS.json'))['hbm_gbs'])" 2>/dev/null || echo 6650)
+MET=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+for SHAPE in ${SHAPES:-0.5b 1.5b}; do
+  for M in ${ROWS:-64 128 256}; do
+    tag=${SHAPE}_M${M}
+    SHAPE=$SHAPE MS=$M L=6 timeout 900 ncu --metrics $MET --clock-control none --csv \
+      --log-file $OUT/dec_$tag.csv python tools/decode_iter.py > $OUT/dec_$tag.log 2>&1
+    alg=$(grep -o "alg_bytes_per_iteration [0-9]*" $OUT/dec_$tag.log | tail -1 | awk '{print $2}')
+    python tools/iter_traffic.py $OUT/dec_$tag.csv \
+      "ncu --metrics $MET --clock-control none (caches flushed per kernel); tools/decode_iter.py SHAPE=$SHAPE M=$M L=6 (prompt 128, ctx 129-134), bf16, 148 SMs; parsed by tools/iter_traffic.py" \
+      ${alg:-0} > $OUT/r02_decode_traffic_$tag.json
+  done
+done
+timeout 900 ncu --profile-from-start off --kernel-name regex:"token_rewards|gae_scan|mc_returns|moments|ppo_clip" \
+  --metrics $MET --clock-control none --csv --log-file $OUT/ppo.csv python tools/update_profile.py > $OUT/ppo.log 2>&1
+tok=$(grep -o "^update_us [0-9.]* tokens [0-9]*" $OUT/ppo.log | awk '{print $4}')
+python tools/ppo_kernels.py $OUT/ppo.csv ${tok:-0} $PEAK > $OUT/r02_ppo_kernels.json
+ls -la $OUT

@@ -13,7 +13,8 @@ from paper_2509_25762_b200.engine import Engine, SHAPES
 
 Ms = [int(x) for x in os.environ.get("MS", "16,64,128,256").split(",")]
 L, P = int(os.environ.get("L", "48")), 128
-shape = dict(SHAPES["0.5b"])
+SHAPE = os.environ.get("SHAPE", "0.5b")
+shape = dict(SHAPES[SHAPE])
 eng = Engine(shape, shape, shape, shape, dtype=abi.DTYPE_BF16, max_slots=max(Ms) + 8, max_prompt_len=P,
              max_response_len=L, train_heads=0, carry=abi.CARRY_TOKEN,
              use_graphs=int(os.environ.get("GRAPHS", "1")))
@@ -28,6 +29,7 @@ for M in Ms:
     per = led.decode_loop_us / L
     gbs = (led.decode_weight_bytes + led.decode_kv_bytes) / (led.decode_loop_us * 1e-6) / 1e9
     print(f"M={M:4d} decode iteration {per:8.1f} us  alg {gbs:7.1f} GB/s  "
+          f"alg_bytes_per_iteration {(led.decode_weight_bytes + led.decode_kv_bytes) / L:.0f}  "
           f"(weights {led.decode_weight_bytes / L / 1e6:.0f} MB + KV {led.decode_kv_bytes / L / 1e6:.1f} MB "
           f"per iteration)", flush=True)
 eng.close()

@@ -38,4 +38,7 @@ out = {"iterations": len(wins), "kernels_per_iteration": mode,
        "serialized_kernel_us_per_iteration": round(sum(us) / len(us), 1),
        "dram_bytes_by_kernel": {k: round(v) for k, v in sorted(by.items(), key=lambda kv: -kv[1])},
        "source": sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]}
+if len(sys.argv) > 3:  # algorithmic bytes of one iteration of the captured run (decode_iter.py)
+    out["algorithmic_bytes_per_iteration"] = round(float(sys.argv[3]))
+    out["traffic_over_algorithmic"] = round(out["dram_bytes_per_iteration"] / float(sys.argv[3]), 3)
 print(json.dumps(out, indent=1))
