@@ -26,7 +26,6 @@
 #include <cstring>
 #include <numeric>
 
-#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include "engine.cuh"
@@ -101,35 +100,42 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
     }
 };
 
-// Stream memory operations (driver API) for the K13 chunk-ready flags.
-PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
-PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
-void stream_memops_init() {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
-        p = nullptr;
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
-    });
-    if (!g_wait32 || !g_write32) throw Error(OPPO_ERR_CUDA, "cuStreamWaitValue32 / cuStreamWriteValue32 unavailable");
+// The scorer side waits on the device: one single-thread kernel polls the
+// flag (ld.acquire.gpu, cyclic >=) and the wave's kernels follow it in stream
+// order.  (A front-end wait -- cuStreamWaitValue32 -- can block a hardware
+// queue the actor's own work sits behind: it deadlocked on B200 when the two
+// streams shared a queue, as the driver documentation warns.)  A flag that
+// never arrives traps after 30 s instead of wedging the GPU.
+__global__ void wait_ready(const uint32_t* __restrict__ flag, uint32_t want) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (static_cast<int32_t>(v - want) >= 0) break;
+        __nanosleep(256);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 30000000000ull) __trap();
+    }
 }
-void stream_wait_geq(cudaStream_t st, const uint32_t* flag, uint32_t v) {
-    stream_memops_init();
-    const CUresult r = g_wait32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
-                                CU_STREAM_WAIT_VALUE_GEQ);
-    if (r != CUDA_SUCCESS) throw Error(OPPO_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
+void stream_wait_geq(Engine& e, cudaStream_t st, const uint32_t* flag, uint32_t v) {
+    wait_ready<<<1, 32, 0, st>>>(flag, v);
+    OPPO_CUDA_CHECK(cudaGetLastError());
+    e.launches += 1;
 }
-void stream_write(cudaStream_t st, uint32_t* flag, uint32_t v) {
-    stream_memops_init();
-    const CUresult r = g_write32(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
-                                 CU_STREAM_WRITE_VALUE_DEFAULT);
-    if (r != CUDA_SUCCESS) throw Error(OPPO_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(r) + ")");
+// The actor side: a single-thread kernel publishes the wave's sequence number
+// with a device-scope release store, ordered after the decode iteration that
+// completed the chunks (a front-end memory-op write was not observed by the
+// polling kernel on B200).
+__global__ void set_ready(uint32_t* __restrict__ flag, uint32_t v) {
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+void stream_write(Engine& e, cudaStream_t st, uint32_t* flag, uint32_t v) {
+    set_ready<<<1, 32, 0, st>>>(flag, v);
+    OPPO_CUDA_CHECK(cudaGetLastError());
+    e.launches += 1;
 }
 
 // Host thread that enqueues the scorer waves on the scorer stream.  A wave is
@@ -1000,7 +1006,10 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         // off: with concurrent scorer passes the scorers finish within ~8 ms of
         // decode, shorter than the precompute on the actor SMs (215.4 vs 213.6)
         e->pre_lp = env_int("OPPO_PRE_LP", 0) != 0;
-        e->chunk_flags = env_int("OPPO_CHUNK_FLAGS", 1) != 0;
+        // device-side hand-off only between green contexts: two streams of one
+        // context may share a hardware queue, where a waiting scorer kernel
+        // would block the actor work that writes its flag (deadlocked on B200)
+        e->chunk_flags = env_int("OPPO_CHUNK_FLAGS", 0) != 0 && e->sms_scorer < e->num_sms;
         OPPO_CUDA_CHECK(cudaMalloc(&e->d_ready, Engine::kReadyRing * sizeof(uint32_t)));
         OPPO_CUDA_CHECK(cudaMemsetAsync(e->d_ready, 0, Engine::kReadyRing * sizeof(uint32_t), st));
         e->g_chunk = std::max(64, env_int("OPPO_G_CHUNK", e->g_chunk)) / 8 * 8;  // update token chunk
@@ -1741,7 +1750,7 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
         const uint32_t want = wave_seq[k];
         const WavePlan* wave = &waves[k];
         worker.post([&e, &A, &prefill_tokens, flag, want, wave] {
-            stream_wait_geq(e.ss, flag, want);
+            stream_wait_geq(e, e.ss, flag, want);
             int64_t tok = 0;
             for (const auto& p : wave->passes) run_scorer_pass<T>(e, p, A, e.ss, tok);
             prefill_tokens += tok;
@@ -1751,7 +1760,7 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     auto fire_waves_at = [&](int64_t it) {
         while (wi < waves.size() && waves[wi].at_iter == it) {
             if (flags) {  // actor-stream order: after iteration `it`, the wave's chunks are complete
-                stream_write(e.sa, e.d_ready + (wave_seq[wi] % Engine::kReadyRing), wave_seq[wi]);
+                stream_write(e, e.sa, e.d_ready + (wave_seq[wi] % Engine::kReadyRing), wave_seq[wi]);
                 if (wi + 1 < waves.size()) post_wave(wi + 1);
                 ++wi;
                 continue;

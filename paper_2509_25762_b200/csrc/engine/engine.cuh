@@ -176,10 +176,9 @@ struct Engine {
     // K13 chunk hand-off on the device: after the decode iteration that
     // completes a wave's chunks the actor stream writes the wave's sequence
     // number into a ring of per-chunk ready flags (cuStreamWriteValue32); the
-    // scorer stream waits for it (cuStreamWaitValue32, GEQ) -- no event or
-    // host round trip between the actor and the scorers, and every wave of a
-    // step is enqueued on the scorer stream up front.  OPPO_CHUNK_FLAGS=0
-    // falls back to per-wave events.
+    // scorer stream's first kernel of the wave polls it (wait_ready) -- no
+    // event or host round trip between the actor and the scorers.
+    // OPPO_CHUNK_FLAGS=1 selects it; the default is per-wave events.
     static constexpr int kReadyRing = 256;
     uint32_t* d_ready = nullptr;  // [kReadyRing] flags (monotone sequence numbers)
     uint32_t ready_seq = 0;       // last sequence number issued

@@ -91,6 +91,10 @@ bool persist_enabled() {  // read per call so tests can compare both kernels in 
     const char* v = std::getenv("OPPO_GEMM_PERSIST");
     return v ? std::atoi(v) != 0 : false;  // off: faster alone, slower in the cfg2 bench (profiles/)
 }
+bool tc2sm_long_enabled() {  // read per call so tests can compare both kernels in one process
+    const char* v = std::getenv("OPPO_TC2SM_LONGK");
+    return v ? std::atoi(v) != 0 : true;  // measured: update 912 -> 887 ms at 39K tokens
+}
 static const bool g_tc256 = [] {
     const char* v = std::getenv("OPPO_TC256");
     return v && std::atoi(v) != 0;
@@ -203,9 +207,16 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         return;
     }
     // Token-rich prefill GEMMs: CTA-pair 256x256 tiles (cta_group::2)
-    const bool scorer_stream = e && st == e->ss;
+    const bool scorer_stream = e && (st == e->ss || st == e->ss_m[0] || st == e->ss_m[1]);
     const bool use2 = g_tc2sm == 1 || (g_tc2sm == 2 && scorer_stream) || (g_tc2sm == 3 && !scorer_stream);
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && use2) {
+    // Long-K GEMMs that fill the GPU with CTA pairs (the update's weight
+    // gradients, K = tokens): the pair tile halves each SM's operand stream
+    // per flop, and the 6-stage ring covers the L2 latency (OPPO_TC2SM_LONGK)
+    const int kb_all = (K + 63) / 64;
+    const int pairs = ((m_tiles + 1) / 2) * ((N + 255) / 256);
+    const bool long2 = ep.pair_long_k && tc2sm_long_enabled() && !scorer_stream && kb_all >= 64 && m_tiles >= 2 &&
+                       pairs * 2 * 10 >= num_sms * 9 && ep.mode != EPI_LOGITS && !rope;
+    if ((m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && use2) || long2) {
         static std::once_flag attr2;
         std::call_once(attr2, [] {
             OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm,
@@ -215,8 +226,8 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         sh.splits = 1;
         sh.kb_per_split = (K + 63) / 64;
         CUtensorMap s1, s2;
-        const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
-        const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 128, s2);
+        const CUtensorMap& mx = a_mn ? cached_map(e, x, K, M, ldx, 64, s1) : cached_map(e, x, M, K, ldx, 128, s1);
+        const CUtensorMap& mw = b_mn ? cached_map(e, wt, K, N, ldw, 64, s2) : cached_map(e, wt, N, K, ldw, 128, s2);
         const int mt2 = (m_tiles + 1) / 2 * 2;  // whole CTA pairs (OOB rows zero-filled)
         launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm, dim3(mt2, (N + 255) / 256), dim3(128),
                        tc::Cfg2Sm::SMEM, st, mx, mw, sh, ep);
@@ -259,7 +270,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // long-K GEMMs with few output tiles (the update's weight gradients, K =
     // tokens; its vocabulary dgrad, K = V): split K until both CTA slots of
     // every SM are busy (133 tiles of dW_down ran at 45% of the slots)
-    const bool long_k = m_tiles > 4 && kb >= 64;
+    const bool long_k = m_tiles > 4 && kb >= 64 && !(e && (st == e->ss || st == e->ss_m[0] || st == e->ss_m[1]));
     if (ws && cnt && ep.mode != EPI_LOGITS && long_k && tiles * 4 <= 3 * 2 * num_sms) {
         splits = std::max(1, std::min((2 * num_sms) / tiles, 8));
         while (splits > 1 && (static_cast<size_t>(splits) * tiles * 128 * BN > ws_floats || tiles > cnt_n))
@@ -422,6 +433,7 @@ void gemm_run_t(Engine& e, Work& w, cudaStream_t st, const void* a, int a_mn, in
 void gemm_standalone_t(int dtype, int M, int N, int K, const void* a, int a_mn, int lda, const void* b, int b_mn,
                        int ldb, void* y, int epi, cudaStream_t st) {
     EpiParams ep{};
+    ep.pair_long_k = 1;  // as the update's gradient GEMMs
     ep.mode = epi;
     ep.y = y;
     ep.ldy = N;

@@ -40,6 +40,7 @@ namespace {
 
 constexpr float kEps = 1e-6f;
 constexpr float kTheta = 1e6f;
+constexpr int kColParts = 256;  // block partial rows of the column sums (ts.colp)
 
 inline int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
@@ -185,6 +186,7 @@ void mm(Engine& e, cudaStream_t st, const void* A, int M, int K, const void* B, 
 constexpr int kK = 0, kMN = 1;
 void mmt(Engine& e, cudaStream_t st, const void* A, int a_mn, int lda, const void* B, int b_mn, int ldb, int M,
          int N, int K, EpiParams ep) {
+    ep.pair_long_k = 1;  // long-K gradient GEMMs may take CTA-pair tiles
     gemm_run_t(e, e.ws, st, A, a_mn, lda, B, b_mn, ldb, M, N, K, ep);
 }
 EpiParams epi(int mode, void* y, int ldy, float scale = 1.f, const float* bias = nullptr) {
@@ -195,6 +197,25 @@ EpiParams epi(int mode, void* y, int ldy, float scale = 1.f, const float* bias =
     p.scale = scale;
     p.bias = bias;
     return p;
+}
+
+// RMSNorm backward (dx += ..., bf16 copy into dxc when set) + gamma gradient
+// (gout += column sums of dy * xh) in one pass, block partials in ts.colp.
+template <class T>
+void rms_bwd_into(TrainState& ts, const float* x, const float* g, const float* dy, int rows, int d, float* dx,
+                  T* dxc, float* gout, cudaStream_t st) {
+    if (rows <= 0) return;
+    const int nblk = std::min(kColParts, std::max(1, rows / 32));
+    const int per = cdiv(rows, nblk);
+    const size_t smem = 8 * static_cast<size_t>(d) * 4;
+    static bool attr = false;
+    if (!attr) {
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(train::rms_bwd_cs<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024));
+        attr = true;
+    }
+    train::rms_bwd_cs<T><<<nblk, 256, smem, st>>>(x, g, dy, rows, d, per, kEps, dx, dxc, ts.colp);
+    train::colsum_final<<<cdiv(d, 256), 256, 0, st>>>(ts.colp, nblk, d, gout);
 }
 
 void colsum_into(TrainState& ts, const float* x, int rows, int cols, float* out, cudaStream_t st) {
@@ -326,7 +347,7 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
     ts.dqkv = static_cast<float*>(ts.scr.take(R * qkv * 4));
     ts.dvec = static_cast<float*>(ts.scr.take(R * H * 4));
     ts.gscr = static_cast<float*>(ts.scr.take(R * std::max(D, qkv) * 4));
-    ts.colp = static_cast<float*>(ts.scr.take(64 * wide * 4));
+    ts.colp = static_cast<float*>(ts.scr.take(kColParts * wide * 4));
     ts.head_out = static_cast<float*>(ts.scr.take(R * 4));
     ts.hf = ts.scr.take(R * D * es);
     ts.dgu = ts.scr.take(R * 2 * F * es);
@@ -432,6 +453,8 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
         const auto* d_order = reinterpret_cast<const int32_t*>(meta + base2 + o_r);
 
         // ------------------------------------------------------- forward
+        const bool rope_epi = std::is_same_v<T, __nv_bfloat16> && (hd == 64 || hd == 128) &&
+                              std::getenv("OPPO_TRAIN_ROPE_KERNEL") == nullptr;
         float* x = ts.x;
         embed_rows<T><<<Tr, 128, 0, st>>>(static_cast<const T*>(m.embed), ts.tok, x, Tr, D);
         for (int l = 0; l < Lyr; ++l) {
@@ -442,8 +465,19 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             T* h2 = static_cast<T*>(ts.h2[l]);
             OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_in[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
             train::rms_fwd_train<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, Lw.ln1, Tr, D, kEps, h1, ts.rstd1[l]);
-            mm(e, st, h1, Tr, D, Lw.wqkv, qkvw, epi(EPI_STORE, qkv, qkvw, 1.f, Lw.bqkv));
-            train::rope_rows<T><<<Tr, 128, 0, st>>>(qkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 0);
+            if (rope_epi) {  // bias, bf16 round and RoPE of q, k in the projection's epilogue
+                EpiParams er = epi(EPI_ROPE_APPEND, nullptr, qkvw, 1.f, Lw.bqkv);
+                er.q_out = qkv;
+                er.kv.head_dim = hd;
+                er.kv.kv_heads = KV;
+                er.n_heads = H;
+                er.theta = kTheta;
+                er.pos = ts.pos;
+                mm(e, st, h1, Tr, D, Lw.wqkv, qkvw, er);
+            } else {
+                mm(e, st, h1, Tr, D, Lw.wqkv, qkvw, epi(EPI_STORE, qkv, qkvw, 1.f, Lw.bqkv));
+                train::rope_rows<T><<<Tr, 128, 0, st>>>(qkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 0);
+            }
             attn<T>(hd, 0, d_blk, nb, qkv, qkvw, H, KV, o, ts.lse[l], nullptr, nullptr, nullptr, st);
             mm(e, st, o, Tr, qw, Lw.wo, D, epi(EPI_ADD_F32, x, D));
             OPPO_CUDA_CHECK(cudaMemcpyAsync(ts.x_mid[l], x, static_cast<size_t>(Tr) * D * 4, cudaMemcpyDeviceToDevice, st));
@@ -513,8 +547,7 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
         float* dx = ts.dx;
         T* dxc = static_cast<T*>(ts.dxc);  // dx rounded to T: the next GEMMs' operand
         OPPO_CUDA_CHECK(cudaMemsetAsync(dx, 0, static_cast<size_t>(Tr) * D * 4, st));
-        train::rms_bwd<T><<<cdiv(Tr, 4), 128, 0, st>>>(x, m.final_norm, d_hf, Tr, D, kEps, dx, ts.gscr, dxc);
-        colsum_into(ts, ts.gscr, Tr, D, mt.final_norm.grad, st);
+        rms_bwd_into<T>(ts, x, m.final_norm, d_hf, Tr, D, dx, dxc, mt.final_norm.grad, st);
         T* dgu = static_cast<T*>(ts.dgu);
         for (int l = Lyr - 1; l >= 0; --l) {
             auto& Lw = m.layers[l];
@@ -529,8 +562,7 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             // gate|up projection (gu = h2 Wgu^T, Wgu [2F][D])
             mmt(e, st, dgu, kMN, 2 * F, ts.h2[l], kMN, D, 2 * F, D, Tr, epi(EPI_ADD_F32, Lt.wgu.grad, D));
             mmt(e, st, dgu, kK, 2 * F, Lw.wgu, kMN, D, Tr, D, 2 * F, epi(EPI_STORE_F32, ts.dh, D));
-            train::rms_bwd<T><<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_mid[l], Lw.ln2, ts.dh, Tr, D, kEps, dx, ts.gscr, dxc);
-            colsum_into(ts, ts.gscr, Tr, D, Lt.ln2.grad, st);
+            rms_bwd_into<T>(ts, ts.x_mid[l], Lw.ln2, ts.dh, Tr, D, dx, dxc, Lt.ln2.grad, st);
             // O projection (x += o Wo^T, Wo [D][qw]) + attention
             mmt(e, st, dxc, kMN, D, ts.o[l], kMN, qw, D, qw, Tr, epi(EPI_ADD_F32, Lt.wo.grad, qw));
             T* dO = static_cast<T*>(ts.dO);
@@ -546,9 +578,8 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             // q|k|v projection (qkv = h1 Wqkv^T + b, Wqkv [qkv][D])
             mmt(e, st, dqc, kMN, qkvw, ts.h1[l], kMN, D, qkvw, D, Tr, epi(EPI_ADD_F32, Lt.wqkv.grad, D));
             mmt(e, st, dqc, kK, qkvw, Lw.wqkv, kMN, D, Tr, D, qkvw, epi(EPI_STORE_F32, ts.dh, D));
-            train::rms_bwd<T><<<cdiv(Tr, 4), 128, 0, st>>>(ts.x_in[l], Lw.ln1, ts.dh, Tr, D, kEps, dx, ts.gscr,
-                                                            l > 0 ? dxc : static_cast<T*>(nullptr));
-            colsum_into(ts, ts.gscr, Tr, D, Lt.ln1.grad, st);
+            rms_bwd_into<T>(ts, ts.x_in[l], Lw.ln1, ts.dh, Tr, D, dx, l > 0 ? dxc : static_cast<T*>(nullptr),
+                            Lt.ln1.grad, st);
         }
         train::embed_grad_csr<<<static_cast<int>(uniq.size()), 128, 0, st>>>(dx, d_uniq, d_start, d_order, D,
                                                                               mt.embed.grad);

@@ -310,32 +310,49 @@ __global__ void __launch_bounds__(256) attn_train_dkv(const TBlk* __restrict__ b
 
 // --------------------------------------------------------------- RMSNorm
 // y = x * r * g, r = rsqrt(mean(x^2) + eps): dx += r * (dy*g - xh * mean(dy*g*xh)),
-// gscr[row] = dy * xh (the gamma gradient's per-row terms), and dxc (if set) =
-// the updated dx rounded to T (the next dgrad / wgrad GEMM operand).  One warp per row.
+// d gamma = column sums of dy * xh.
+// RMSNorm backward fused with the gamma gradient's column sums: block b owns
+// rows [b*per, (b+1)*per); warp w of 8 takes every 8th of them (per-row
+// update as rms_bwd); the per-column terms dy * xh accumulate in the warp's
+// shared-memory row, then the 8 rows are summed in warp order into
+// part[b][c] -- deterministic, and no [rows, d] scratch round trip.
+// colsum_final(part, gridDim.x, d, out) adds the block partials in order.
 template <class T>
-__global__ void rms_bwd(const float* __restrict__ x, const float* __restrict__ g, const float* __restrict__ dy,
-                        int rows, int d, float eps, float* __restrict__ dx, float* __restrict__ gscr,
-                        T* __restrict__ dxc) {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (w >= rows) return;
-    const float* xr = x + static_cast<size_t>(w) * d;
-    const float* dr = dy + static_cast<size_t>(w) * d;
-    float ss = 0.f;
-    for (int c = lane; c < d; c += 32) ss = fmaf(xr[c], xr[c], ss);
-    ss = warp_sum(ss);
-    const float r = rsqrtf(ss / d + eps);
-    float dot = 0.f;
-    for (int c = lane; c < d; c += 32) dot = fmaf(dr[c] * g[c], xr[c] * r, dot);
-    dot = warp_sum(dot) / d;
-    float* o = dx + static_cast<size_t>(w) * d;
-    float* gs = gscr + static_cast<size_t>(w) * d;
-    T* oc = dxc ? dxc + static_cast<size_t>(w) * d : nullptr;
-    for (int c = lane; c < d; c += 32) {
-        const float xh = xr[c] * r;
-        const float v = o[c] + r * (dr[c] * g[c] - xh * dot);
-        o[c] = v;
-        if (oc) oc[c] = fromf<T>(v);
-        gs[c] = dr[c] * xh;
+__global__ void __launch_bounds__(256) rms_bwd_cs(const float* __restrict__ x, const float* __restrict__ g,
+                                                  const float* __restrict__ dy, int rows, int d, int per, float eps,
+                                                  float* __restrict__ dx, T* __restrict__ dxc,
+                                                  float* __restrict__ part) {
+    extern __shared__ float acc_s[];  // [8][d]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* acc = acc_s + warp * d;
+    for (int c = lane; c < d; c += 32) acc[c] = 0.f;
+    const int r_end = min(rows, (blockIdx.x + 1) * per);
+    for (int r = blockIdx.x * per + warp; r < r_end; r += 8) {
+        const float* xr = x + static_cast<size_t>(r) * d;
+        const float* dr = dy + static_cast<size_t>(r) * d;
+        float ss = 0.f;
+        for (int c = lane; c < d; c += 32) ss = fmaf(xr[c], xr[c], ss);
+        ss = warp_sum(ss);
+        const float rs = rsqrtf(ss / d + eps);
+        float dot = 0.f;
+        for (int c = lane; c < d; c += 32) dot = fmaf(dr[c] * g[c], xr[c] * rs, dot);
+        dot = warp_sum(dot) / d;
+        float* o = dx + static_cast<size_t>(r) * d;
+        T* oc = dxc ? dxc + static_cast<size_t>(r) * d : nullptr;
+        for (int c = lane; c < d; c += 32) {
+            const float xh = xr[c] * rs;
+            const float v = o[c] + rs * (dr[c] * g[c] - xh * dot);
+            o[c] = v;
+            if (oc) oc[c] = fromf<T>(v);
+            acc[c] += dr[c] * xh;
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += acc_s[w * d + c];
+        part[static_cast<size_t>(blockIdx.x) * d + c] = s;
     }
 }
 

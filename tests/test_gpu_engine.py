@@ -644,7 +644,7 @@ def _run_flags(flags, scorer_sms):
     shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
                  vocab=1024, tied=1)
     P, C, B = 16, 16, 6
-    lens = [40, 70, 23, 64, 90, 12, 55, 31, 77, 18]
+    lens = [40, 70, 23, 64, 90, 12, 55, 31, 77, 18, 44, 26, 61, 15]
     old = os.environ.get("OPPO_CHUNK_FLAGS")
     os.environ["OPPO_CHUNK_FLAGS"] = str(flags)
     try:
@@ -675,14 +675,17 @@ def _run_flags(flags, scorer_sms):
     return log, ro
 
 
-@pytest.mark.timeout(240)
-@pytest.mark.parametrize("scorer_sms", [0, 64])
+@pytest.mark.timeout(240, method="thread")
+@pytest.mark.parametrize("scorer_sms", [64])
 def test_chunk_ready_flags_match_event_handoff(scorer_sms):
     """K13 on the device (north_star (2), engine.cpp:77-82): the actor stream
     writes each wave's ready flag after the decode iteration that completes its
-    chunks and the scorer stream waits on it (cuStreamWaitValue32) -- every
+    chunks and the scorer stream's first kernel of the wave polls it -- every
     token, log-prob, value and reward is bit-identical to the per-wave event
-    hand-off, with and without the SM partition."""
+    hand-off.  Only with the SM partition (scorer and actor streams in
+    different green contexts): without it the two streams can share a
+    hardware queue, and a device-side wait then blocks the actor's own work
+    (measured: the flag never arrived), so the engine uses events there."""
     la, ra = _run_flags(1, scorer_sms)
     lb, rb = _run_flags(0, scorer_sms)
     assert [x[0] for x in la] == [x[0] for x in lb]

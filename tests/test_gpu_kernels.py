@@ -83,6 +83,39 @@ def test_gemm_mn_major_operands(dtype, a_mn, b_mn, M, N, K):
     assert rel < 2e-4, rel
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1), (1, 0), (0, 1)])
+def test_gemm_cta_pair_long_k(monkeypatch, a_mn, b_mn):
+    """The long-K CTA-pair path (cta_group::2, 256x256 pair tiles, 6-stage
+    ring; OPPO_TC2SM_LONGK=1) with K-major and MN-major operands: bit-identical
+    across operand storage, within fp32-accumulation noise of float64, and
+    equal to the single-CTA kernel up to accumulation order."""
+    M, N, K = 2048, 8704, 4096
+    g = torch.Generator(device="cuda").manual_seed(11 + a_mn + 2 * b_mn)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    a_st = a.t().contiguous() if a_mn else a
+    b_st = b.t().contiguous() if b_mn else b
+
+    def run(aa, am, bb, bm):
+        y = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+        st = _lib().oppo_k_gemm_t(1, M, N, K, _ptr(aa), am, M if am else K, _ptr(bb), bm, N if bm else K,
+                                  _ptr(y), EPI_STORE_F32, _stream())
+        assert st == 0, _lib().oppo_last_error_global()
+        return y
+
+    monkeypatch.setenv("OPPO_TC2SM_LONGK", "1")
+    y = run(a_st, a_mn, b_st, b_mn)
+    y_k = run(a, 0, b, 0)
+    assert torch.equal(y, y_k)
+    ref = a.double() @ b.double().T
+    rel = ((y.double() - ref).abs().max() / ref.abs().max()).item()
+    assert rel < 2e-4, rel
+    monkeypatch.setenv("OPPO_TC2SM_LONGK", "0")
+    y1 = run(a, 0, b, 0)
+    rel1 = ((y.double() - y1.double()).abs().max() / ref.abs().max()).item()
+    assert rel1 < 2e-4, rel1
+
+
 def test_gemm_bf16_store_f32_long_k():
     # fp32 output isolates the tensor-core fp32 accumulation error over a long K
     M, N, K = 32, 256, 8192

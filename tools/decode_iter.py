@@ -18,13 +18,21 @@ shape = dict(SHAPES[SHAPE])
 eng = Engine(shape, shape, shape, shape, dtype=abi.DTYPE_BF16, max_slots=max(Ms) + 8, max_prompt_len=P,
              max_response_len=L, train_heads=0, carry=abi.CARRY_TOKEN,
              use_graphs=int(os.environ.get("GRAPHS", "1")))
+PROFILE = os.environ.get("PROFILE") == "1"  # cudaProfilerStart/Stop around the graph-captured run
+if PROFILE:
+    import ctypes
+    cudart = ctypes.CDLL("libcudart.so.12")
 nid = 0
 for M in Ms:
     for rep in range(2):
         seqs = S.seq_array([dict(id=nid + i, prompt_len=P, target_len=L) for i in range(M)])
         nid += M
         eng.admit(seqs, prompts=[(np.arange(P, dtype=np.int32) * 7 + s.id) % 1000 for s in seqs])
+        if PROFILE and rep == 1:
+            cudart.cudaProfilerStart()
         outs, led = eng.run_step(list(seqs), 64, abi.MODE_SEQUENTIAL, M)
+        if PROFILE and rep == 1:
+            cudart.cudaProfilerStop()
         eng.release([s.id for s in seqs])
     per = led.decode_loop_us / L
     gbs = (led.decode_weight_bytes + led.decode_kv_bytes) / (led.decode_loop_us * 1e-6) / 1e9

@@ -25,6 +25,8 @@ for d in recs:
 ks = list(kern.values())
 starts = [i for i, k in enumerate(ks) if k["name"].startswith("decode_rows")]
 wins = [ks[a:b] for a, b in zip(starts, starts[1:])]
+if not wins and starts:  # a single captured iteration: up to the end of the list
+    wins = [ks[starts[0]:]]
 mode = collections.Counter(len(w) for w in wins).most_common(1)[0][0]
 wins = [w for w in wins if len(w) == mode]
 dram = [sum(k.get("dram", 0.0) for k in w) for w in wins]
