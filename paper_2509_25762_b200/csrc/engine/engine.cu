@@ -100,44 +100,6 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
     }
 };
 
-// The scorer side waits on the device: one single-thread kernel polls the
-// flag (ld.acquire.gpu, cyclic >=) and the wave's kernels follow it in stream
-// order.  (A front-end wait -- cuStreamWaitValue32 -- can block a hardware
-// queue the actor's own work sits behind: it deadlocked on B200 when the two
-// streams shared a queue, as the driver documentation warns.)  A flag that
-// never arrives traps after 30 s instead of wedging the GPU.
-__global__ void wait_ready(const uint32_t* __restrict__ flag, uint32_t want) {
-    if (threadIdx.x != 0) return;
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (;;) {
-        uint32_t v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-        if (static_cast<int32_t>(v - want) >= 0) break;
-        __nanosleep(256);
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 30000000000ull) __trap();
-    }
-}
-void stream_wait_geq(Engine& e, cudaStream_t st, const uint32_t* flag, uint32_t v) {
-    wait_ready<<<1, 32, 0, st>>>(flag, v);
-    OPPO_CUDA_CHECK(cudaGetLastError());
-    e.launches += 1;
-}
-// The actor side: a single-thread kernel publishes the wave's sequence number
-// with a device-scope release store, ordered after the decode iteration that
-// completed the chunks (a front-end memory-op write was not observed by the
-// polling kernel on B200).
-__global__ void set_ready(uint32_t* __restrict__ flag, uint32_t v) {
-    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
-}
-void stream_write(Engine& e, cudaStream_t st, uint32_t* flag, uint32_t v) {
-    set_ready<<<1, 32, 0, st>>>(flag, v);
-    OPPO_CUDA_CHECK(cudaGetLastError());
-    e.launches += 1;
-}
-
 // Host thread that enqueues the scorer waves on the scorer stream.  A wave is
 // hundreds of launches; enqueued from the driver thread they can fill the
 // launch queue and block it, starving the actor stream of its next decode
@@ -1006,12 +968,6 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         // off: with concurrent scorer passes the scorers finish within ~8 ms of
         // decode, shorter than the precompute on the actor SMs (215.4 vs 213.6)
         e->pre_lp = env_int("OPPO_PRE_LP", 0) != 0;
-        // device-side hand-off only between green contexts: two streams of one
-        // context may share a hardware queue, where a waiting scorer kernel
-        // would block the actor work that writes its flag (deadlocked on B200)
-        e->chunk_flags = env_int("OPPO_CHUNK_FLAGS", 0) != 0 && e->sms_scorer < e->num_sms;
-        OPPO_CUDA_CHECK(cudaMalloc(&e->d_ready, Engine::kReadyRing * sizeof(uint32_t)));
-        OPPO_CUDA_CHECK(cudaMemsetAsync(e->d_ready, 0, Engine::kReadyRing * sizeof(uint32_t), st));
         e->g_chunk = std::max(64, env_int("OPPO_G_CHUNK", e->g_chunk)) / 8 * 8;  // update token chunk
         // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
         // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
@@ -1067,8 +1023,7 @@ void engine_free(Engine* e) {
                     static_cast<void*>(e->d_mega_bar), static_cast<void*>(e->d_mega_aws),
                     static_cast<void*>(e->d_mega_acnt), e->pre_hf, static_cast<void*>(e->pre_tok),
                     static_cast<void*>(e->pre_new), static_cast<void*>(e->pre_lse), static_cast<void*>(e->pre_meta),
-                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt),
-                    static_cast<void*>(e->d_ready)})
+                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) free_work(*w);
@@ -1738,33 +1693,8 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
             }
         }
     } drain_guard{worker};
-    const bool flags = e.chunk_flags;
-    std::vector<uint32_t> wave_seq(waves.size());
-    for (size_t k = 0; flags && k < waves.size(); ++k) wave_seq[k] = ++e.ready_seq;
-    // The scorer stream's copy of wave k is enqueued one wave ahead (when wave
-    // k-1's flag is written), gated on the device by wave k's flag: the launch
-    // queue never holds more than ~two waves of work that waits on the actor,
-    // so the actor's own launches are never stuck behind them.
-    auto post_wave = [&](size_t k) {
-        uint32_t* flag = e.d_ready + (wave_seq[k] % Engine::kReadyRing);
-        const uint32_t want = wave_seq[k];
-        const WavePlan* wave = &waves[k];
-        worker.post([&e, &A, &prefill_tokens, flag, want, wave] {
-            stream_wait_geq(e, e.ss, flag, want);
-            int64_t tok = 0;
-            for (const auto& p : wave->passes) run_scorer_pass<T>(e, p, A, e.ss, tok);
-            prefill_tokens += tok;
-        });
-    };
-    if (flags && !waves.empty()) post_wave(0);
     auto fire_waves_at = [&](int64_t it) {
         while (wi < waves.size() && waves[wi].at_iter == it) {
-            if (flags) {  // actor-stream order: after iteration `it`, the wave's chunks are complete
-                stream_write(e, e.sa, e.d_ready + (wave_seq[wi] % Engine::kReadyRing), wave_seq[wi]);
-                if (wi + 1 < waves.size()) post_wave(wi + 1);
-                ++wi;
-                continue;
-            }
             cudaEvent_t ev = e.ev_pool[wi + 1];
             OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));  // actor-stream order: after iteration `it`
             const WavePlan* wave = &waves[wi];

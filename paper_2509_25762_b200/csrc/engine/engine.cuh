@@ -173,16 +173,6 @@ struct Engine {
     cudaStream_t sa = nullptr, ss = nullptr;
     cudaStream_t su = nullptr;  // admission prefill + PPO update: whole GPU (== sa without a partition)
     std::vector<cudaEvent_t> ev_pool;
-    // K13 chunk hand-off on the device: after the decode iteration that
-    // completes a wave's chunks the actor stream writes the wave's sequence
-    // number into a ring of per-chunk ready flags (cuStreamWriteValue32); the
-    // scorer stream's first kernel of the wave polls it (wait_ready) -- no
-    // event or host round trip between the actor and the scorers.
-    // OPPO_CHUNK_FLAGS=1 selects it; the default is per-wave events.
-    static constexpr int kReadyRing = 256;
-    uint32_t* d_ready = nullptr;  // [kReadyRing] flags (monotone sequence numbers)
-    uint32_t ready_seq = 0;       // last sequence number issued
-    bool chunk_flags = true;
     cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr,
                 ev_loop0 = nullptr;
     bool step_open = false;

@@ -87,9 +87,9 @@ int gemm_logit_tiles(int, int N) { return (N + kSampleBlock - 1) / kSampleBlock;
 // experimental, off: the 256x256 tile serialises its epilogue with the
 // mainloop at one CTA per SM and measured slower (249 vs 182 us, gate|up at
 // 8192 rows) than two 128x256 CTAs per SM
-bool persist_enabled() {  // read per call so tests can compare both kernels in one process
+int persist_mode() {  // read per call so tests can compare both kernels in one process
     const char* v = std::getenv("OPPO_GEMM_PERSIST");
-    return v ? std::atoi(v) != 0 : false;  // off: faster alone, slower in the cfg2 bench (profiles/)
+    return v ? std::atoi(v) : 0;  // 0 off (slower in the cfg2 bench), 1 everywhere, 2 PPO update only
 }
 bool tc2sm_long_enabled() {  // read per call so tests can compare both kernels in one process
     const char* v = std::getenv("OPPO_TC2SM_LONGK");
@@ -155,7 +155,8 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // mainloop and the 2-CTA/SM kernel (8 epilogue warps per SM) wins
     // (bench: update 60 -> 69 ms on the persistent kernel; O / down no gain).
     const bool light = ep.mode == EPI_STORE || ep.mode == EPI_SWIGLU || ep.mode == EPI_ROPE_APPEND;
-    if (m_tiles >= 8 && light && !mn && dtype == OPPO_DTYPE_BF16 && persist_enabled()) {
+    const int pm = persist_mode();
+    if (m_tiles >= 8 && light && !mn && dtype == OPPO_DTYPE_BF16 && (pm == 1 || (pm == 2 && ep.update_gemm))) {
         // 128-wide tiles where a 256-wide last tile would waste > 5% (N = 896, 1152)
         const int pad256 = (N + 255) / 256 * 256 - N;
         const int BNp = (N % 128 == 0 && pad256 * 20 > N) ? 128 : 256;

@@ -179,6 +179,7 @@ void setup_model(Engine& e, TrainState& ts, int mid, cudaStream_t st) {
 
 // Y[M, N] (epilogue ep) = A[M, K] . B[N, K]^T, packed rows
 void mm(Engine& e, cudaStream_t st, const void* A, int M, int K, const void* B, int N, EpiParams ep) {
+    ep.update_gemm = 1;
     gemm_run(e, e.ws, st, A, M, K, K, B, N, K, ep);
 }
 // The same with operands read in place: K-major (kK, stored [M][K] / [N][K])
@@ -187,6 +188,7 @@ constexpr int kK = 0, kMN = 1;
 void mmt(Engine& e, cudaStream_t st, const void* A, int a_mn, int lda, const void* B, int b_mn, int ldb, int M,
          int N, int K, EpiParams ep) {
     ep.pair_long_k = 1;  // long-K gradient GEMMs may take CTA-pair tiles
+    ep.update_gemm = 1;
     gemm_run_t(e, e.ws, st, A, a_mn, lda, B, b_mn, ldb, M, N, K, ep);
 }
 EpiParams epi(int mode, void* y, int ldy, float scale = 1.f, const float* bias = nullptr) {
