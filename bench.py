@@ -38,9 +38,9 @@ CFG2 = dict(name="cfg2", actor="0.5b", scorer="0.5b", batch=256, prompt_len=128,
 CFG3 = dict(name="cfg3", actor="1.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
             sigma=1.0, cap=1024, chunk=64, delta=26)
 # BASELINE configs[3] per GPU: 7B actor + 1.5B scorers, 512 prompts over 8 GPUs = 64 per GPU,
-# LN(5.5, 1.0) cap 2048, 10% overcommit (6 per GPU); the update in 4096-row micro-batches
+# LN(5.5, 1.0) cap 2048, 10% overcommit (6 per GPU)
 CFG4 = dict(name="cfg4", actor="7b", scorer="1.5b", batch=64, prompt_len=128, mu=5.5,
-            sigma=1.0, cap=2048, chunk=64, delta=6, train_rows=4096)
+            sigma=1.0, cap=2048, chunk=64, delta=6)
 WORKLOADS = {}
 TINY = dict(name="cfg1", actor="tiny", scorer="tiny", batch=8, prompt_len=8, mu=3.5, sigma=0.6,
             cap=64, chunk=16, delta=2)

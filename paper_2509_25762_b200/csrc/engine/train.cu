@@ -107,6 +107,7 @@ struct TrainState {
     std::vector<float*> x_in, x_mid, lse, rstd1, rstd2;
     std::vector<void*> h1, h2, qkv, o, gu, ff;
     // transients
+    float* dkv_part = nullptr;  // [G][rows][2 * KV * hd] head-split dK / dV partials
     float *x = nullptr, *dx = nullptr, *dh = nullptr, *dqkv = nullptr, *dvec = nullptr, *gscr = nullptr,
           *colp = nullptr, *head_out = nullptr, *dhf_c = nullptr;
     void *hf = nullptr, *dgu = nullptr, *dxc = nullptr, *dO = nullptr, *dqkvc = nullptr, *hf_resp = nullptr,
@@ -264,7 +265,7 @@ void attn_launch(int which, const train::TBlk* blks, int nb, const T* qkv, int l
 template <int HD>
 void attn_mma_launch(int which, const train::TBlk* blks, int nb, const __nv_bfloat16* qkv, int ld, int H, int KV,
                      __nv_bfloat16* o, float* lse, const __nv_bfloat16* dO, const float* dvec, float* dqkv,
-                     cudaStream_t st) {
+                     cudaStream_t st, float* part, int rows) {
     using M = train::MmaT<HD>;
     static bool attr = false;
     if (!attr) {
@@ -280,8 +281,15 @@ void attn_mma_launch(int which, const train::TBlk* blks, int nb, const __nv_bflo
         train::attn_fwd_mma<HD><<<dim3(nb, H), 128, M::SMEM_FWD, st>>>(blks, qkv, ld, H, KV, o, lse);
     else if (which == 1)
         train::attn_dq_mma<HD><<<dim3(nb, H), 128, M::SMEM_DQ, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
-    else
-        train::attn_dkv_mma<HD><<<dim3(nb, KV), 128, M::SMEM_DKV, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
+    else {  // the G query heads of each KV head over G CTAs, then the ordered sum
+        const int gs = part ? H / KV : 1;
+        train::attn_dkv_mma<HD><<<dim3(nb, KV * gs), 128, M::SMEM_DKV, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv,
+                                                                         ld, gs, part, rows);
+        if (gs > 1) {
+            const int64_t n4 = static_cast<int64_t>(rows) * 2 * KV * HD / 4;
+            train::dkv_combine<<<cdiv(n4, 256), 256, 0, st>>>(part, gs, rows, 2 * KV * HD, dqkv, ld, H * HD);
+        }
+    }
 }
 
 // tensor-core (mma.sync) attention for bf16 with head_dim 64 / 128 (64-row
@@ -293,12 +301,12 @@ constexpr bool use_mma_attn(int hd) {
 
 template <class T>
 void attn(int hd, int which, const train::TBlk* blks, int nb, const T* qkv, int ld, int H, int KV, T* o, float* lse,
-          const T* dO, const float* dvec, float* dqkv, cudaStream_t st) {
+          const T* dO, const float* dvec, float* dqkv, cudaStream_t st, float* part = nullptr, int rows = 0) {
     if (nb <= 0) return;
     if constexpr (std::is_same_v<T, __nv_bfloat16>) {
         if (use_mma_attn<T>(hd) && std::getenv("OPPO_TRAIN_SIMT_ATTN") == nullptr) {
-            if (hd == 64) attn_mma_launch<64>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st);
-            else attn_mma_launch<128>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st);
+            if (hd == 64) attn_mma_launch<64>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st, part, rows);
+            else attn_mma_launch<128>(which, blks, nb, qkv, ld, H, KV, o, lse, dO, dvec, dqkv, st, part, rows);
             return;
         }
     }
@@ -347,6 +355,13 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
     ts.dx = static_cast<float*>(ts.scr.take(R * D * 4));
     ts.dh = static_cast<float*>(ts.scr.take(R * D * 4));
     ts.dqkv = static_cast<float*>(ts.scr.take(R * qkv * 4));
+    size_t part_floats = 0;
+    for (int mid : {ACTOR, CRITIC}) {
+        const auto& md = e.models[mid].dims;
+        part_floats = std::max(part_floats, static_cast<size_t>(md.n_heads / md.n_kv_heads) * R * 2 * md.n_kv_heads *
+                                                md.head_dim);
+    }
+    ts.dkv_part = static_cast<float*>(ts.scr.take(part_floats * 4));
     ts.dvec = static_cast<float*>(ts.scr.take(R * H * 4));
     ts.gscr = static_cast<float*>(ts.scr.take(R * std::max(D, qkv) * 4));
     ts.colp = static_cast<float*>(ts.scr.take(kColParts * wide * 4));
@@ -572,7 +587,8 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             train::attn_dvec<T><<<cdiv(static_cast<int64_t>(Tr) * H * 32, 256), 256, 0, st>>>(
                 dO, static_cast<const T*>(ts.o[l]), Tr, H, hd, ts.dvec);
             attn<T>(hd, 1, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
-            attn<T>(hd, 2, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
+            attn<T>(hd, 2, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st,
+                    std::getenv("OPPO_TRAIN_DKV_NOSPLIT") ? nullptr : ts.dkv_part, Tr);
             train::rope_rows<float><<<Tr, 128, 0, st>>>(ts.dqkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 1);
             colsum_into(ts, ts.dqkv, Tr, qkvw, Lt.bqkv.grad, st);
             T* dqc = static_cast<T*>(ts.dqkvc);

@@ -275,11 +275,17 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
     }
 }
 
+// gsplit > 1: the G query heads of a KV head are split over gsplit CTAs
+// (blockIdx.y = kvh * gsplit + part); each writes its dK / dV sums into
+// part[gs][row][2 * KV * HD] and dkv_combine adds them in part order
+// (deterministic).  The first key block of a long sequence otherwise walks
+// G x (its query blocks) tiles alone and sets the kernel's duration.
 template <int HD>
 __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blks, const __nv_bfloat16* __restrict__ qkv,
                                                     int ld, int H, int KV, const __nv_bfloat16* __restrict__ dout,
                                                     const float* __restrict__ lse, const float* __restrict__ dvec,
-                                                    float* __restrict__ dqkv, int ldd) {
+                                                    float* __restrict__ dqkv, int ldd, int gsplit, float* __restrict__ part,
+                                                    int rows) {
     using M = MmaT<HD>;
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw);
@@ -291,7 +297,8 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
     float* lse_s = reinterpret_cast<float*>(dOt + M::TR);
     float* d_s = lse_s + kMBlk;
     const TBlk b = blks[blockIdx.x];  // q0 = key block start
-    const int kvh = blockIdx.y, G = H / KV;
+    const int kvh = blockIdx.y / gsplit, gs = blockIdx.y % gsplit, G = H / KV;
+    const int gh0 = gs * G / gsplit, gh1 = (gs + 1) * G / gsplit;
     const int k0 = b.q0, nk = min(kMBlk, b.len - k0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;  // this warp's 16 keys
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
     for (int dt = 0; dt < HD / 8; ++dt)
 #pragma unroll
         for (int c = 0; c < 4; ++c) dk[dt][c] = dv[dt][c] = 0.f;
-    for (int gh = 0; gh < G; ++gh) {
+    for (int gh = gh0; gh < gh1; ++gh) {
         const int h = kvh * G + gh;
         for (int q0 = k0; q0 < b.len; q0 += kMBlk) {
             const int nq = min(kMBlk, b.len - q0);
@@ -338,14 +345,34 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
         const int key = r0 + g + 8 * i;
         if (key >= nk) continue;
         const size_t r = static_cast<size_t>(b.row0 + k0 + key);
+        // gsplit == 1: straight into dqkv's K | V columns; else this part's row
+        float* dst = gsplit == 1 ? dqkv + r * ldd + H * HD
+                                 : part + (static_cast<size_t>(gs) * rows + r) * (2 * KV * HD);
 #pragma unroll
         for (int dt = 0; dt < HD / 8; ++dt) {
-            *reinterpret_cast<float2*>(dqkv + r * ldd + (H + kvh) * HD + dt * 8 + 2 * tq) =
+            *reinterpret_cast<float2*>(dst + kvh * HD + dt * 8 + 2 * tq) =
                 make_float2(dk[dt][2 * i] * scale, dk[dt][2 * i + 1] * scale);
-            *reinterpret_cast<float2*>(dqkv + r * ldd + (H + KV + kvh) * HD + dt * 8 + 2 * tq) =
+            *reinterpret_cast<float2*>(dst + (KV + kvh) * HD + dt * 8 + 2 * tq) =
                 make_float2(dv[dt][2 * i], dv[dt][2 * i + 1]);
         }
     }
+}
+
+// dqkv[r][H*HD + c] = sum over parts (in order) of part[p][r][c], c < w = 2*KV*HD
+static __global__ void dkv_combine(const float* __restrict__ part, int parts, int rows, int w, float* __restrict__ dqkv,
+                                   int ldd, int col0) {
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4;
+    if (i >= static_cast<int64_t>(rows) * w) return;
+    const int64_t r = i / w, c = i % w;
+    float4 acc = *reinterpret_cast<const float4*>(part + i);
+    for (int p = 1; p < parts; ++p) {
+        const float4 v = *reinterpret_cast<const float4*>(part + static_cast<size_t>(p) * rows * w + i);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(dqkv + r * ldd + col0 + c) = acc;
 }
 
 }  // namespace train

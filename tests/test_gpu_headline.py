@@ -61,11 +61,11 @@ def _cuda():
         pytest.skip("no GPU")
 
 
-def run_cfg2(steps=STEPS, scorer_sms=64, env=None, keep=None, weights=False):
+def run_cfg2(steps=STEPS, scorer_sms=64, env=None, keep=None, weights=False, wl=None):
     """Two cfg2 steps through the engine exactly as bench.py drives it.  Returns
     per-step decisions + outcomes, and rollouts of the sequences in `keep`
     (all selected sequences when keep == 'all')."""
-    wl = bench.CFG2
+    wl = wl or bench.CFG2
     cfg = bench.make_cfg(wl)
     old = {}
     for k, v in (env or {}).items():
@@ -258,3 +258,37 @@ def test_headline_partition_and_streams_do_not_change_results():
         for f in ("tokens", "old_lp", "ref_lp", "values"):
             assert np.array_equal(x[f], y[f]), (k, f)
         assert x["reward"] == y["reward"] or (np.isnan(x["reward"]) and np.isnan(y["reward"])), k
+
+
+def test_cfg3_decisions_and_content_vs_reference():
+    """BASELINE configs[2] on one GPU as bench.py runs it (1.5B actor + 0.5B
+    scorers, B = 256 + 26, 64-SM scorer partition): two steps of cut / chunk
+    progress / selection against the compiled reference's run_step, and the
+    shortest selected sequence's tokens and old log-probs at full depth (28
+    layers) against the bf16-rounding fp64 oracle."""
+    _cuda()
+    run = run_cfg2(steps=2, keep="all", weights=True, wl=bench.CFG3)
+    lat = R.lockstep_latency()
+    for st in run["log"]:
+        act = [_mk(t) for t in st["active"]]
+        arr = (abi.SeqState * len(act))(*act)
+        tok_out, _ = O.run_step(arr, len(act), 64, abi.MODE_STREAMED, lat, st["need"], credit_partial=True)
+        assert [o.as_tuple() for o in tok_out] == st["outs"]
+        ref_out, _ = R.run_step(arr, len(act), 64, abi.MODE_STREAMED, lat, st["need"])
+        assert [(o.seq_id, o.score_ready) for o in ref_out] == [(g[0], g[1]) for g in st["outs"]]
+    assert all(len(st["selected"]) == 256 for st in run["log"])
+    P = 128
+    sel0 = run["log"][0]["selected"]
+    i = min(sel0, key=lambda k: (run["rollouts"][k]["length"], k))
+    ro = run["rollouts"][i]
+    seq = np.concatenate([run["prompts"][i], ro["tokens"]]).astype(np.int64)
+    da, wa = run["weights"][0]
+    m = N.GptNp(da, wa, bf16_mode=True)
+    L = ro["length"]
+    _, lg = m.forward(seq[:-1], rows=np.arange(P - 1, P + L - 1))
+    lp = _logsm(lg)[np.arange(L), ro["tokens"][:L]]
+    assert np.abs(lp - ro["old_lp"]).max() <= TOL_LP
+    for j in range(L):
+        tok, _, mb, mi = O.sample_token(lg[j], O.token_key(SAMPLE_SEED, i, j + 1))
+        if min(mb, mi) > MARGIN:
+            assert tok == ro["tokens"][j], (i, j)
