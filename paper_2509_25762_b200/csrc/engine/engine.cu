@@ -1045,6 +1045,7 @@ void engine_free(Engine* e) {
     } catch (...) {
     }
     delete e;
+    cudaGetLastError();  // teardown is best effort: leave no error for the caller's next CUDA call
 }
 
 // =================================================================== admit

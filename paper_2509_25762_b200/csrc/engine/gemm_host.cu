@@ -95,6 +95,10 @@ bool tc2sm_long_enabled() {  // read per call so tests can compare both kernels 
     const char* v = std::getenv("OPPO_TC2SM_LONGK");
     return v ? std::atoi(v) != 0 : true;  // measured: update 912 -> 887 ms at 39K tokens
 }
+bool tc2sm_short_enabled() {  // read per call (A/B in one process)
+    const char* v = std::getenv("OPPO_TC2SM_SHORT");
+    return v ? std::atoi(v) != 0 : false;
+}
 static const bool g_tc256 = [] {
     const char* v = std::getenv("OPPO_TC256");
     return v && std::atoi(v) != 0;
@@ -217,12 +221,17 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     const int pairs = ((m_tiles + 1) / 2) * ((N + 255) / 256);
     const bool long2 = ep.pair_long_k && tc2sm_long_enabled() && !scorer_stream && kb_all >= 64 && m_tiles >= 2 &&
                        pairs * 2 * 10 >= num_sms * 9 && ep.mode != EPI_LOGITS && !rope;
-    if ((m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && use2) || long2) {
+    // the update's token-rich short-K GEMMs (forward, dgrad against D-wide
+    // weights) on CTA pairs, two pairs per SM pair (OPPO_TC2SM_SHORT)
+    const bool short2 = ep.update_gemm && tc2sm_short_enabled() && !long2 && m_tiles >= 8 && N >= 512 &&
+                        pairs * 2 >= num_sms && ep.mode != EPI_LOGITS && !rope;
+    if ((m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && use2) || long2 || short2) {
         static std::once_flag attr2;
         std::call_once(attr2, [] {
-            OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 tc::Cfg2Sm::SMEM));
+            OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 tc::Cfg2Sm<6>::SMEM));
+            OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 tc::Cfg2Sm<3>::SMEM));
         });
         sh.splits = 1;
         sh.kb_per_split = (K + 63) / 64;
@@ -230,8 +239,12 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         const CUtensorMap& mx = a_mn ? cached_map(e, x, K, M, ldx, 64, s1) : cached_map(e, x, M, K, ldx, 128, s1);
         const CUtensorMap& mw = b_mn ? cached_map(e, wt, K, N, ldw, 64, s2) : cached_map(e, wt, N, K, ldw, 128, s2);
         const int mt2 = (m_tiles + 1) / 2 * 2;  // whole CTA pairs (OOB rows zero-filled)
-        launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm, dim3(mt2, (N + 255) / 256), dim3(128),
-                       tc::Cfg2Sm::SMEM, st, mx, mw, sh, ep);
+        if (long2)
+            launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm<6>, dim3(mt2, (N + 255) / 256), dim3(128),
+                           tc::Cfg2Sm<6>::SMEM, st, mx, mw, sh, ep);
+        else
+            launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm<3>, dim3(mt2, (N + 255) / 256), dim3(128),
+                           tc::Cfg2Sm<3>::SMEM, st, mx, mw, sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
@@ -434,7 +447,8 @@ void gemm_run_t(Engine& e, Work& w, cudaStream_t st, const void* a, int a_mn, in
 void gemm_standalone_t(int dtype, int M, int N, int K, const void* a, int a_mn, int lda, const void* b, int b_mn,
                        int ldb, void* y, int epi, cudaStream_t st) {
     EpiParams ep{};
-    ep.pair_long_k = 1;  // as the update's gradient GEMMs
+    ep.pair_long_k = 1;  // as the update's GEMMs
+    ep.update_gemm = 1;
     ep.mode = epi;
     ep.y = y;
     ep.ldy = N;

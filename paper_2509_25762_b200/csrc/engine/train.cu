@@ -123,7 +123,8 @@ void train_free(Engine& e) {
     for (auto& m : ts->m)
         for (PT* p : m.all()) {
             if (p->grad) cudaFree(p->grad);
-            if (p->master && !(p == &m.embed && p->master == e.models[ACTOR].lm_master)) cudaFree(p->master);
+            // the actor's lm_head master belongs to the engine (freed in engine_free)
+            if (p->master && p->master != e.models[ACTOR].lm_master) cudaFree(p->master);
         }
     delete ts;
     e.train_state = nullptr;

@@ -549,6 +549,27 @@ def test_7b_actor_15b_scorers_width_bf16_vs_oracle():
     eng.close()
 
 
+def test_untied_full_update_teardown_leaves_cuda_clean():
+    """An untied actor (7B geometry, separate lm_head) through the full
+    update and engine teardown: its lm_head fp32 master is freed once, and
+    the caller's next CUDA call (torch here) sees no leftover error -- a
+    double free used to surface as 'invalid argument' in bench.py's cfg4 run."""
+    shape = dict(n_layers=2, d_model=256, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=512, vocab=2048, tied=0)
+    P = 8
+    eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=32,
+                 sample_seed=SAMPLE_SEED, train_heads=2)
+    st = fresh_states(4, P, [12, 20, 7, 16])
+    eng.admit(st)
+    outs, _ = eng.run_step(st, 8, abi.MODE_STREAMED, 4)
+    hp = abi.PpoHparams(gamma=1.0, lambda_=0.95, clip_epsilon=0.2, learning_rate=1e-3,
+                        value_learning_rate=1e-3, kl_coef=0.05, whiten=1)
+    eng.ppo_update([s["id"] for s in st], hp)
+    eng.close()
+    x = torch.ones(4, device="cuda") * 2
+    torch.cuda.synchronize()
+    assert float(x.sum()) == 8.0
+
+
 def test_edge_cases_single_token_prompts_and_responses_vs_oracle():
     """Edge cases of the step executor (fp32, strict token parity): one-token
     prompts (no admission prefill; decode starts from the prompt token),

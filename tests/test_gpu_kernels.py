@@ -116,6 +116,34 @@ def test_gemm_cta_pair_long_k(monkeypatch, a_mn, b_mn):
     assert rel1 < 2e-4, rel1
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1)])
+def test_gemm_cta_pair_short_k(monkeypatch, a_mn, b_mn):
+    """The short-K CTA-pair path (two pairs per SM pair, 3-stage ring;
+    OPPO_TC2SM_SHORT=1) for the update's token-rich forward / dgrad GEMMs:
+    within fp32-accumulation noise of float64 and of the single-CTA kernel."""
+    M, N, K = 2048, 9728, 896
+    g = torch.Generator(device="cuda").manual_seed(21 + b_mn)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b_st = b.t().contiguous() if b_mn else b
+
+    def run():
+        y = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+        st = _lib().oppo_k_gemm_t(1, M, N, K, _ptr(a), a_mn, K, _ptr(b_st), b_mn, N if b_mn else K,
+                                  _ptr(y), EPI_STORE_F32, _stream())
+        assert st == 0, _lib().oppo_last_error_global()
+        return y
+
+    monkeypatch.setenv("OPPO_TC2SM_SHORT", "1")
+    y = run()
+    monkeypatch.setenv("OPPO_TC2SM_SHORT", "0")
+    y1 = run()
+    ref = a.double() @ b.double().T
+    for out in (y, y1):
+        rel = ((out.double() - ref).abs().max() / ref.abs().max()).item()
+        assert rel < 2e-4, rel
+
+
 def test_gemm_bf16_store_f32_long_k():
     # fp32 output isolates the tensor-core fp32 accumulation error over a long K
     M, N, K = 32, 256, 8192
