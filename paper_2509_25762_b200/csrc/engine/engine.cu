@@ -499,124 +499,6 @@ void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
     }
 }
 
-// ------------------------------------------------ persistent decode kernel
-bool mega_supported(const Engine& e, const oppo_model_dims& d) {
-    const int G = d.n_heads / d.n_kv_heads;
-    return e.dtype == OPPO_DTYPE_BF16 && G <= 16 && (d.head_dim == 64 || d.head_dim == 128) &&
-           d.d_model % 64 == 0 && d.d_model <= 3584 && (d.n_heads * d.head_dim) % 64 == 0 &&
-           d.d_ff % 64 == 0;
-}
-
-void mega_setup(Engine& e) {
-    Model& m = e.models[ACTOR];
-    const auto& d = m.dims;
-    std::vector<mega::LayerP> lp(d.n_layers);
-    const int qkvw = m.qkv_width(), qw = m.q_width();
-    for (int l = 0; l < d.n_layers; ++l) {
-        const auto& L = m.layers[l];
-        lp[l].w[mega::W_QKV] = make_tma_2d(L.wqkv, qkvw, d.d_model, d.d_model, 128);
-        lp[l].w[mega::W_O] = make_tma_2d(L.wo, d.d_model, qw, qw, 128);
-        lp[l].w[mega::W_GU] = make_tma_2d(L.wgu, 2 * d.d_ff, d.d_model, d.d_model, 128);
-        lp[l].w[mega::W_DN] = make_tma_2d(L.wdown, d.d_model, d.d_ff, d.d_ff, 128);
-        lp[l].bqkv = L.bqkv;
-        lp[l].ln1 = L.ln1;
-        lp[l].ln2 = L.ln2;
-    }
-    e.d_mega_layers = static_cast<mega::LayerP*>(dalloc(lp.size() * sizeof(mega::LayerP)));
-    OPPO_CUDA_CHECK(cudaMemcpy(e.d_mega_layers, lp.data(), lp.size() * sizeof(mega::LayerP),
-                               cudaMemcpyHostToDevice));
-    if (e.mega_trace) e.mega_trace_buf = static_cast<unsigned long long*>(dalloc(8 * (7 * d.n_layers + 2)));
-    e.d_mega_bar = static_cast<unsigned*>(dalloc(64));
-    OPPO_CUDA_CHECK(cudaMemset(e.d_mega_bar, 0, 64));
-    const size_t rows = static_cast<size_t>(e.S + 16) * d.n_kv_heads;
-    const size_t slot = static_cast<size_t>(16) * d.head_dim + 32;
-    e.d_mega_aws = static_cast<float*>(dalloc(rows * 4 * slot * 4));
-    e.d_mega_acnt = static_cast<int*>(dalloc(rows * 4));
-    OPPO_CUDA_CHECK(cudaMemset(e.d_mega_acnt, 0, rows * 4));
-}
-
-// One decode iteration's transformer stack as one persistent kernel; returns
-// the split count of the down-projection partials left for the final norm.
-template <int HD>
-int mega_launch_hd(Engine& e, Model& m, Work& w, cudaStream_t st, int R) {
-    const auto& d = m.dims;
-    mega::Args a{};
-    a.M = R;
-    a.Mp = (R + 15) / 16 * 16;
-    a.D = d.d_model;
-    a.H = d.n_heads;
-    a.KV = d.n_kv_heads;
-    a.HD = d.head_dim;
-    a.F = d.d_ff;
-    a.L = d.n_layers;
-    a.qkvw = m.qkv_width();
-    a.qw = m.q_width();
-    a.x = w.x;
-    a.h = static_cast<__nv_bfloat16*>(w.h);
-    a.attn = static_cast<__nv_bfloat16*>(w.attn);
-    a.ff = static_cast<__nv_bfloat16*>(w.ff);
-    a.ws = w.gemm_ws;
-    a.aws = e.d_mega_aws;
-    a.acnt = e.d_mega_acnt;
-    a.bar = e.d_mega_bar;
-    a.layers = e.d_mega_layers;
-    a.kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
-    a.slot = w.meta.slot;
-    a.pos = w.meta.pos;
-    const int G = w.sms;  // one CTA per SM of the actor partition
-    a.stage_bytes = dec::kWBytes + a.Mp * 128;
-    const int attn_smem = AttnDecCfg<HD>::SMEM;
-    const int budget = 225 * 1024 - 1024 - attn_smem - 512;  // + static smem < the 227 KB opt-in
-    a.stages = std::max(1, std::min(8, budget / a.stage_bytes));
-    // K split per GEMM.  qkv and O: one pipeline's worth of k blocks per item,
-    // so an item's weights are entirely prefetched during the preceding
-    // attention / norm phase and the consumer folds few partials.  down: split
-    // across the grid (its weights stream right after the gate|up barrier).
-    // gate|up: unsplit (SwiGLU needs the full sum).  OPPO_MEGA_KBPS_* override.
-    const int Ns[4] = {a.qkvw, a.D, 2 * a.F, a.D}, Ks[4] = {a.D, a.qw, a.D, a.F};
-    const char* env_k[4] = {"OPPO_MEGA_KBPS_QKV", "OPPO_MEGA_KBPS_O", "OPPO_MEGA_KBPS_GU", "OPPO_MEGA_KBPS_DN"};
-    for (int g = 0; g < 4; ++g) {
-        const int tiles = (Ns[g] + 127) / 128, kbt = Ks[g] / 64;
-        int kbps;
-        if (g == mega::W_GU) kbps = kbt;
-        else if (g == mega::W_DN) kbps = (kbt + std::max(1, G / tiles) - 1) / std::max(1, G / tiles);
-        else kbps = std::min(kbt, a.stages);
-        kbps = std::max(1, std::min(kbt, env_int(env_k[g], kbps)));
-        while (static_cast<size_t>((kbt + kbps - 1) / kbps) * R * Ns[g] > w.gemm_ws_floats) ++kbps;
-        a.kbps[g] = kbps;
-        a.sp[g] = (kbt + kbps - 1) / kbps;
-    }
-    a.att_sp = std::max(1, std::min(4, env_int("OPPO_MEGA_ATT_SP", 1)));
-    a.attn_off = a.stages * a.stage_bytes;
-    int cols = 32;
-    while (cols < a.Mp) cols *= 2;
-    a.tmem_cols = cols;
-    a.first_np = 0;
-    a.trace = nullptr;
-    if (e.mega_trace) a.trace = e.mega_trace_buf;
-    a.barriers_only = e.debug_skip == 255;
-    a.bar_ra = env_int("OPPO_MEGA_BAR_RA", 1);
-    a.eps = kRmsEps;
-    a.theta = kRopeTheta;
-    const int smem = 1024 + a.attn_off + attn_smem + 512;
-    static std::once_flag attr;
-    std::call_once(attr, [] {
-        OPPO_CUDA_CHECK(cudaFuncSetAttribute(mega::decode_layers<HD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-    });
-    CUtensorMap s1, s2, s3;
-    const CUtensorMap& xh = cached_map_pub(&e, w.h, R, a.D, a.D, a.Mp, s1);
-    const CUtensorMap& xa = cached_map_pub(&e, w.attn, R, a.qw, a.qw, a.Mp, s2);
-    const CUtensorMap& xf = cached_map_pub(&e, w.ff, R, a.F, a.F, a.Mp, s3);
-    launch(e.pdl, mega::decode_layers<HD>, dim3(G), dim3(128), smem, st, xh, xa, xf, a);
-    e.launches += 1;
-    return a.sp[mega::W_DN];
-}
-
-int mega_launch(Engine& e, Model& m, Work& w, cudaStream_t st, int R) {
-    return m.dims.head_dim == 64 ? mega_launch_hd<64>(e, m, w, st, R) : mega_launch_hd<128>(e, m, w, st, R);
-}
-
 template <class T>
 struct Final {
     bool write_h = true;
@@ -651,16 +533,6 @@ void forward(Engine& e, Model& m, Work& w, cudaStream_t st, int R, bool decode, 
     // by the consumer kernels (RoPE/KV append, RMSNorm residual add)
     const bool dec_gemm = std::is_same_v<T, __nv_bfloat16> && decode && R <= 512 && D <= 4096 &&
                           D % 64 == 0 && m.q_width() % 64 == 0 && d.d_ff % 64 == 0;
-    if (dec_gemm && e.d_mega_layers && &m == &e.models[ACTOR] && R <= e.mega_max_rows) {
-        const int np = mega_launch(e, m, w, st, R);
-        launch(e.pdl, residual_rmsnorm<T>, dim3(R), dim3(256), 0, st, w.x, m.final_norm,
-               fin.write_h ? static_cast<T*>(w.h) : nullptr, R, D, kRmsEps, w.gemm_ws, np,
-               static_cast<size_t>(R) * D, fin.head, w.head_out, fin.cache, w.meta.slot, w.meta.t,
-               e.tok_stride, fin.t_lo, fin.t_hi);
-        e.launches += 2;
-        OPPO_CUDA_CHECK(cudaGetLastError());
-        return;
-    }
     if (dec_gemm) {
         const size_t rope_smem = static_cast<size_t>(m.qkv_width()) * sizeof(T);
         const float* part = w.gemm_ws;
@@ -952,9 +824,6 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
             for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) w->sms = ns;
         // persistent decode kernel: experimental, off by default (measured slower
         // than the PDL-chained kernels: 2 us per grid barrier x 168, profiles/)
-        e->mega_max_rows = env_int("OPPO_MEGA_MAX_ROWS", 0);
-        e->mega_trace = env_int("OPPO_MEGA_TRACE", 0) != 0;
-        if (e->mega_max_rows > 0 && mega_supported(*e, cfg.actor)) mega_setup(*e);
         e->attn_cluster = env_int("OPPO_ATTN_CLUSTER", 1) != 0;
         e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
         e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
@@ -1019,9 +888,7 @@ void engine_free(Engine* e) {
     }
     for (void* p : {static_cast<void*>(e->d_hf_actor), static_cast<void*>(e->d_hf_critic),
                     static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf,
-                    static_cast<void*>(e->g_lm), static_cast<void*>(e->d_mega_layers),
-                    static_cast<void*>(e->d_mega_bar), static_cast<void*>(e->d_mega_aws),
-                    static_cast<void*>(e->d_mega_acnt), e->pre_hf, static_cast<void*>(e->pre_tok),
+                    static_cast<void*>(e->g_lm), e->pre_hf, static_cast<void*>(e->pre_tok),
                     static_cast<void*>(e->pre_new), static_cast<void*>(e->pre_lse), static_cast<void*>(e->pre_meta),
                     static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt)})
         if (p) cudaFree(p);
@@ -1764,17 +1631,6 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     OPPO_CUDA_CHECK(cudaGetLastError());
     e.step_open = false;
 
-    if (e.mega_trace && e.mega_trace_buf) {  // phase times of the last decode iteration
-        const int L = e.models[ACTOR].dims.n_layers;
-        std::vector<unsigned long long> t(7 * L + 1);
-        OPPO_CUDA_CHECK(cudaMemcpy(t.data(), e.mega_trace_buf, t.size() * 8, cudaMemcpyDeviceToHost));
-        double ph[7] = {0};
-        for (int l = 0; l < L; ++l)
-            for (int k = 0; k < 7; ++k) ph[k] += (t[l * 7 + k + 1] - t[l * 7 + k]) * 1e-3;
-        std::fprintf(stderr, "[oppo] mega phases (us, sum over %d layers): norm1 %.1f qkv %.1f attn %.1f o %.1f "
-                     "norm2 %.1f gu %.1f down %.1f total %.1f\n", L, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5],
-                     ph[6], (t[7 * L] - t[0]) * 1e-3);
-    }
     out = plan.outcomes;
     ledger = plan.ledger;
     float ms = 0;

@@ -19,7 +19,6 @@
 #include "kernels/model.cuh"
 #include "kernels/attn_mma.cuh"
 #include "kernels/attn_dec.cuh"
-#include "kernels/decode_mega.cuh"
 #include "oppo/oppo.h"
 
 namespace oppo {
@@ -189,14 +188,6 @@ struct Engine {
     bool rope_epi = true;       // prefill: RoPE + KV append in the q|k|v GEMM epilogue
     int attn_w8_tenths = 20;   // auto rule: 8 warps while CTAs <= tenths/10 x SMs
     int lmhead_dec_max = 32;   // decode lm_head through lmhead_dec.cuh up to this batch (0: off)
-    // persistent decode kernel (decode_mega.cuh) for batches <= mega_max_rows
-    int mega_max_rows = 256;
-    mega::LayerP* d_mega_layers = nullptr;
-    unsigned* d_mega_bar = nullptr;
-    float* d_mega_aws = nullptr;
-    int* d_mega_acnt = nullptr;
-    bool mega_trace = false;
-    unsigned long long* mega_trace_buf = nullptr;    // decode: RoPE + KV append + attention in one kernel (attn_dec)        // OPPO_DEBUG_SKIP: perf diagnosis only    // cap on split-KV (0: the merge buffer's limit)
     int dec_qkv_max = 96;      // largest batch for which qkv uses the swap-AB decode GEMM
     int dec_gu_max = 64;       // ... gate|up
     int dec_res_max = 192;     // ... O and down (down always: K >= 2048)

@@ -84,9 +84,6 @@ int gemm_logit_tiles(int, int N) { return (N + kSampleBlock - 1) / kSampleBlock;
 // zero-filled past M by TMA) x BN-row weight tiles; BN = 256 for prefill and
 // the lm_head, 64/128 for decode so the grid covers the SMs; split-K when the
 // tile count is still under half the SMs.
-// experimental, off: the 256x256 tile serialises its epilogue with the
-// mainloop at one CTA per SM and measured slower (249 vs 182 us, gate|up at
-// 8192 rows) than two 128x256 CTAs per SM
 int persist_mode() {  // read per call so tests can compare both kernels in one process
     const char* v = std::getenv("OPPO_GEMM_PERSIST");
     return v ? std::atoi(v) : 0;  // 0 off (slower in the cfg2 bench), 1 everywhere, 2 PPO update only
@@ -99,18 +96,6 @@ bool tc2sm_short_enabled() {  // read per call (A/B in one process)
     const char* v = std::getenv("OPPO_TC2SM_SHORT");
     return v ? std::atoi(v) != 0 : false;
 }
-static const bool g_tc256 = [] {
-    const char* v = std::getenv("OPPO_TC256");
-    return v && std::atoi(v) != 0;
-}();
-
-// experimental, off: measured 2x slower than the unsplit kernel (cluster
-// co-scheduling of two ~130 KB-smem CTAs costs more than the halved stream)
-static const bool g_dec_pair = [] {
-    const char* v = std::getenv("OPPO_DEC_PAIR");
-    return v && std::atoi(v) != 0;
-}();
-
 // cost-model latency (ns) of one fold round trip in the consuming kernel
 static const double g_fold_ns = [] {
     const char* v = std::getenv("OPPO_DEC_FOLD_NS");
@@ -188,26 +173,6 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
             });
             launch(e && e->pdl, tc::gemm_bf16_persist<128>, grid, dim3(192), tc::CfgP<128>::SMEM, st, mx, mw, sh, ep);
         }
-        OPPO_CUDA_CHECK(cudaGetLastError());
-        return;
-    }
-    // Token-rich prefill GEMMs (>= 8 token tiles, not the logits epilogue, the
-    // output wide enough to fill the SMs): 256x256 tiles, one CTA per SM.
-    if (m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && g_tc256 &&
-        ((M + 255) / 256) * ((N + 255) / 256) >= num_sms) {
-        static std::once_flag attr256;
-        std::call_once(attr256, [] {
-            OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc256,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 tc::Cfg256::SMEM));
-        });
-        sh.splits = 1;
-        sh.kb_per_split = (K + 63) / 64;
-        CUtensorMap s1, s2;
-        const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
-        const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 256, s2);
-        launch(e && e->pdl, tc::gemm_bf16_tc256, dim3((M + 255) / 256, (N + 255) / 256), dim3(128),
-               tc::Cfg256::SMEM, st, mx, mw, sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
@@ -358,14 +323,8 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
             }
         }
     }
-    // SwiGLU: K split over a CTA pair (DSMEM reduce) doubles the CTAs that
-    // stream the weights (gate|up has only N/128 weight tiles)
-    const bool pair = mode == DEC_SWIGLU && s.nbox == 1 && kb_total >= 4 && g_dec_pair &&
-                      tiles * 2 <= 2 * num_sms;
-    if (pair) splits = 2;
     s.kb_per_split = (kb_total + splits - 1) / splits;
     splits = (kb_total + s.kb_per_split - 1) / s.kb_per_split;
-    s.pair = pair ? 1 : 0;
     s.stages = std::max(1, std::min(s.kb_per_split, std::min(8, (200 * 1024) / stage)));
     int cols = 32;
     while (cols < (s.nbox == 2 ? 512 : s.box_rows)) cols *= 2;
@@ -384,10 +343,7 @@ int gemm_dec_impl(Engine* e, cudaStream_t st, const void* x, int M, int K, int l
     CUtensorMap s1, s2;
     const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, 128, s1);
     const CUtensorMap& mx = cached_map(e, x, M, K, ldx, s.box_rows, s2);
-    if (pair)
-        launch_cluster(pdl, dim3(1, 2, 1), dec::gemm_dec, dim3(tiles, 2), dim3(128), smem, st, mw, mx, s);
-    else
-        launch(pdl, dec::gemm_dec, dim3(tiles, splits), dim3(128), smem, st, mw, mx, s);
+    launch(pdl, dec::gemm_dec, dim3(tiles, splits), dim3(128), smem, st, mw, mx, s);
     OPPO_CUDA_CHECK(cudaGetLastError());
     return mode == DEC_PARTIAL ? splits : 1;
 }

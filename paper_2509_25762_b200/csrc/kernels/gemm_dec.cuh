@@ -18,7 +18,6 @@
 //     interleaved (gate_i, up_i) row pairs of adjacent lanes.
 #pragma once
 
-#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -42,7 +41,6 @@ struct DecShape {
     int ldy;
     const float* bias;  // DEC_STORE only
     float* ws;          // DEC_PARTIAL: [split][M][N] fp32
-    int pair;           // DEC_SWIGLU: K split over a 2-CTA cluster (grid.y = 2), DSMEM reduce
 };
 
 namespace dec {
@@ -174,45 +172,7 @@ static __global__ void __launch_bounds__(128, 1)
     const int n = n0 + row;
     const bool nv = n < s.N;
     const uint32_t tl = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    if (s.pair) {
-        // the two K halves of one weight tile live in the two CTAs of a
-        // cluster: each CTA pushes the token columns the OTHER one finalises
-        // into the other's (now idle) stage buffers, then finalises its own
-        // half: half0 + half1 -> SwiGLU -> bf16.
-        namespace cg = cooperative_groups;
-        cg::cluster_group cl = cg::this_cluster();
-        const int rank = static_cast<int>(cl.block_rank());
-        const int mcols = (s.M + 15) / 16 * 16;
-        const int h0 = (mcols / 2 + 15) / 16 * 16;  // rank 0 finalises [0, h0), rank 1 [h0, mcols)
-        const int lo = rank == 0 ? 0 : h0, hi = rank == 0 ? h0 : mcols;
-        const int plo = rank == 0 ? h0 : 0, phi = rank == 0 ? mcols : h0;
-        const int xs = max(h0, mcols - h0) + 1;  // exchange row stride (floats)
-        cl.sync();  // both mainloops done: stage buffers free
-        float* peer = cl.map_shared_rank(reinterpret_cast<float*>(smem), rank ^ 1);
-        for (int c0 = plo; c0 < phi; c0 += 16) {
-            float v[16];
-            tmem_ld16(tl + c0, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) peer[row * xs + (c0 - plo) + j] = v[j];
-        }
-        cl.sync();  // pushes visible
-        const float* mine = reinterpret_cast<const float*>(smem);
-        __nv_bfloat16* y = static_cast<__nv_bfloat16*>(s.y) + n / 2;
-        for (int c0 = lo; c0 < hi; c0 += 16) {
-            if (c0 >= s.M) break;
-            float v[16];
-            tmem_ld16(tl + c0, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const float o = mine[row * xs + (c0 - lo) + j];
-                const float t = rank == 0 ? v[j] + o : o + v[j];  // half0 + half1
-                const float up = __shfl_xor_sync(0xffffffffu, t, 1);
-                if (!(lane & 1) && nv && c0 + j < s.M)
-                    y[static_cast<size_t>(c0 + j) * s.ldy] = __float2bfloat16_rn(silu(t) * up);
-            }
-        }
-    }
-    for (int g = 0; g < (s.pair ? 0 : s.nbox); ++g) {
+    for (int g = 0; g < s.nbox; ++g) {
         for (int c0 = 0; c0 < s.box_rows; c0 += 16) {
             const int m0 = g * s.box_rows + c0;
             if (m0 >= s.M) break;  // warp-uniform

@@ -449,44 +449,6 @@ def test_two_branch_decode_iterations_vs_oracle():
     eng.close()
 
 
-def test_persistent_decode_kernel_vs_oracle_and_multi_kernel_path():
-    """The persistent decode kernel (decode_mega.cuh, experimental, enabled by OPPO_MEGA_MAX_ROWS)
-    at 40 rows, 0.5B geometry, 3 layers: sampled tokens / log-probs against the
-    fp64 oracle (near-ties excepted, as in the other bf16 tests), and against
-    the multi-kernel decode path (OPPO_MEGA_MAX_ROWS=0) on identical weights
-    and seeds: log-probs agree up to the first sampled-token divergence (the
-    random-init policy is near-uniform, so fp32 summation-order differences
-    flip near-tied draws)."""
-    import os
-    shape = dict(n_layers=3, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
-                 vocab=1024, tied=1)
-    P, C = 16, 16
-    lens = [20 + (7 * i) % 40 for i in range(40)]
-    res = []
-    for rows in ("256", "0"):
-        os.environ["OPPO_MEGA_MAX_ROWS"] = rows
-        try:
-            eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=48, max_prompt_len=P,
-                         max_response_len=64, sample_seed=SAMPLE_SEED)
-        finally:
-            os.environ.pop("OPPO_MEGA_MAX_ROWS", None)
-        st = fresh_states(len(lens), P, lens)
-        eng.admit(st)
-        eng.run_step(st, C, abi.MODE_SEQUENTIAL, len(lens))
-        res.append([eng.read_rollout(s["id"]) for s in st])
-        if rows == "256":
-            orc = oracles(eng)
-            for s in st[:6]:
-                check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.25, margin_tol=0.2,
-                              strict_tokens=False)  # 3 bf16 layers: scorer values drift more
-        eng.close()
-    for a, b in zip(*res):
-        n = min(a["length"], b["length"])
-        agree = a["tokens"][:n] == b["tokens"][:n]
-        k = int(np.argmin(agree)) if not agree.all() else n
-        assert np.max(np.abs(a["old_lp"][:k] - b["old_lp"][:k]), initial=0.0) < 0.05
-
-
 def test_gpu_tuner_on_measured_step_time_replays(tmp_path):
     """the chunk-size tuner (chunking.cpp:61-107) fed the GPU's
     measured step time.  Replaying the recorded (candidate, step_us) pairs

@@ -185,8 +185,7 @@ def test_gemm_swiglu_epilogue():
 @pytest.mark.parametrize("M,N,K,epi", [(4096, 9728, 896, EPI_SWIGLU), (8192, 4864, 896, EPI_STORE),
                                        (2304, 5120, 4864, EPI_STORE)])
 def test_gemm_prefill_256x256_tile_vs_torch(M, N, K, epi, monkeypatch):
-    """Token-rich GEMMs: the default path (128x256 tiles) and, where enabled
-    (OPPO_TC256=1, read at library load), the 256x256-tile kernel."""
+    """Token-rich GEMMs (prefill shapes) on the default 128x256-tile path."""
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(N, K, device="cuda", generator=g) * 0.03).to(torch.bfloat16)
