@@ -69,11 +69,13 @@ class Port:
         return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], -1)
 
     # ---------------------------------------------------------- decode
-    def decode_iteration(self, R, ctx, kv, rng):
+    def decode_iteration(self, R, ctx, kv, rng, tok=None, return_logits=False):
+        """One batched decode step at position ctx - 1 over kv[layer] = (K, V)
+        caches [R, KV, >= ctx, hd] (the new row is written at ctx - 1)."""
         d = self.d
         H, KV, hd = d["n_heads"], d["n_kv_heads"], d["head_dim"]
         G = H // KV
-        x = self.embed[rng.integers(0, d["vocab"], R)]
+        x = self.embed[rng.integers(0, d["vocab"], R) if tok is None else np.asarray(tok)]
         c, s = self.rope_tab(np.full(R, ctx - 1))
         for Lw, (kc, vc) in zip(self.layers, kv):
             h, _ = self.rms(x, Lw["g1"])
@@ -91,6 +93,8 @@ class Port:
             x = x + ((g / (1.0 + np.exp(-g))) * u) @ Lw["wdown"].T
         hf, _ = self.rms(x, self.gf)
         lg = hf @ self.lm_head.T
+        if return_logits:
+            return lg
         p = np.exp(lg - lg.max(-1, keepdims=True))
         cdf = np.cumsum(p, -1)
         return (cdf < rng.random((R, 1), dtype=F32) * cdf[:, -1:]).sum(-1)

@@ -40,7 +40,7 @@ namespace {
 
 constexpr float kEps = 1e-6f;
 constexpr float kTheta = 1e6f;
-constexpr int kColParts = 256;  // block partial rows of the column sums (ts.colp)
+constexpr int kColParts = 1024;  // block partial rows of the column sums (ts.colp)
 
 inline int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
@@ -209,7 +209,7 @@ template <class T>
 void rms_bwd_into(TrainState& ts, const float* x, const float* g, const float* dy, int rows, int d, float* dx,
                   T* dxc, float* gout, cudaStream_t st) {
     if (rows <= 0) return;
-    const int nblk = std::min(kColParts, std::max(1, rows / 32));
+    const int nblk = std::min(kColParts, std::max(1, rows / 16));  // 2 rows per warp at 32K rows
     const int per = cdiv(rows, nblk);
     const size_t smem = 8 * static_cast<size_t>(d) * 4;
     static bool attr = false;
@@ -220,6 +220,16 @@ void rms_bwd_into(TrainState& ts, const float* x, const float* g, const float* d
     }
     train::rms_bwd_cs<T><<<nblk, 256, smem, st>>>(x, g, dy, rows, d, per, kEps, dx, dxc, ts.colp);
     train::colsum_final<<<cdiv(d, 256), 256, 0, st>>>(ts.colp, nblk, d, gout);
+}
+
+// y = x rounded to T and out += column sums of x, in one pass over x
+template <class T>
+void cvt_colsum_into(TrainState& ts, const float* x, int rows, int cols, T* y, float* out, cudaStream_t st) {
+    if (rows <= 0) return;
+    const int chunks = std::min(kColParts, std::max(1, rows / 64));
+    const int per = cdiv(rows, chunks);
+    train::cvt_colsum_part<T><<<dim3(cdiv(cols, 256), chunks), 256, 0, st>>>(x, rows, cols, per, y, ts.colp);
+    train::colsum_final<<<cdiv(cols, 256), 256, 0, st>>>(ts.colp, chunks, cols, out);
 }
 
 void colsum_into(TrainState& ts, const float* x, int rows, int cols, float* out, cudaStream_t st) {
@@ -280,12 +290,13 @@ void attn_mma_launch(int which, const train::TBlk* blks, int nb, const __nv_bflo
     }
     if (which == 0)
         train::attn_fwd_mma<HD><<<dim3(nb, H), 128, M::SMEM_FWD, st>>>(blks, qkv, ld, H, KV, o, lse);
-    else if (which == 1)
-        train::attn_dq_mma<HD><<<dim3(nb, H), 128, M::SMEM_DQ, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld);
+    else if (which == 1)  // dq / dk come out with the RoPE transpose applied
+        train::attn_dq_mma<HD><<<dim3(nb, H), 128, M::SMEM_DQ, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv, ld,
+                                                                     kTheta);
     else {  // the G query heads of each KV head over G CTAs, then the ordered sum
         const int gs = part ? H / KV : 1;
         train::attn_dkv_mma<HD><<<dim3(nb, KV * gs), 128, M::SMEM_DKV, st>>>(blks, qkv, ld, H, KV, dO, lse, dvec, dqkv,
-                                                                         ld, gs, part, rows);
+                                                                         ld, gs, part, rows, kTheta);
         if (gs > 1) {
             const int64_t n4 = static_cast<int64_t>(rows) * 2 * KV * HD / 4;
             train::dkv_combine<<<cdiv(n4, 256), 256, 0, st>>>(part, gs, rows, 2 * KV * HD, dqkv, ld, H * HD);
@@ -590,10 +601,10 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             attn<T>(hd, 1, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st);
             attn<T>(hd, 2, d_blk, nb, qkv, qkvw, H, KV, nullptr, ts.lse[l], dO, ts.dvec, ts.dqkv, st,
                     std::getenv("OPPO_TRAIN_DKV_NOSPLIT") ? nullptr : ts.dkv_part, Tr);
-            train::rope_rows<float><<<Tr, 128, 0, st>>>(ts.dqkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 1);
-            colsum_into(ts, ts.dqkv, Tr, qkvw, Lt.bqkv.grad, st);
+            if (!use_mma_attn<T>(hd) || std::getenv("OPPO_TRAIN_SIMT_ATTN"))  // (the mma kernels rotate back)
+                train::rope_rows<float><<<Tr, 128, 0, st>>>(ts.dqkv, qkvw, Tr, ts.pos, H + KV, hd, kTheta, 1);
             T* dqc = static_cast<T*>(ts.dqkvc);
-            cvt_f32<T>(ts.dqkv, dqc, static_cast<int64_t>(Tr) * qkvw, st);
+            cvt_colsum_into<T>(ts, ts.dqkv, Tr, qkvw, dqc, Lt.bqkv.grad, st);  // bf16 operand + bias gradient
             // q|k|v projection (qkv = h1 Wqkv^T + b, Wqkv [qkv][D])
             mmt(e, st, dqc, kMN, qkvw, ts.h1[l], kMN, D, qkvw, D, Tr, epi(EPI_ADD_F32, Lt.wqkv.grad, D));
             mmt(e, st, dqc, kK, qkvw, Lw.wqkv, kMN, D, Tr, D, qkvw, epi(EPI_STORE_F32, ts.dh, D));

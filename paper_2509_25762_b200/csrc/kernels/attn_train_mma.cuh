@@ -36,6 +36,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 __device__ __forceinline__ uint32_t ld32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
+// Transpose of the forward's rotate-half RoPE (the backward of q / k) applied
+// to a thread's accumulator fragment of one row: dims dt*8 + 2*tq + e and
+// their rotation partners dims + HD/2 (dt + HD/16) sit in the same thread.
+// Same angle arithmetic as train::rope_rows (powf, sincosf) at position pos.
+template <int HD>
+__device__ __forceinline__ void rope_bwd_frag(float (&f)[HD / 8][4], int i, int tq, int pos, float theta) {
+#pragma unroll
+    for (int dt = 0; dt < HD / 16; ++dt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int d = dt * 8 + 2 * tq + e;
+            float sn, cs;
+            sincosf(static_cast<float>(pos) * powf(theta, -2.0f * d / HD), &sn, &cs);
+            const float a = f[dt][2 * i + e], b = f[dt + HD / 16][2 * i + e];
+            f[dt][2 * i + e] = a * cs + b * sn;
+            f[dt + HD / 16][2 * i + e] = b * cs - a * sn;
+        }
+}
+
 template <int HD>
 struct MmaT {
     static constexpr int RS = HD + 8;        // row-major tile stride (elements)
@@ -212,7 +231,7 @@ template <int HD>
 __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks, const __nv_bfloat16* __restrict__ qkv,
                                                    int ld, int H, int KV, const __nv_bfloat16* __restrict__ dout,
                                                    const float* __restrict__ lse, const float* __restrict__ dvec,
-                                                   float* __restrict__ dqkv, int ldd) {
+                                                   float* __restrict__ dqkv, int ldd, float theta) {
     using M = MmaT<HD>;
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smraw);
@@ -267,6 +286,7 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
         const int row = r0 + g + 8 * i;
         if (row >= nq) continue;
         const size_t r = static_cast<size_t>(b.row0 + b.q0 + row);
+        if (theta > 0.f) rope_bwd_frag<HD>(dq, i, tq, b.q0 + row, theta);  // d q_pre-RoPE
 #pragma unroll
         for (int dt = 0; dt < HD / 8; ++dt) {
             float2 v = make_float2(dq[dt][2 * i] * scale, dq[dt][2 * i + 1] * scale);
@@ -285,7 +305,7 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
                                                     int ld, int H, int KV, const __nv_bfloat16* __restrict__ dout,
                                                     const float* __restrict__ lse, const float* __restrict__ dvec,
                                                     float* __restrict__ dqkv, int ldd, int gsplit, float* __restrict__ part,
-                                                    int rows) {
+                                                    int rows, float theta) {
     using M = MmaT<HD>;
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw);
@@ -345,6 +365,7 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
         const int key = r0 + g + 8 * i;
         if (key >= nk) continue;
         const size_t r = static_cast<size_t>(b.row0 + k0 + key);
+        if (theta > 0.f) rope_bwd_frag<HD>(dk, i, tq, k0 + key, theta);  // linear: partial sums commute
         // gsplit == 1: straight into dqkv's K | V columns; else this part's row
         float* dst = gsplit == 1 ? dqkv + r * ldd + H * HD
                                  : part + (static_cast<size_t>(gs) * rows + r) * (2 * KV * HD);

@@ -368,6 +368,22 @@ static __global__ void colsum_part(const float* __restrict__ x, int rows, int co
     part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
 }
 // stage 2: out[c] += sum over chunks (fixed order)
+// cvt + column sums: y[r][c] = round(x[r][c]), part[chunk][c] = sum over the chunk's rows
+template <class T>
+__global__ void cvt_colsum_part(const float* __restrict__ x, int rows, int cols, int per, T* __restrict__ y,
+                                float* __restrict__ part) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+    float s = 0.f;
+    for (int r = r0; r < r1; ++r) {
+        const float v = x[static_cast<size_t>(r) * cols + c];
+        y[static_cast<size_t>(r) * cols + c] = fromf<T>(v);
+        s += v;
+    }
+    part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
+}
+
 static __global__ void colsum_final(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;

@@ -69,3 +69,52 @@ def test_backward_matches_finite_differences(target):
         fd = (lp - lm) / (2 * e)
         an = g[name][idx] if li is None else g[name][li][idx]
         assert abs(fd - an) <= 1e-6 * max(1.0, abs(fd)), (name, fd, an)
+
+
+def _port_from(w, d):
+    """The CPU port (oracle/cpu_step.py, the reference arm's workload) with the
+    given weights instead of its timing constants."""
+    from oracle import cpu_step as P
+    port = P.Port(d)
+    f = lambda a: np.asarray(a, dtype=np.float32)
+    port.embed, port.lm_head, port.gf = f(w["embed"]), f(w["lm_head"]), f(w["final_norm"])
+    for l, Lw in enumerate(port.layers):
+        Lw.update(wqkv=f(w["wqkv"][l]), bqkv=f(w["bqkv"][l]), wo=f(w["wo"][l]), wgu=f(w["wgu"][l]),
+                  wdown=f(w["wdown"][l]), g1=f(w["ln1"][l]), g2=f(w["ln2"][l]))
+    return port
+
+
+def test_cpu_port_computes_the_oracle_model():
+    """The all-cores CPU port that bench.py times as the reference arm runs
+    the same model as the fp64 oracle: prefill forward, one KV-cache decode
+    step (logits of the last position) and the backward's weight gradients,
+    within fp32 rounding."""
+    w = rand_weights(DIMS, seed=7)
+    d = DIMS
+    tok = np.random.default_rng(8).integers(0, d["vocab"], 19)
+    ref = N.GptNp(d, w)
+    hf_r, lg_r, cache_r = ref.forward(tok, keep=True)
+    port = _port_from(w, d)
+    hf_p, cache_p = port.forward(tok, keep=True)
+    assert np.abs(hf_p - hf_r).max() < 2e-4
+    # decode the last token against the cache of the first T-1 positions
+    T, KV, hd, G = len(tok), d["n_kv_heads"], d["head_dim"], d["n_heads"] // d["n_kv_heads"]
+    _, (acts, *_rest) = port.forward(tok[:-1], keep=True)
+    kv = []
+    for a in acts:
+        K = np.zeros((1, KV, T, hd), np.float32)
+        V = np.zeros((1, KV, T, hd), np.float32)
+        K[0, :, :T - 1] = a["kk"][::G]
+        V[0, :, :T - 1] = a["vv"][::G]
+        kv.append((K, V))
+    lg_dec = port.decode_iteration(1, T, kv, np.random.default_rng(0), tok=[tok[-1]], return_logits=True)
+    assert np.abs(lg_dec[0] - lg_r[-1]).max() < 5e-4 * max(1.0, np.abs(lg_r[-1]).max())
+    # backward of sum(c * hidden) through every layer
+    c = np.random.default_rng(9).standard_normal(hf_r.shape)
+    g_r = ref.backward(cache_r, c)
+    g_p = port.backward(cache_p, c.astype(np.float32))
+    for l in range(d["n_layers"]):
+        gp = g_p[d["n_layers"] - 1 - l]  # port returns layers last-first
+        for name in ("wdown", "wgu", "wo", "wqkv", "bqkv"):
+            a, b = gp[name], g_r[name][l]
+            assert np.abs(a - b).max() <= 1e-3 * max(1.0, np.abs(b).max()), (l, name)
