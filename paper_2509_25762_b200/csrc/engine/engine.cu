@@ -2718,6 +2718,12 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
         float* ws = nullptr;
         const size_t ws_floats = static_cast<size_t>(16) << 20;
         if (epilogue >= 16) OPPO_CUDA_CHECK(cudaMalloc(&ws, ws_floats * 4));
+        __nv_bfloat16* aux = nullptr;  // SwiGLU backward: saved (gate, up) [M][2N]
+        if (epilogue == oppo::EPI_SWIGLU_BWD) {
+            OPPO_CUDA_CHECK(cudaMalloc(&aux, static_cast<size_t>(M) * 2 * N * 2));
+            oppo::init_normal<__nv_bfloat16><<<static_cast<int>((static_cast<size_t>(M) * 2 * N + 255) / 256), 256, 0,
+                                               st>>>(aux, static_cast<int64_t>(M) * 2 * N, 1, 3, 1.0f);
+        }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         auto launch = [&](int i) {
@@ -2725,6 +2731,13 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
                 const int mode = epilogue - 16;
                 oppo::gemm_dec_impl(nullptr, st, x, M, K, K, w + (i % copies) * wn, N, K, mode, y,
                                     mode == oppo::DEC_SWIGLU ? N / 2 : N, nullptr, ws, ws_floats, sms, true);
+            } else if (epilogue == oppo::EPI_SWIGLU_BWD) {
+                oppo::EpiParams ep{};
+                ep.mode = oppo::EPI_SWIGLU_BWD;
+                ep.y = y;
+                ep.ldy = 2 * N;
+                ep.aux = aux;
+                oppo::gemm_with_params(OPPO_DTYPE_BF16, M, N, K, x, w + (i % copies) * wn, ep, st);
             } else if (epilogue == oppo::EPI_LOGITS) {
                 oppo::EpiParams ep{};
                 ep.mode = oppo::EPI_LOGITS;
@@ -2757,6 +2770,7 @@ extern "C" oppo_status oppo_k_gemm_bench(int32_t M, int32_t N, int32_t K, int32_
         if (keys) cudaFree(keys);
         if (tl) cudaFree(tl);
         if (ws) cudaFree(ws);
+        if (aux) cudaFree(aux);
         cudaStreamDestroy(st);
         return OPPO_OK;
     } catch (const oppo::Error& x) {

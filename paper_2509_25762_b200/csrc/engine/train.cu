@@ -219,7 +219,7 @@ void rms_bwd_into(TrainState& ts, const float* x, const float* g, const float* d
         attr = true;
     }
     train::rms_bwd_cs<T><<<nblk, 256, smem, st>>>(x, g, dy, rows, d, per, kEps, dx, dxc, ts.colp);
-    train::colsum_final<<<cdiv(d, 256), 256, 0, st>>>(ts.colp, nblk, d, gout);
+    train::colsum_final<<<cdiv(d, 32), 256, 0, st>>>(ts.colp, nblk, d, gout);
 }
 
 // y = x rounded to T and out += column sums of x, in one pass over x
@@ -229,7 +229,7 @@ void cvt_colsum_into(TrainState& ts, const float* x, int rows, int cols, T* y, f
     const int chunks = std::min(kColParts, std::max(1, rows / 64));
     const int per = cdiv(rows, chunks);
     train::cvt_colsum_part<T><<<dim3(cdiv(cols, 256), chunks), 256, 0, st>>>(x, rows, cols, per, y, ts.colp);
-    train::colsum_final<<<cdiv(cols, 256), 256, 0, st>>>(ts.colp, chunks, cols, out);
+    train::colsum_final<<<cdiv(cols, 32), 256, 0, st>>>(ts.colp, chunks, cols, out);
 }
 
 void colsum_into(TrainState& ts, const float* x, int rows, int cols, float* out, cudaStream_t st) {
@@ -237,7 +237,7 @@ void colsum_into(TrainState& ts, const float* x, int rows, int cols, float* out,
     const int chunks = std::min(64, std::max(1, rows / 64));
     const int per = cdiv(rows, chunks);
     train::colsum_part<<<dim3(cdiv(cols, 256), chunks), 256, 0, st>>>(x, rows, cols, cols, per, ts.colp);
-    train::colsum_final<<<cdiv(cols, 256), 256, 0, st>>>(ts.colp, chunks, cols, out);
+    train::colsum_final<<<cdiv(cols, 32), 256, 0, st>>>(ts.colp, chunks, cols, out);
 }
 
 template <class T>

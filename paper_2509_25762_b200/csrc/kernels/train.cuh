@@ -384,12 +384,25 @@ __global__ void cvt_colsum_part(const float* __restrict__ x, int rows, int cols,
     part[static_cast<size_t>(blockIdx.y) * cols + c] = s;
 }
 
-static __global__ void colsum_final(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= cols) return;
+// out[c] += sum over chunks of part[k][c]: block = 32 columns x 8 warps; warp w
+// sums chunks w, w+8, ... (lane = column, coalesced), then the 8 warp sums are
+// added in warp order -- deterministic for a given chunk count.
+static __global__ void __launch_bounds__(256) colsum_final(const float* __restrict__ part, int chunks, int cols,
+                                                           float* __restrict__ out) {
+    __shared__ float ws[8][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 32 + lane;
     float s = 0.f;
-    for (int k = 0; k < chunks; ++k) s += part[static_cast<size_t>(k) * cols + c];
-    out[c] += s;
+    if (c < cols)
+        for (int k = warp; k < chunks; k += 8) s += part[static_cast<size_t>(k) * cols + c];
+    ws[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && c < cols) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += ws[w][lane];
+        out[c] += t;
+    }
 }
 
 // ----------------------------------------------------------------- misc
