@@ -92,6 +92,10 @@ bool tc2sm_long_enabled() {  // read per call so tests can compare both kernels 
     const char* v = std::getenv("OPPO_TC2SM_LONGK");
     return v ? std::atoi(v) != 0 : true;  // measured: update 912 -> 887 ms at 39K tokens
 }
+bool raster_n_fast() {  // read per call (A/B in one process)
+    const char* v = std::getenv("OPPO_RASTER_N");
+    return v ? std::atoi(v) != 0 : true;
+}
 bool tc2sm_short_enabled() {  // read per call (A/B in one process)
     const char* v = std::getenv("OPPO_TC2SM_SHORT");
     return v ? std::atoi(v) != 0 : false;
@@ -145,15 +149,22 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // (bench: update 60 -> 69 ms on the persistent kernel; O / down no gain).
     const bool light = ep.mode == EPI_STORE || ep.mode == EPI_SWIGLU || ep.mode == EPI_ROPE_APPEND;
     const int pm = persist_mode();
-    if (m_tiles >= 8 && light && !mn && dtype == OPPO_DTYPE_BF16 && (pm == 1 || (pm == 2 && ep.update_gemm))) {
+    // (2: the update's GEMMs with any epilogue but the logits one, K-major or MN-major operands)
+    // (long-K gradient GEMMs stay on the CTA-pair kernel below)
+    const bool pair_long = ep.pair_long_k && tc2sm_long_enabled() && (K + 63) / 64 >= 64;
+    const bool persist = dtype == OPPO_DTYPE_BF16 && m_tiles >= 8 &&
+                         ((pm == 1 && light && !mn) ||
+                          (pm == 2 && ep.update_gemm && ep.mode != EPI_LOGITS && !pair_long));
+    if (persist) {
         // 128-wide tiles where a 256-wide last tile would waste > 5% (N = 896, 1152)
         const int pad256 = (N + 255) / 256 * 256 - N;
         const int BNp = (N % 128 == 0 && pad256 * 20 > N) ? 128 : 256;
         sh.splits = 1;
         sh.kb_per_split = (K + 63) / 64;
+        sh.n_fast = raster_n_fast();
         CUtensorMap s1, s2;
-        const CUtensorMap& mx = cached_map(e, x, M, K, ldx, 128, s1);
-        const CUtensorMap& mw = cached_map(e, wt, N, K, ldw, BNp, s2);
+        const CUtensorMap& mx = a_mn ? cached_map(e, x, K, M, ldx, 64, s1) : cached_map(e, x, M, K, ldx, 128, s1);
+        const CUtensorMap& mw = b_mn ? cached_map(e, wt, K, N, ldw, 64, s2) : cached_map(e, wt, N, K, ldw, BNp, s2);
         const int total = m_tiles * ((N + BNp - 1) / BNp);
         const dim3 grid(std::min(total, num_sms));
         if (BNp == 256) {
@@ -163,7 +174,8 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      tc::CfgP<256>::SMEM));
             });
-            launch(e && e->pdl, tc::gemm_bf16_persist<256>, grid, dim3(192), tc::CfgP<256>::SMEM, st, mx, mw, sh, ep);
+            launch(e && e->pdl, tc::gemm_bf16_persist<256>, grid, dim3(tc::kPersistThreads), tc::CfgP<256>::SMEM, st,
+                   mx, mw, sh, ep);
         } else {
             static std::once_flag a128;
             std::call_once(a128, [] {
@@ -171,7 +183,8 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      tc::CfgP<128>::SMEM));
             });
-            launch(e && e->pdl, tc::gemm_bf16_persist<128>, grid, dim3(192), tc::CfgP<128>::SMEM, st, mx, mw, sh, ep);
+            launch(e && e->pdl, tc::gemm_bf16_persist<128>, grid, dim3(tc::kPersistThreads), tc::CfgP<128>::SMEM, st,
+                   mx, mw, sh, ep);
         }
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
@@ -204,12 +217,15 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         const CUtensorMap& mx = a_mn ? cached_map(e, x, K, M, ldx, 64, s1) : cached_map(e, x, M, K, ldx, 128, s1);
         const CUtensorMap& mw = b_mn ? cached_map(e, wt, K, N, ldw, 64, s2) : cached_map(e, wt, N, K, ldw, 128, s2);
         const int mt2 = (m_tiles + 1) / 2 * 2;  // whole CTA pairs (OOB rows zero-filled)
+        sh.n_fast = raster_n_fast();
+        const dim3 grid2 = sh.n_fast ? dim3(2 * ((N + 255) / 256), mt2 / 2) : dim3(mt2, (N + 255) / 256);
+        const dim3 clu(2, 1, 1);
         if (long2)
-            launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm<6>, dim3(mt2, (N + 255) / 256), dim3(128),
-                           tc::Cfg2Sm<6>::SMEM, st, mx, mw, sh, ep);
+            launch_cluster(e && e->pdl, clu, tc::gemm_bf16_tc2sm<6>, grid2, dim3(128), tc::Cfg2Sm<6>::SMEM, st, mx, mw,
+                           sh, ep);
         else
-            launch_cluster(e && e->pdl, dim3(2, 1, 1), tc::gemm_bf16_tc2sm<3>, dim3(mt2, (N + 255) / 256), dim3(128),
-                           tc::Cfg2Sm<3>::SMEM, st, mx, mw, sh, ep);
+            launch_cluster(e && e->pdl, clu, tc::gemm_bf16_tc2sm<3>, grid2, dim3(128), tc::Cfg2Sm<3>::SMEM, st, mx, mw,
+                           sh, ep);
         OPPO_CUDA_CHECK(cudaGetLastError());
         return;
     }
@@ -270,7 +286,12 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // MN-major operands are stored [K][M] / [K][N]: [64 k][64] boxes
     const CUtensorMap& mx = a_mn ? cached_map(e, x, K, M, ldx, 64, s1) : cached_map(e, x, M, K, ldx, 128, s1);
     const CUtensorMap& mw = b_mn ? cached_map(e, wt, K, N, ldw, 64, s2) : cached_map(e, wt, N, K, ldw, BN, s2);
-    const dim3 grid(m_tiles, n_tiles, splits);
+    // token-rich GEMMs: feature tiles fastest, so the CTAs reading one token
+    // tile run together (a 32K-row update GEMM re-read its 59 MB token operand
+    // from DRAM once per feature tile with the m-fast order: 1.57 GB read by
+    // the SwiGLU-backward GEMM for 0.64 GB of algorithmic reads)
+    sh.n_fast = m_tiles >= 8 && raster_n_fast();
+    const dim3 grid = sh.n_fast ? dim3(n_tiles, m_tiles, splits) : dim3(m_tiles, n_tiles, splits);
     switch (BN) {
     case 64:
         launch_tc<64>(mx, mw, grid, sh, ep, st, e && e->pdl);

@@ -144,6 +144,38 @@ def test_gemm_cta_pair_short_k(monkeypatch, a_mn, b_mn):
         assert rel < 2e-4, rel
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(2048, 896, 896), (1536, 4864, 896), (1104, 1152, 960)])
+def test_gemm_persistent_update_path(monkeypatch, a_mn, b_mn, M, N, K):
+    """The persistent double-buffered-TMEM GEMM as the PPO update uses it
+    (OPPO_GEMM_PERSIST=2: 8 epilogue warps, K-major or MN-major operands,
+    f32 store / f32 add epilogues): bit-identical to the 2-CTA/SM kernel
+    (same tiles, same K order) and within fp32 noise of float64."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + a_mn + 2 * b_mn)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    a_st = a.t().contiguous() if a_mn else a
+    b_st = b.t().contiguous() if b_mn else b
+    y0 = torch.randn(M, N, device="cuda", generator=g)
+
+    def run(epi):
+        y = y0.clone()
+        st = _lib().oppo_k_gemm_t(1, M, N, K, _ptr(a_st), a_mn, M if a_mn else K, _ptr(b_st), b_mn,
+                                  N if b_mn else K, _ptr(y), epi, _stream())
+        assert st == 0, _lib().oppo_last_error_global()
+        return y
+
+    for epi in (EPI_STORE_F32, EPI_ADD_F32):
+        monkeypatch.setenv("OPPO_GEMM_PERSIST", "2")
+        yp = run(epi)
+        monkeypatch.setenv("OPPO_GEMM_PERSIST", "0")
+        yt = run(epi)
+        assert torch.equal(yp, yt), epi
+        ref = a.double() @ b.double().T + (y0.double() if epi == EPI_ADD_F32 else 0)
+        rel = ((yp.double() - ref).abs().max() / ref.abs().max()).item()
+        assert rel < 2e-4, rel
+
+
 def test_gemm_bf16_store_f32_long_k():
     # fp32 output isolates the tensor-core fp32 accumulation error over a long K
     M, N, K = 32, 256, 8192
