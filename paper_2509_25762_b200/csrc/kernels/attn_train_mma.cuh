@@ -58,31 +58,24 @@ __device__ __forceinline__ void rope_bwd_frag(float (&f)[HD / 8][4], int i, int 
 template <int HD>
 struct MmaT {
     static constexpr int RS = HD + 8;        // row-major tile stride (elements)
-    static constexpr int TS = kMBlk + 8;     // transposed tile stride
     static constexpr int ROW = kMBlk * RS;   // elements of a row-major tile
-    static constexpr int TR = HD * TS;       // elements of a transposed tile
-    static constexpr int SMEM_FWD = (2 * ROW + TR) * 2;
-    static constexpr int SMEM_DQ = (4 * ROW + TR) * 2;
-    static constexpr int SMEM_DKV = (4 * ROW + 2 * TR) * 2 + 2 * kMBlk * 4;
+    static constexpr int SMEM_FWD = 3 * ROW * 2;
+    static constexpr int SMEM_DQ = 4 * ROW * 2;
+    static constexpr int SMEM_DKV = 4 * ROW * 2 + 2 * kMBlk * 4;
 };
 
 // rows [r0, r0 + n) of columns [col, col + HD) of a row-major bf16 matrix ->
-// smem (row-major, stride RS; zero rows beyond n) and optionally transposed (stride TS)
+// smem (row-major, stride RS; zero rows beyond n)
 template <int HD>
-__device__ __forceinline__ void load_rows(__nv_bfloat16* dst, __nv_bfloat16* dstT, const __nv_bfloat16* __restrict__ src,
-                                          size_t ld, int r0, int n, int col) {
+__device__ __forceinline__ void load_rows(__nv_bfloat16* dst, const __nv_bfloat16* __restrict__ src, size_t ld,
+                                          int r0, int n, int col) {
     using M = MmaT<HD>;
     constexpr int VPR = HD / 8;  // 16-byte vectors per row
     for (int i = threadIdx.x; i < kMBlk * VPR; i += blockDim.x) {
         const int r = i / VPR, c = (i % VPR) * 8;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (r < n) v = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(r0 + r) * ld + col + c);
-        if (dst) *reinterpret_cast<uint4*>(dst + r * M::RS + c) = v;
-        if (dstT) {
-            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dstT[(c + k) * M::TS + r] = e[k];
-        }
+        *reinterpret_cast<uint4*>(dst + r * M::RS + c) = v;
     }
 }
 
@@ -118,12 +111,21 @@ __device__ __forceinline__ void qk_tile(float (&acc)[8][4], const __nv_bfloat16*
     }
 }
 
-// out[dt] (16 x HD) += P (16 x 64 in registers, C layout) . Bt^T where Bt is a
-// transposed smem tile [HD][64]
+// out[dt] (16 x HD) += P (16 x 64 in registers, C layout) . B where B is a
+// row-major smem tile [64 keys][HD] (stride RS): the col-major B fragments
+// (pairs along the key dimension) come straight from ldmatrix .trans, two
+// 8-column d blocks per ldmatrix.x4 -- no transposed copy of the tile.
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
 template <int HD>
-__device__ __forceinline__ void pv_tile(float (&out)[HD / 8][4], const float (&p)[8][4], const __nv_bfloat16* bt,
-                                        int g, int tq) {
+__device__ __forceinline__ void pv_tile(float (&out)[HD / 8][4], const float (&p)[8][4], const __nv_bfloat16* b,
+                                        int lane) {
     using M = MmaT<HD>;
+    // this lane's ldmatrix row: matrix lane/8 = (key half, d block), row lane%8
+    const int key_off = (lane & 7) + ((lane >> 3) & 1) * 8, d_off = (lane >> 4) * 8;
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc) {
         uint32_t a[4];
@@ -132,9 +134,11 @@ __device__ __forceinline__ void pv_tile(float (&out)[HD / 8][4], const float (&p
         a[2] = pack_bf16(p[2 * kc + 1][0], p[2 * kc + 1][1]);
         a[3] = pack_bf16(p[2 * kc + 1][2], p[2 * kc + 1][3]);
 #pragma unroll
-        for (int dt = 0; dt < HD / 8; ++dt) {
-            const __nv_bfloat16* br = bt + (dt * 8 + g) * M::TS + kc * 16 + 2 * tq;
-            mma16816(out[dt], a, ld32(br), ld32(br + 8));
+        for (int dt = 0; dt < HD / 8; dt += 2) {
+            uint32_t r[4];
+            ldsm_x4_trans(r, b + (kc * 16 + key_off) * M::RS + dt * 8 + d_off);
+            mma16816(out[dt], a, r[0], r[1]);
+            mma16816(out[dt + 1], a, r[2], r[3]);
         }
     }
 }
@@ -147,14 +151,14 @@ __global__ void __launch_bounds__(128) attn_fwd_mma(const TBlk* __restrict__ blk
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smraw);
     __nv_bfloat16* Ks = Qs + M::ROW;
-    __nv_bfloat16* Vt = Ks + M::ROW;
+    __nv_bfloat16* Vs = Ks + M::ROW;
     const TBlk b = blks[blockIdx.x];
     const int h = blockIdx.y, kvh = h / (H / KV);
     const int nq = min(kMBlk, b.len - b.q0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;
     const float scale = rsqrtf(static_cast<float>(HD));
-    load_rows<HD>(Qs, nullptr, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    load_rows<HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
     float o[HD / 8][4];
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt)
@@ -164,8 +168,8 @@ __global__ void __launch_bounds__(128) attn_fwd_mma(const TBlk* __restrict__ blk
     for (int k0 = 0; k0 < b.q0 + nq; k0 += kMBlk) {
         const int nk = min(kMBlk, b.len - k0);
         __syncthreads();
-        load_rows<HD>(Ks, nullptr, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
-        load_rows<HD>(nullptr, Vt, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+        load_rows<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+        load_rows<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
         __syncthreads();
         float s[8][4];
         qk_tile<HD>(s, Qs, r0, Ks, g, tq);
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(128) attn_fwd_mma(const TBlk* __restrict__ blk
             o[dt][2] *= corr[1];
             o[dt][3] *= corr[1];
         }
-        pv_tile<HD>(o, s, Vt, g, tq);
+        pv_tile<HD>(o, s, Vs, lane);
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -238,15 +242,14 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
     __nv_bfloat16* dOs = Qs + M::ROW;
     __nv_bfloat16* Vs = dOs + M::ROW;
     __nv_bfloat16* Ks = Vs + M::ROW;
-    __nv_bfloat16* Kt = Ks + M::ROW;
     const TBlk b = blks[blockIdx.x];
     const int h = blockIdx.y, kvh = h / (H / KV);
     const int nq = min(kMBlk, b.len - b.q0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;
     const float scale = rsqrtf(static_cast<float>(HD));
-    load_rows<HD>(Qs, nullptr, qkv, ld, b.row0 + b.q0, nq, h * HD);
-    load_rows<HD>(dOs, nullptr, dout, static_cast<size_t>(H) * HD, b.row0 + b.q0, nq, h * HD);
+    load_rows<HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    load_rows<HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + b.q0, nq, h * HD);
     float lr[2], dr[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -263,8 +266,8 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
     for (int k0 = 0; k0 < b.q0 + nq; k0 += kMBlk) {
         const int nk = min(kMBlk, b.len - k0);
         __syncthreads();
-        load_rows<HD>(Ks, Kt, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
-        load_rows<HD>(Vs, nullptr, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+        load_rows<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+        load_rows<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
         __syncthreads();
         float s[8][4], dp[8][4];
         qk_tile<HD>(s, Qs, r0, Ks, g, tq);    // S = Q K^T
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
                 const float p = ok ? __expf(s[nt][c] * scale - lr[i]) : 0.f;
                 s[nt][c] = p * (dp[nt][c] - dr[i]);  // dS
             }
-        pv_tile<HD>(dq, s, Kt, g, tq);  // dQ += dS K  (Kt is K^T: [d][key])
+        pv_tile<HD>(dq, s, Ks, lane);  // dQ += dS K
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -312,9 +315,7 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
     __nv_bfloat16* Vs = Ks + M::ROW;
     __nv_bfloat16* Qs = Vs + M::ROW;
     __nv_bfloat16* dOs = Qs + M::ROW;
-    __nv_bfloat16* Qt = dOs + M::ROW;
-    __nv_bfloat16* dOt = Qt + M::TR;
-    float* lse_s = reinterpret_cast<float*>(dOt + M::TR);
+    float* lse_s = reinterpret_cast<float*>(dOs + M::ROW);
     float* d_s = lse_s + kMBlk;
     const TBlk b = blks[blockIdx.x];  // q0 = key block start
     const int kvh = blockIdx.y / gsplit, gs = blockIdx.y % gsplit, G = H / KV;
@@ -323,8 +324,8 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;  // this warp's 16 keys
     const float scale = rsqrtf(static_cast<float>(HD));
-    load_rows<HD>(Ks, nullptr, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
-    load_rows<HD>(Vs, nullptr, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+    load_rows<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+    load_rows<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
     float dk[HD / 8][4], dv[HD / 8][4];
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt)
@@ -335,8 +336,8 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
         for (int q0 = k0; q0 < b.len; q0 += kMBlk) {
             const int nq = min(kMBlk, b.len - q0);
             __syncthreads();
-            load_rows<HD>(Qs, Qt, qkv, ld, b.row0 + q0, nq, h * HD);
-            load_rows<HD>(dOs, dOt, dout, static_cast<size_t>(H) * HD, b.row0 + q0, nq, h * HD);
+            load_rows<HD>(Qs, qkv, ld, b.row0 + q0, nq, h * HD);
+            load_rows<HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + q0, nq, h * HD);
             for (int i = threadIdx.x; i < kMBlk; i += blockDim.x) {
                 const size_t r = static_cast<size_t>(b.row0 + q0 + min(i, nq - 1));
                 lse_s[i] = lse[r * H + h];
@@ -356,8 +357,8 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
                     st[nt][c] = p;
                     dpt[nt][c] = p * (dpt[nt][c] - d_s[qi]);  // dS^T
                 }
-            pv_tile<HD>(dv, st, dOt, g, tq);  // dV += P^T dO
-            pv_tile<HD>(dk, dpt, Qt, g, tq);  // dK += dS^T Q
+            pv_tile<HD>(dv, st, dOs, lane);  // dV += P^T dO
+            pv_tile<HD>(dk, dpt, Qs, lane);  // dK += dS^T Q
         }
     }
 #pragma unroll

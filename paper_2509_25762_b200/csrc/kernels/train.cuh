@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(256) attn_train_dkv(const TBlk* __restrict__ b
 // shared-memory row, then the 8 rows are summed in warp order into
 // part[b][c] -- deterministic, and no [rows, d] scratch round trip.
 // colsum_final(part, gridDim.x, d, out) adds the block partials in order.
+constexpr int kRmsRegs = 28;  // register path up to d = 896 (28 columns per lane)
 template <class T>
 __global__ void __launch_bounds__(256) rms_bwd_cs(const float* __restrict__ x, const float* __restrict__ g,
                                                   const float* __restrict__ dy, int rows, int d, int per, float eps,
@@ -327,6 +328,52 @@ __global__ void __launch_bounds__(256) rms_bwd_cs(const float* __restrict__ x, c
     float* acc = acc_s + warp * d;
     for (int c = lane; c < d; c += 32) acc[c] = 0.f;
     const int r_end = min(rows, (blockIdx.x + 1) * per);
+    if (d <= 32 * kRmsRegs) {  // the row's x, dy and dx in registers: every load issued up front
+        constexpr int NR = kRmsRegs;
+        float gv[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) gv[k] = lane + 32 * k < d ? g[lane + 32 * k] : 0.f;
+        float ac[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) ac[k] = 0.f;
+        for (int r = blockIdx.x * per + warp; r < r_end; r += 8) {
+            const float* xr = x + static_cast<size_t>(r) * d;
+            const float* dr = dy + static_cast<size_t>(r) * d;
+            float* o = dx + static_cast<size_t>(r) * d;
+            float xv[NR], dv[NR], ov[NR];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int c = lane + 32 * k;
+                const bool ok = c < d;
+                xv[k] = ok ? xr[c] : 0.f;
+                dv[k] = ok ? dr[c] : 0.f;
+                ov[k] = ok ? o[c] : 0.f;
+            }
+            float ss = 0.f;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) ss = fmaf(xv[k], xv[k], ss);
+            ss = warp_sum(ss);
+            const float rs = rsqrtf(ss / d + eps);
+            float dot = 0.f;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) dot = fmaf(dv[k] * gv[k], xv[k] * rs, dot);
+            dot = warp_sum(dot) / d;
+            T* oc = dxc ? dxc + static_cast<size_t>(r) * d : nullptr;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int c = lane + 32 * k;
+                if (c >= d) continue;
+                const float xh = xv[k] * rs;
+                const float v = ov[k] + rs * (dv[k] * gv[k] - xh * dot);
+                o[c] = v;
+                if (oc) oc[c] = fromf<T>(v);
+                ac[k] += dv[k] * xh;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (lane + 32 * k < d) acc[lane + 32 * k] = ac[k];
+    } else
     for (int r = blockIdx.x * per + warp; r < r_end; r += 8) {
         const float* xr = x + static_cast<size_t>(r) * d;
         const float* dr = dy + static_cast<size_t>(r) * d;
