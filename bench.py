@@ -178,7 +178,8 @@ def run_arm(eng, wl, cfg, seed, steps, warmup, rank, world, dist):
                         prefill_tokens=led.prefill_tokens, launches=led.kernel_launches,
                         h2d=marks["prompts"][r.step] + r.finished * C.sizeof(abi.SeqState),
                         d2h=C.sizeof(abi.StepRecord) + C.sizeof(abi.Ledger) + int(r.batch_tokens) * 4 + r.finished * 4,
-                        tokens=int(r.batch_tokens), reward=r.mean_reward, obj=r.ppo_loss))
+                        tokens=int(r.batch_tokens), reward=r.mean_reward, obj=r.ppo_loss,
+                        util_actor=r.util_generation, util_scorer=r.util_scoring))
     return out, wall
 
 
@@ -535,6 +536,10 @@ def ours(args):
         "update_ms": round(np.mean([r["update_us"] for r in rec]) / 1e3, 2),
         "tokens_per_step": int(np.mean([r["tokens"] for r in rec])),
         "prefill_tokens_per_step": int(np.mean([r["prefill_tokens"] for r in rec])),
+        # measured SM-partition utilization over the generation+scoring device time
+        # (engine.cpp:225-233): actor decode loop, and the scorer waves' busy spans
+        "util_actor_partition": round(float(np.mean([r["util_actor"] for r in rec])), 4),
+        "util_scorer_partition": round(float(np.mean([r["util_scorer"] for r in rec])), 4),
     }
     line["roofline"] = decode_roofline(rec, hbm, peak_src, wl["actor"])
     line["step_roofline"] = step_roofline(rec, wl, hbm, tf_sust)

@@ -109,6 +109,10 @@ typedef struct oppo_ledger {
     double decode_flops;
     double prefill_flops;
     double prefill_bytes;
+    /* measured busy time of the scorer partition: the sum over the step's
+     * waves of (wave end - wave start) on the scorer stream (engine.cpp:225-233's
+     * busy_scoring, in us); the actor partition's is decode_loop_us */
+    double score_busy_us;
 } oppo_ledger;
 
 enum { OPPO_MODE_STREAMED = 0, OPPO_MODE_SEQUENTIAL = 1 };      /* ScheduleMode */

@@ -51,7 +51,7 @@ class Ledger(C.Structure):
                 ("prefill_tokens", C.c_int64), ("kernel_launches", C.c_int64),
                 ("decode_loop_us", C.c_double), ("decode_weight_bytes", C.c_double),
                 ("decode_kv_bytes", C.c_double), ("decode_flops", C.c_double),
-                ("prefill_flops", C.c_double), ("prefill_bytes", C.c_double)]
+                ("prefill_flops", C.c_double), ("prefill_bytes", C.c_double), ("score_busy_us", C.c_double)]
 
 
 class Latency(C.Structure):

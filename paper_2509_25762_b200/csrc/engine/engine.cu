@@ -898,6 +898,7 @@ void engine_free(Engine* e) {
         if (ev) cudaEventDestroy(ev);
     for (cudaStream_t sm : e->ss_m)
         if (sm) cudaStreamDestroy(sm);
+    for (cudaEvent_t ev : e->ev_wave) cudaEventDestroy(ev);
     for (cudaEvent_t ev : {e->ev_begin, e->ev_dec_end, e->ev_sc_end, e->ev_done, e->ev_loop0, e->ev_fork, e->ev_join,
                            e->ev_pre})
         if (ev) cudaEventDestroy(ev);
@@ -1537,6 +1538,11 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     set_int<<<1, 1, 0, e.sa>>>(e.d_iter, 1);
 
     // ------------------------------------------------------------- enqueue
+    while (e.ev_wave.size() < 2 * waves.size()) {
+        cudaEvent_t ev;
+        OPPO_CUDA_CHECK(cudaEventCreate(&ev));
+        e.ev_wave.push_back(ev);
+    }
     if (e.ev_pool.size() < waves.size() + 2) {
         const size_t old = e.ev_pool.size();
         e.ev_pool.resize(waves.size() + 2);
@@ -1566,10 +1572,13 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
             cudaEvent_t ev = e.ev_pool[wi + 1];
             OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));  // actor-stream order: after iteration `it`
             const WavePlan* wave = &waves[wi];
-            worker.post([&e, &A, &prefill_tokens, ev, wave] {
+            cudaEvent_t t0 = e.ev_wave[2 * wi], t1 = e.ev_wave[2 * wi + 1];
+            worker.post([&e, &A, &prefill_tokens, ev, wave, t0, t1] {
                 OPPO_CUDA_CHECK(cudaStreamWaitEvent(e.ss, ev, 0));
+                OPPO_CUDA_CHECK(cudaEventRecord(t0, e.ss));  // the wave's chunks are ready
                 int64_t tok = 0;
                 for (const auto& p : wave->passes) run_scorer_pass<T>(e, p, A, e.ss, tok);
+                OPPO_CUDA_CHECK(cudaEventRecord(t1, e.ss));  // (passes end joined back on ss)
                 prefill_tokens += tok;
             });
             ++wi;
@@ -1640,6 +1649,12 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
     ledger.decode_us = ms * 1e3;
     OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_begin, e.ev_sc_end));
     ledger.score_us = ms * 1e3;
+    double busy = 0;  // scorer partition busy time: sum of the waves' spans
+    for (size_t k = 0; k < waves.size(); ++k) {
+        OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_wave[2 * k], e.ev_wave[2 * k + 1]));
+        busy += ms * 1e3;
+    }
+    ledger.score_busy_us = busy;
     OPPO_CUDA_CHECK(cudaEventElapsedTime(&ms, e.ev_loop0, e.ev_dec_end));
     ledger.decode_loop_us = ms * 1e3;
     ledger.decode_weight_bytes = loop_w;

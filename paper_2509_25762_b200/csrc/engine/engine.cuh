@@ -172,6 +172,7 @@ struct Engine {
     cudaStream_t sa = nullptr, ss = nullptr;
     cudaStream_t su = nullptr;  // admission prefill + PPO update: whole GPU (== sa without a partition)
     std::vector<cudaEvent_t> ev_pool;
+    std::vector<cudaEvent_t> ev_wave;  // timing events around each scorer wave (start, end): partition busy time
     cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr,
                 ev_loop0 = nullptr;
     bool step_open = false;

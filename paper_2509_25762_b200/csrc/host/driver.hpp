@@ -150,7 +150,11 @@ inline int run_seed_loop(const oppo_run_config& cfg, uint64_t seed, LoopHooks& h
             rec.has_controller_stat = up.stat.has_value();
             rec.controller_stat = up.stat.value_or(0.0);
             rec.mean_reward = reward;
-            if (ledger.wall > 0) {  // utilization (engine.cpp:225-233)
+            if (ledger.step_us > 0.0) {  // utilization (engine.cpp:225-233), measured on the GPU:
+                // busy time of each SM partition over the step's device time
+                rec.util_generation = ledger.decode_loop_us / ledger.step_us;
+                rec.util_scoring = ledger.score_busy_us / ledger.step_us;
+            } else if (ledger.wall > 0) {  // logical executor: the reference's tick ledger
                 rec.util_generation = double(ledger.busy_generation) / double(ledger.wall);
                 rec.util_scoring = double(ledger.busy_scoring) / double(ledger.wall);
             }

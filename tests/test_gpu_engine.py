@@ -619,3 +619,23 @@ def test_run_seed_ex_prompt_source_and_kv_admission_control():
     assert sel != lsel  # the deferrals changed the schedule (the test is not vacuous)
     eng.close()
 
+
+
+def test_measured_partition_utilization():
+    """engine.cpp:225-233's utilization on the GPU: the step loop's records
+    carry the actor partition's decode-loop time and the scorer partition's
+    summed wave spans over the step's device time (streamed: both busy; the
+    scorer's share smaller than the decode's for this small step)."""
+    shape = dict(n_layers=2, d_model=256, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=512, vocab=2048, tied=1)
+    eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=24, max_prompt_len=16, max_response_len=96,
+                 sample_seed=SAMPLE_SEED, train_heads=0)
+    cfg = S.default_config(mode=abi.RUN_TRAIN, steps=3, batch_size=8, prompt_len=16, delta_init=2, delta_min=0,
+                           delta_max=2, chunk_size=16, schedule_mode=abi.MODE_STREAMED, lengths_kind=abi.LEN_LOGNORMAL,
+                           lengths_mu_log=3.5, lengths_sigma_log=0.6, lengths_cap=96, ppo_learning_rate=0.0,
+                           ppo_value_learning_rate=0.0)
+    recs, _, leds = eng.run_seed_ex(cfg, 5)
+    eng.close()
+    for r, led in zip(recs, leds):
+        assert led.step_us > 0 and led.score_busy_us > 0
+        assert 0.0 < r.util_generation <= 1.01 and 0.0 < r.util_scoring <= 1.01, (r.util_generation, r.util_scoring)
+        assert abs(r.util_generation - led.decode_loop_us / led.step_us) < 1e-9
