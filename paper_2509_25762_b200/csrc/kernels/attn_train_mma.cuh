@@ -59,9 +59,9 @@ template <int HD>
 struct MmaT {
     static constexpr int RS = HD + 8;        // row-major tile stride (elements)
     static constexpr int ROW = kMBlk * RS;   // elements of a row-major tile
-    static constexpr int SMEM_FWD = 3 * ROW * 2;
-    static constexpr int SMEM_DQ = 4 * ROW * 2;
-    static constexpr int SMEM_DKV = 4 * ROW * 2 + 2 * kMBlk * 4;
+    static constexpr int SMEM_FWD = 5 * ROW * 2;  // Q + double-buffered K, V
+    static constexpr int SMEM_DQ = 6 * ROW * 2;   // Q, dO + double-buffered K, V
+    static constexpr int SMEM_DKV = 6 * ROW * 2 + 4 * kMBlk * 4;  // K, V + double-buffered Q, dO, lse, dvec
 };
 
 // rows [r0, r0 + n) of columns [col, col + HD) of a row-major bf16 matrix ->
@@ -78,6 +78,30 @@ __device__ __forceinline__ void load_rows(__nv_bfloat16* dst, const __nv_bfloat1
         *reinterpret_cast<uint4*>(dst + r * M::RS + c) = v;
     }
 }
+
+// The same with cp.async (16-byte copies into smem, L2 only); rows beyond n
+// are zeroed with plain stores.  Complete after cp_async_wait + __syncthreads.
+template <int HD>
+__device__ __forceinline__ void load_rows_async(__nv_bfloat16* dst, const __nv_bfloat16* __restrict__ src, size_t ld,
+                                                int r0, int n, int col) {
+    using M = MmaT<HD>;
+    constexpr int VPR = HD / 8;
+    for (int i = threadIdx.x; i < kMBlk * VPR; i += blockDim.x) {
+        const int r = i / VPR, c = (i % VPR) * 8;
+        __nv_bfloat16* d = dst + r * M::RS + c;
+        if (r < n) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(d))),
+                         "l"(src + static_cast<size_t>(r0 + r) * ld + col + c)
+                         : "memory");
+        } else {
+            *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+        }
+    }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // A fragment (16 rows x 16 k) of a row-major smem tile at (row0, k0)
 template <int HD>
@@ -150,27 +174,41 @@ __global__ void __launch_bounds__(128) attn_fwd_mma(const TBlk* __restrict__ blk
     using M = MmaT<HD>;
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smraw);
-    __nv_bfloat16* Ks = Qs + M::ROW;
-    __nv_bfloat16* Vs = Ks + M::ROW;
     const TBlk b = blks[blockIdx.x];
     const int h = blockIdx.y, kvh = h / (H / KV);
     const int nq = min(kMBlk, b.len - b.q0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;
     const float scale = rsqrtf(static_cast<float>(HD));
-    load_rows<HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    // key block j's K, V in buffer j & 1; block j + 1 is copied in while j computes
+    auto kv_issue = [&](int j) {
+        __nv_bfloat16* kb = Qs + M::ROW * (1 + 2 * (j & 1));
+        const int kk0 = j * kMBlk;
+        load_rows_async<HD>(kb, qkv, ld, b.row0 + kk0, min(kMBlk, b.len - kk0), (H + kvh) * HD);
+        load_rows_async<HD>(kb + M::ROW, qkv, ld, b.row0 + kk0, min(kMBlk, b.len - kk0), (H + KV + kvh) * HD);
+        cp_async_commit();
+    };
+    load_rows_async<HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    kv_issue(0);
     float o[HD / 8][4];
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt)
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[dt][c] = 0.f;
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-    for (int k0 = 0; k0 < b.q0 + nq; k0 += kMBlk) {
+    const int nblk = (b.q0 + nq + kMBlk - 1) / kMBlk;
+    for (int j = 0; j < nblk; ++j) {
+        const int k0 = j * kMBlk;
         const int nk = min(kMBlk, b.len - k0);
+        if (j + 1 < nblk) {
+            kv_issue(j + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        load_rows<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
-        load_rows<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
-        __syncthreads();
+        const __nv_bfloat16* Ks = Qs + M::ROW * (1 + 2 * (j & 1));
+        const __nv_bfloat16* Vs = Ks + M::ROW;
         float s[8][4];
         qk_tile<HD>(s, Qs, r0, Ks, g, tq);
         float mx[2] = {-INFINITY, -INFINITY};
@@ -216,6 +254,7 @@ __global__ void __launch_bounds__(128) attn_fwd_mma(const TBlk* __restrict__ blk
             o[dt][3] *= corr[1];
         }
         pv_tile<HD>(o, s, Vs, lane);
+        __syncthreads();  // buffer j & 1 is refilled by iteration j + 1's copy of block j + 2
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -240,16 +279,22 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smraw);
     __nv_bfloat16* dOs = Qs + M::ROW;
-    __nv_bfloat16* Vs = dOs + M::ROW;
-    __nv_bfloat16* Ks = Vs + M::ROW;
     const TBlk b = blks[blockIdx.x];
     const int h = blockIdx.y, kvh = h / (H / KV);
     const int nq = min(kMBlk, b.len - b.q0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;
     const float scale = rsqrtf(static_cast<float>(HD));
-    load_rows<HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
-    load_rows<HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + b.q0, nq, h * HD);
+    auto kv_issue = [&](int j) {  // key block j's K, V into buffer j & 1
+        __nv_bfloat16* kb = Qs + M::ROW * (2 + 2 * (j & 1));
+        const int kk0 = j * kMBlk;
+        load_rows_async<HD>(kb, qkv, ld, b.row0 + kk0, min(kMBlk, b.len - kk0), (H + kvh) * HD);
+        load_rows_async<HD>(kb + M::ROW, qkv, ld, b.row0 + kk0, min(kMBlk, b.len - kk0), (H + KV + kvh) * HD);
+        cp_async_commit();
+    };
+    load_rows_async<HD>(Qs, qkv, ld, b.row0 + b.q0, nq, h * HD);
+    load_rows_async<HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + b.q0, nq, h * HD);
+    kv_issue(0);
     float lr[2], dr[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -263,12 +308,19 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
     for (int dt = 0; dt < HD / 8; ++dt)
 #pragma unroll
         for (int c = 0; c < 4; ++c) dq[dt][c] = 0.f;
-    for (int k0 = 0; k0 < b.q0 + nq; k0 += kMBlk) {
+    const int nblk = (b.q0 + nq + kMBlk - 1) / kMBlk;
+    for (int j = 0; j < nblk; ++j) {
+        const int k0 = j * kMBlk;
         const int nk = min(kMBlk, b.len - k0);
+        if (j + 1 < nblk) {
+            kv_issue(j + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        load_rows<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
-        load_rows<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
-        __syncthreads();
+        const __nv_bfloat16* Ks = Qs + M::ROW * (2 + 2 * (j & 1));
+        const __nv_bfloat16* Vs = Ks + M::ROW;
         float s[8][4], dp[8][4];
         qk_tile<HD>(s, Qs, r0, Ks, g, tq);    // S = Q K^T
         qk_tile<HD>(dp, dOs, r0, Vs, g, tq);  // dP = dO V^T
@@ -283,6 +335,7 @@ __global__ void __launch_bounds__(128) attn_dq_mma(const TBlk* __restrict__ blks
                 s[nt][c] = p * (dp[nt][c] - dr[i]);  // dS
             }
         pv_tile<HD>(dq, s, Ks, lane);  // dQ += dS K
+        __syncthreads();  // buffer j & 1 is refilled by iteration j + 1's copy of block j + 2
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -313,10 +366,9 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
     extern __shared__ __align__(16) uint8_t smraw[];
     __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw);
     __nv_bfloat16* Vs = Ks + M::ROW;
-    __nv_bfloat16* Qs = Vs + M::ROW;
-    __nv_bfloat16* dOs = Qs + M::ROW;
-    float* lse_s = reinterpret_cast<float*>(dOs + M::ROW);
-    float* d_s = lse_s + kMBlk;
+    // double-buffered (Q, dO) tiles [2][2][ROW] and (lse, dvec) rows [2][2][kMBlk]
+    __nv_bfloat16* QdO = Vs + M::ROW;
+    float* ld_s = reinterpret_cast<float*>(QdO + 4 * M::ROW);
     const TBlk b = blks[blockIdx.x];  // q0 = key block start
     const int kvh = blockIdx.y / gsplit, gs = blockIdx.y % gsplit, G = H / KV;
     const int gh0 = gs * G / gsplit, gh1 = (gs + 1) * G / gsplit;
@@ -324,26 +376,45 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
     const int r0 = warp * 16;  // this warp's 16 keys
     const float scale = rsqrtf(static_cast<float>(HD));
-    load_rows<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
-    load_rows<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+    // iterations it = (head, query block) pairs; iteration it + 1's tiles are
+    // copied in (cp.async) while it computes
+    const int nqb = (b.len - k0 + kMBlk - 1) / kMBlk, n_it = (gh1 - gh0) * nqb;
+    auto qd_issue = [&](int it) {
+        const int h = kvh * G + gh0 + it / nqb, q0 = k0 + (it % nqb) * kMBlk, nq = min(kMBlk, b.len - q0);
+        __nv_bfloat16* qb = QdO + 2 * M::ROW * (it & 1);
+        load_rows_async<HD>(qb, qkv, ld, b.row0 + q0, nq, h * HD);
+        load_rows_async<HD>(qb + M::ROW, dout, static_cast<size_t>(H) * HD, b.row0 + q0, nq, h * HD);
+        cp_async_commit();
+        float* lb = ld_s + 2 * kMBlk * (it & 1);
+        for (int i = threadIdx.x; i < kMBlk; i += blockDim.x) {
+            const size_t r = static_cast<size_t>(b.row0 + q0 + min(i, nq - 1));
+            lb[i] = lse[r * H + h];
+            lb[kMBlk + i] = dvec[r * H + h];
+        }
+    };
+    load_rows_async<HD>(Ks, qkv, ld, b.row0 + k0, nk, (H + kvh) * HD);
+    load_rows_async<HD>(Vs, qkv, ld, b.row0 + k0, nk, (H + KV + kvh) * HD);
+    if (n_it > 0) qd_issue(0);
     float dk[HD / 8][4], dv[HD / 8][4];
 #pragma unroll
     for (int dt = 0; dt < HD / 8; ++dt)
 #pragma unroll
         for (int c = 0; c < 4; ++c) dk[dt][c] = dv[dt][c] = 0.f;
-    for (int gh = gh0; gh < gh1; ++gh) {
-        const int h = kvh * G + gh;
-        for (int q0 = k0; q0 < b.len; q0 += kMBlk) {
+    for (int it = 0; it < n_it; ++it) {
+        {
+            const int q0 = k0 + (it % nqb) * kMBlk;
             const int nq = min(kMBlk, b.len - q0);
-            __syncthreads();
-            load_rows<HD>(Qs, qkv, ld, b.row0 + q0, nq, h * HD);
-            load_rows<HD>(dOs, dout, static_cast<size_t>(H) * HD, b.row0 + q0, nq, h * HD);
-            for (int i = threadIdx.x; i < kMBlk; i += blockDim.x) {
-                const size_t r = static_cast<size_t>(b.row0 + q0 + min(i, nq - 1));
-                lse_s[i] = lse[r * H + h];
-                d_s[i] = dvec[r * H + h];
+            if (it + 1 < n_it) {
+                qd_issue(it + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
             }
             __syncthreads();
+            const __nv_bfloat16* Qs = QdO + 2 * M::ROW * (it & 1);
+            const __nv_bfloat16* dOs = Qs + M::ROW;
+            const float* lse_s = ld_s + 2 * kMBlk * (it & 1);
+            const float* d_s = lse_s + kMBlk;
             float st[8][4], dpt[8][4];
             qk_tile<HD>(st, Ks, r0, Qs, g, tq);   // S^T = K Q^T   (keys x queries)
             qk_tile<HD>(dpt, Vs, r0, dOs, g, tq); // dP^T = V dO^T
@@ -359,8 +430,10 @@ __global__ void __launch_bounds__(128) attn_dkv_mma(const TBlk* __restrict__ blk
                 }
             pv_tile<HD>(dv, st, dOs, lane);  // dV += P^T dO
             pv_tile<HD>(dk, dpt, Qs, lane);  // dK += dS^T Q
+            __syncthreads();  // buffer it & 1 is refilled by iteration it + 1's copy of it + 2
         }
     }
+    if (n_it == 0) cp_async_wait<0>();
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const int key = r0 + g + 8 * i;

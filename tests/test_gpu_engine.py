@@ -631,8 +631,8 @@ def test_measured_partition_utilization():
                  sample_seed=SAMPLE_SEED, train_heads=0)
     cfg = S.default_config(mode=abi.RUN_TRAIN, steps=3, batch_size=8, prompt_len=16, delta_init=2, delta_min=0,
                            delta_max=2, chunk_size=16, schedule_mode=abi.MODE_STREAMED, lengths_kind=abi.LEN_LOGNORMAL,
-                           lengths_mu_log=3.5, lengths_sigma_log=0.6, lengths_cap=96, ppo_learning_rate=0.0,
-                           ppo_value_learning_rate=0.0)
+                           lengths_mu_log=3.5, lengths_sigma_log=0.6, lengths_cap=96, ppo_learning_rate=1e-3,
+                           ppo_value_learning_rate=1e-3)
     recs, _, leds = eng.run_seed_ex(cfg, 5)
     eng.close()
     for r, led in zip(recs, leds):
