@@ -16,6 +16,13 @@ The PPO update trains every parameter of the actor and the critic
 (train_heads=2: training forward + backward through all layers, SGD on fp32
 masters), as the reference's toy_rlhf_step updates every policy parameter.
 """
+import os
+
+# K13 device-side chunk hand-off needs every kernel loaded before the step
+# (a polling scorer kernel and a lazily loaded actor kernel deadlock); set
+# before CUDA initialises in this process (DESIGN.md §4)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import argparse
 import ctypes as C
 import json

@@ -100,6 +100,41 @@ struct Arena {  // one pinned host staging buffer -> one device buffer per step
     }
 };
 
+// K13 flags.  wait_ready: the scorer wave's first kernel, one thread polling
+// its flag (ld.acquire.gpu, cyclic >=; traps after 30 s instead of hanging);
+// set_ready: a release store on the actor stream after the decode iteration
+// that completed the wave's chunks.
+__global__ void wait_ready(const uint32_t* __restrict__ flag, uint32_t want) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (static_cast<int32_t>(v - want) >= 0) break;
+        __nanosleep(256);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 30000000000ull) __trap();
+    }
+}
+__global__ void set_ready(uint32_t* __restrict__ flag, uint32_t v) {
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+bool eager_module_loading() {
+    using Fn = CUresult (*)(CUmoduleLoadingMode*);
+    static const bool eager = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        CUmoduleLoadingMode m;
+        return reinterpret_cast<Fn>(p)(&m) == CUDA_SUCCESS && m == CU_MODULE_EAGER_LOADING;
+    }();
+    return eager;
+}
+
 // Host thread that enqueues the scorer waves on the scorer stream.  A wave is
 // hundreds of launches; enqueued from the driver thread they can fill the
 // launch queue and block it, starving the actor stream of its next decode
@@ -837,6 +872,10 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         // off: with concurrent scorer passes the scorers finish within ~8 ms of
         // decode, shorter than the precompute on the actor SMs (215.4 vs 213.6)
         e->pre_lp = env_int("OPPO_PRE_LP", 0) != 0;
+        e->prompt_t0 = env_int("OPPO_PROMPT_T0", 1) != 0;
+        e->chunk_flags = env_int("OPPO_CHUNK_FLAGS", 1) != 0 && eager_module_loading();
+        e->d_ready = static_cast<uint32_t*>(dalloc(Engine::kReadyRing * sizeof(uint32_t)));
+        OPPO_CUDA_CHECK(cudaMemsetAsync(e->d_ready, 0, Engine::kReadyRing * sizeof(uint32_t), st));
         e->g_chunk = std::max(64, env_int("OPPO_G_CHUNK", e->g_chunk)) / 8 * 8;  // update token chunk
         // 16-position tiles (5 CTAs/SM instead of 3) once the 32-position grid
         // needs 2+ waves: measured -190 us per iteration at 256 rows on 84 SMs
@@ -890,7 +929,8 @@ void engine_free(Engine* e) {
                     static_cast<void*>(e->d_ref_pending), e->g_buf, e->ht_buf, e->ppo_buf,
                     static_cast<void*>(e->g_lm), e->pre_hf, static_cast<void*>(e->pre_tok),
                     static_cast<void*>(e->pre_new), static_cast<void*>(e->pre_lse), static_cast<void*>(e->pre_meta),
-                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt)})
+                    static_cast<void*>(e->pre_partials), static_cast<void*>(e->pre_tgt),
+                    static_cast<void*>(e->d_ready)})
         if (p) cudaFree(p);
     for (auto& kv : e->decode_graphs) cudaGraphExecDestroy(kv.second);
     for (Work* w : {&e->wa, &e->wa2, &e->ws, &e->ws_m[0], &e->ws_m[1]}) free_work(*w);
@@ -1308,11 +1348,7 @@ void decode_iteration(Engine& e, int M, cudaStream_t st) {
 // One decode iteration for batch size M: replay the captured graph (capture on
 // first use).  Host cost per iteration is one cudaGraphLaunch.
 template <class T>
-void decode_iteration_graph(Engine& e, int M, cudaStream_t st) {
-    if (!e.cfg.use_graphs) {
-        decode_iteration<T>(e, M, st);
-        return;
-    }
+cudaGraphExec_t ensure_decode_graph(Engine& e, int M, cudaStream_t st) {
     auto it = e.decode_graphs.find(M);
     if (it == e.decode_graphs.end()) {
         const int64_t before = e.launches;
@@ -1328,11 +1364,21 @@ void decode_iteration_graph(Engine& e, int M, cudaStream_t st) {
         cudaGraphExec_t ge;
         OPPO_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
         OPPO_CUDA_CHECK(cudaGraphDestroy(g));
+        OPPO_CUDA_CHECK(cudaGraphUpload(ge, st));  // device-side setup now, not at the first launch
         it = e.decode_graphs.emplace(M, ge).first;
         e.decode_graph_launches[M] = e.launches - before;
         e.launches = before;
     }
-    OPPO_CUDA_CHECK(cudaGraphLaunch(it->second, st));
+    return it->second;
+}
+
+template <class T>
+void decode_iteration_graph(Engine& e, int M, cudaStream_t st) {
+    if (!e.cfg.use_graphs) {
+        decode_iteration<T>(e, M, st);
+        return;
+    }
+    OPPO_CUDA_CHECK(cudaGraphLaunch(ensure_decode_graph<T>(e, M, st), st));
     e.launches += e.decode_graph_launches[M];
 }
 
@@ -1472,11 +1518,24 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
              3.0 * d.d_model * d.d_ff);
         kv_bytes_tok[mi] = 2.0 * d.n_layers * d.n_kv_heads * d.head_dim * e.esz;
     }
+    // Streamed mode scores the prompts of fresh sequences in the wave at tick 0
+    // (the scorer partition is otherwise idle until the first chunk is decoded);
+    // their first response chunk then starts at position P.  Decisions do not
+    // change (prefill time is 0 on the logical clock); numerics are per row.
+    const bool prompts_at_0 = streamed && e.prompt_t0;
     auto make_wave = [&](int at_iter, auto&& target_p) {
         std::vector<SegReq> reqs;
         for (int i : order) {  // deterministic order
             const int want = target_p(i);
-            if (want <= p_cur[i]) continue;
+            if (want <= p_cur[i]) {
+                auto& inf = e.slots[slot[i]];
+                if (at_iter == 0 && prompts_at_0 && p_cur[i] == 0 && !inf.scored_prompt) {
+                    const int P = active[i].prompt_len;
+                    reqs.push_back({slot[i], 0, P, P});  // prompt only: positions 0 .. P-1
+                    inf.scored_prompt = true;
+                }
+                continue;
+            }
             auto& info = e.slots[slot[i]];
             const int P = active[i].prompt_len;
             const bool first = p_cur[i] == 0 && !info.scored_prompt;
@@ -1567,8 +1626,45 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
             }
         }
     } drain_guard{worker};
+    const bool flags = e.chunk_flags;
+    if (flags && e.cfg.use_graphs) {
+        // every decode graph this step can launch exists (captured, instantiated,
+        // uploaded) before a scorer kernel starts polling: first-time setup of a
+        // graph or kernel must not wait behind a spinning poller
+        const int top = std::min(cdiv(static_cast<int64_t>(n_dec), 16) * 16, e.S + 16);
+        for (int bkt = 16; bkt <= top; bkt += 16) ensure_decode_graph<T>(e, bkt, e.sa);
+    }
+    std::vector<uint32_t> wave_seq(waves.size());
+    for (size_t k = 0; flags && k < waves.size(); ++k) wave_seq[k] = ++e.ready_seq;
+    // With flags the scorer stream's copy of wave k is enqueued one wave ahead
+    // (when wave k-1's flag is written), gated on the device by wave k's flag.
+    auto post_wave = [&](size_t k) {
+        const uint32_t* flag = e.d_ready + (wave_seq[k] % Engine::kReadyRing);
+        const uint32_t want = wave_seq[k];
+        const WavePlan* wave = &waves[k];
+        cudaEvent_t t0 = e.ev_wave[2 * k], t1 = e.ev_wave[2 * k + 1];
+        worker.post([&e, &A, &prefill_tokens, flag, want, wave, t0, t1] {
+            wait_ready<<<1, 32, 0, e.ss>>>(flag, want);
+            OPPO_CUDA_CHECK(cudaGetLastError());
+            e.launches += 1;
+            OPPO_CUDA_CHECK(cudaEventRecord(t0, e.ss));  // the wave's chunks are ready
+            int64_t tok = 0;
+            for (const auto& p : wave->passes) run_scorer_pass<T>(e, p, A, e.ss, tok);
+            OPPO_CUDA_CHECK(cudaEventRecord(t1, e.ss));
+            prefill_tokens += tok;
+        });
+    };
+    if (flags && !waves.empty()) post_wave(0);
     auto fire_waves_at = [&](int64_t it) {
         while (wi < waves.size() && waves[wi].at_iter == it) {
+            if (flags) {  // actor-stream order: after iteration `it`, the wave's chunks are complete
+                set_ready<<<1, 32, 0, e.sa>>>(e.d_ready + (wave_seq[wi] % Engine::kReadyRing), wave_seq[wi]);
+                OPPO_CUDA_CHECK(cudaGetLastError());
+                e.launches += 1;
+                if (wi + 1 < waves.size()) post_wave(wi + 1);
+                ++wi;
+                continue;
+            }
             cudaEvent_t ev = e.ev_pool[wi + 1];
             OPPO_CUDA_CHECK(cudaEventRecord(ev, e.sa));  // actor-stream order: after iteration `it`
             const WavePlan* wave = &waves[wi];

@@ -151,6 +151,7 @@ struct Engine {
     // scorers finish their last wave; oppo_ppo_update reuses them when the
     // lm_head has not changed since (pre_version == lm_version).
     bool pre_lp = false;
+    bool prompt_t0 = true;  // streamed: fresh prompts scored in the tick-0 wave (OPPO_PROMPT_T0)
     int64_t lm_version = 0, pre_version = -1;
     std::unordered_map<int64_t, std::pair<int, int>> pre_index;  // seq id -> (token offset, tokens)
     size_t pre_cap = 0;                 // tokens
@@ -173,6 +174,18 @@ struct Engine {
     cudaStream_t su = nullptr;  // admission prefill + PPO update: whole GPU (== sa without a partition)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<cudaEvent_t> ev_wave;  // timing events around each scorer wave (start, end): partition busy time
+    // K13 chunk hand-off on the device: after the decode iteration that
+    // completes a wave's chunks the actor stream publishes the wave's sequence
+    // number into a ring of per-chunk ready flags (release store); the scorer
+    // stream's first kernel of the wave polls its flag (acquire loads).  Only
+    // with eager module loading: under lazy loading the first launch of a
+    // kernel waits for the device, so a scorer kernel polling for a flag whose
+    // writer (or any kernel ahead of it) is not loaded yet deadlocks -- measured
+    // on B200 (tools/probe/flag_probe.cu); per-wave events otherwise.
+    static constexpr int kReadyRing = 256;
+    uint32_t* d_ready = nullptr;  // [kReadyRing] flags (monotone sequence numbers)
+    uint32_t ready_seq = 0;       // last sequence number issued
+    bool chunk_flags = false;
     cudaEvent_t ev_begin = nullptr, ev_dec_end = nullptr, ev_sc_end = nullptr, ev_done = nullptr,
                 ev_loop0 = nullptr;
     bool step_open = false;

@@ -2,6 +2,9 @@ import json
 import os
 import sys
 
+# as bench.py: the engine's device-side chunk hand-off requires eager kernel loading
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import pytest
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))

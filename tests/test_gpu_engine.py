@@ -639,3 +639,63 @@ def test_measured_partition_utilization():
         assert led.step_us > 0 and led.score_busy_us > 0
         assert 0.0 < r.util_generation <= 1.01 and 0.0 < r.util_scoring <= 1.01, (r.util_generation, r.util_scoring)
         assert abs(r.util_generation - led.decode_loop_us / led.step_us) < 1e-9
+
+
+def _run_flags(flags, scorer_sms):
+    """Two overcommitted streamed steps (0.5B width, 2 layers) with the K13
+    chunk hand-off on device flags (1) or per-wave events (0)."""
+    import os
+    shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                 vocab=1024, tied=1)
+    P, C, B = 16, 16, 6
+    lens = [40, 70, 23, 64, 90, 12, 55, 31, 77, 18, 44, 26, 61, 15]
+    old = os.environ.get("OPPO_CHUNK_FLAGS")
+    os.environ["OPPO_CHUNK_FLAGS"] = str(flags)
+    try:
+        eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=16, max_prompt_len=P, max_response_len=96,
+                     sample_seed=SAMPLE_SEED, carry=abi.CARRY_TOKEN, scorer_sms=scorer_sms)
+    finally:
+        if old is None:
+            os.environ.pop("OPPO_CHUNK_FLAGS", None)
+        else:
+            os.environ["OPPO_CHUNK_FLAGS"] = old
+    entries = list(S.seq_array(fresh_states(8, P, lens[:8])))
+    eng.admit(entries)
+    log, ro, nid = [], {}, 8
+    for step in range(2):
+        active = [e for e in entries if not e.scored]
+        need = B - (len(entries) - len(active))
+        outs, led = eng.run_step(active, C, abi.MODE_STREAMED, need)
+        batch, entries, _ = S.select_finished(entries, outs, B)
+        log.append(([o.as_tuple() for o in outs], led.score_us - led.decode_us))
+        for b in batch:
+            ro[b.id] = eng.read_rollout(b.id)
+        eng.release([b.id for b in batch])
+        fresh = list(S.seq_array(fresh_states(2, P, lens[nid:nid + 2], start_id=nid)))
+        nid += 2
+        eng.admit(fresh)
+        entries = list(entries) + fresh
+    eng.close()
+    return log, ro
+
+
+@pytest.mark.timeout(240, method="thread")
+@pytest.mark.parametrize("scorer_sms", [0, 64])
+def test_chunk_ready_flags_match_event_handoff(scorer_sms):
+    """K13 on the device (north_star (2), engine.cpp:77-82): the actor stream
+    publishes each wave's ready flag after the decode iteration that
+    completes its chunks and the scorer stream's first kernel of the wave
+    polls it -- every token, log-prob, value and reward is bit-identical to
+    the per-wave event hand-off, with and without the SM partition (eager
+    kernel loading, as conftest.py / bench.py set it)."""
+    import os
+    assert os.environ.get("CUDA_MODULE_LOADING") == "EAGER"
+    la, ra = _run_flags(1, scorer_sms)
+    lb, rb = _run_flags(0, scorer_sms)
+    assert [x[0] for x in la] == [x[0] for x in lb]
+    assert ra.keys() == rb.keys() and len(ra) >= 6
+    for k in ra:
+        for f in ("tokens", "old_lp", "ref_lp", "values"):
+            assert np.array_equal(ra[k][f], rb[k][f]), (k, f)
+        assert ra[k]["reward"] == rb[k]["reward"], k
+    print("score tail after decode (us): flags", [x[1] for x in la], "events", [x[1] for x in lb])

@@ -1,5 +1,9 @@
 // Device-flag hand-off probe: stream B polls a flag that stream A sets after a
-// delay kernel.  Prints whether B observed it (and how long it took).
+// delay kernel.  Prints whether B observed it (and how long it took).  Under
+// lazy module loading (the CUDA 12 default) round 1 times out: A's kernels are
+// loaded on first launch, which waits for the device while B's poller spins;
+// with CUDA_MODULE_LOADING=EAGER every round sees the flag after the delay.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o flag_probe flag_probe.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -37,6 +41,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (uint32_t k = 1; k <= 5; ++k) {
+        cudaMemset(to, 0, 4);
         cudaEventRecord(e0, b);
         wait_ready<<<1, 32, 0, b>>>(f, k, to);
         cudaEventRecord(e1, b);
