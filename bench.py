@@ -667,7 +667,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--scorer-sms", type=int, default=64,
+    ap.add_argument("--scorer-sms", type=int, default=56,
                     help="fixed SM partition for the scorer stream in the overlapped arm (0: shared)")
     ap.add_argument("--config", default=None,
                     help="reference-schema JSON run config (+ model/gpu blocks) instead of --workload")

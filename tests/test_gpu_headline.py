@@ -1,7 +1,7 @@
 """Parity at the benchmarked configuration (BASELINE.json configs[1], the line
 bench.py reports): 0.5B actor + 0.5B reward / critic / reference, bf16,
 V = 151,936, B = 256 + 26 overcommit, prompt 128, LN(5, 1) cap 1024, chunk 64,
-token-granular carry, the scorer SM partition (64 SMs, green contexts), three
+token-granular carry, the scorer SM partition (56 SMs, green contexts), three
 concurrent scorer streams and two-branch decode iterations — built exactly as
 bench.py builds the engine (bench.make_cfg / bench.CFG2 / bench.host_prompts).
 
@@ -61,7 +61,7 @@ def _cuda():
         pytest.skip("no GPU")
 
 
-def run_cfg2(steps=STEPS, scorer_sms=64, env=None, keep=None, weights=False, wl=None):
+def run_cfg2(steps=STEPS, scorer_sms=56, env=None, keep=None, weights=False, wl=None):
     """Two cfg2 steps through the engine exactly as bench.py drives it.  Returns
     per-step decisions + outcomes, and rollouts of the sequences in `keep`
     (all selected sequences when keep == 'all')."""
@@ -248,8 +248,8 @@ def test_headline_partition_and_streams_do_not_change_results():
     the three concurrent scorer streams leave every token, log-prob, value and
     reward of two cfg2 steps bit-identical."""
     _cuda()
-    env = {"OPPO_NUMERICS_SMS": "84"}
-    a = run_cfg2(steps=2, scorer_sms=64, env={**env, "OPPO_SCORER_STREAMS": "3"}, keep="all")
+    env = {"OPPO_NUMERICS_SMS": "92"}
+    a = run_cfg2(steps=2, scorer_sms=56, env={**env, "OPPO_SCORER_STREAMS": "3"}, keep="all")
     b = run_cfg2(steps=2, scorer_sms=0, env={**env, "OPPO_SCORER_STREAMS": "1"}, keep="all")
     assert [s["selected"] for s in a["log"]] == [s["selected"] for s in b["log"]]
     assert a["rollouts"].keys() == b["rollouts"].keys()
@@ -262,7 +262,7 @@ def test_headline_partition_and_streams_do_not_change_results():
 
 def test_cfg3_decisions_and_content_vs_reference():
     """BASELINE configs[2] on one GPU as bench.py runs it (1.5B actor + 0.5B
-    scorers, B = 256 + 26, 64-SM scorer partition): two steps of cut / chunk
+    scorers, B = 256 + 26, 56-SM scorer partition): two steps of cut / chunk
     progress / selection against the compiled reference's run_step, and the
     shortest selected sequence's tokens and old log-probs at full depth (28
     layers) against the bf16-rounding fp64 oracle."""

@@ -21,7 +21,7 @@ def main():
     eng = Engine(wl["actor"], wl["scorer"], wl["scorer"], wl["scorer"], dtype=abi.DTYPE_BF16,
                  max_slots=wl["batch"] + wl["delta"] + 8, max_prompt_len=wl["prompt_len"],
                  max_response_len=wl["cap"], page_size=64, carry=cfg.carry_granularity,
-                 train_heads=2, sample_seed=2, weight_seed=1, scorer_sms=64)
+                 train_heads=2, sample_seed=2, weight_seed=1, scorer_sms=56)
     V = eng.cfg.actor.vocab
     B, P = cfg.batch_size, cfg.prompt_len
     lengths = S.sample_lengths(cfg.lengths, 7, 4 * (B + cfg.delta_max))
