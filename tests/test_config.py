@@ -140,4 +140,4 @@ def test_bench_workload_from_config_matches_cfg2():
     a, b = bench.make_cfg(wl), bench.make_cfg(bench.WORKLOADS["cfg2"])
     assert bytes(a) == bytes(b)
     assert bytes(bench.make_cfg(wl, True)) == bytes(bench.make_cfg(bench.WORKLOADS["cfg2"], True))
-    assert (wl["batch"], wl["chunk"], wl["delta"], wl["scorer_sms"]) == (256, 64, 26, 64)
+    assert (wl["batch"], wl["chunk"], wl["delta"], wl["scorer_sms"]) == (256, 64, 26, 56)
