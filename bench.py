@@ -39,15 +39,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PPO samples/sec per step (overlap vs sequential) at 1/2/4/8 B200; roofline %"
+CFG3_SMS, CFG4_SMS = 40, 32  # measured: cfg3 24/32/40/56 -> 62.5/66.4/67.1/65.3, cfg4 16/24/32/64 -> 8.3/8.4/8.3/7.1 samples/s
+# scorer_sms: the fixed SM partition of the overlapped arm, measured per workload
 CFG2 = dict(name="cfg2", actor="0.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
-            sigma=1.0, cap=1024, chunk=64, delta=26)
+            sigma=1.0, cap=1024, chunk=64, delta=26, scorer_sms=56)
 # BASELINE configs[2] shape on one GPU: 1.5B actor + 0.5B scorers (chunk 64, 10% overcommit)
 CFG3 = dict(name="cfg3", actor="1.5b", scorer="0.5b", batch=256, prompt_len=128, mu=5.0,
-            sigma=1.0, cap=1024, chunk=64, delta=26)
+            sigma=1.0, cap=1024, chunk=64, delta=26, scorer_sms=CFG3_SMS)
 # BASELINE configs[3] per GPU: 7B actor + 1.5B scorers, 512 prompts over 8 GPUs = 64 per GPU,
 # LN(5.5, 1.0) cap 2048, 10% overcommit (6 per GPU)
 CFG4 = dict(name="cfg4", actor="7b", scorer="1.5b", batch=64, prompt_len=128, mu=5.5,
-            sigma=1.0, cap=2048, chunk=64, delta=6)
+            sigma=1.0, cap=2048, chunk=64, delta=6, scorer_sms=CFG4_SMS)
 WORKLOADS = {}
 TINY = dict(name="cfg1", actor="tiny", scorer="tiny", batch=8, prompt_len=8, mu=3.5, sigma=0.6,
             cap=64, chunk=16, delta=2)
@@ -667,8 +669,9 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-sequential", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--scorer-sms", type=int, default=56,
-                    help="fixed SM partition for the scorer stream in the overlapped arm (0: shared)")
+    ap.add_argument("--scorer-sms", type=int, default=None,
+                    help="fixed SM partition for the scorer stream in the overlapped arm (0: shared; "
+                         "default: the workload's measured best)")
     ap.add_argument("--config", default=None,
                     help="reference-schema JSON run config (+ model/gpu blocks) instead of --workload")
     ap.add_argument("--dry-run-ranks", action="store_true", help=argparse.SUPPRESS)
@@ -688,8 +691,10 @@ def main():
         wl = workload_from_config(args.config)
         WORKLOADS["config"] = wl
         args.workload = "config"
-        if wl.get("scorer_sms") is not None:
+        if wl.get("scorer_sms") is not None and args.scorer_sms is None:
             args.scorer_sms = wl["scorer_sms"]
+    if args.scorer_sms is None:
+        args.scorer_sms = WORKLOADS[args.workload].get("scorer_sms", 56)
     if args.impl == "reference":
         reference(args)
     else:
