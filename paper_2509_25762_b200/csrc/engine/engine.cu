@@ -2178,6 +2178,21 @@ void dp_allreduce_pub(Engine& e, void* buf, int64_t count, bool f64, cudaStream_
     dp_allreduce(e, buf, count, f64, st);
 }
 
+// One gradient bucket (fp32 tensors): a single NCCL group launch when the
+// engine has a communicator (the tensors of a layer travel as one fused
+// collective), else one host-callback allreduce per tensor.
+void dp_allreduce_bucket(Engine& e, const std::vector<std::pair<float*, int64_t>>& bufs, cudaStream_t st) {
+    if (e.nccl) {
+        OPPO_NCCL_CHECK(ncclGroupStart());
+        for (const auto& b : bufs)
+            OPPO_NCCL_CHECK(ncclAllReduce(b.first, b.first, static_cast<size_t>(b.second), ncclFloat, ncclSum,
+                                          static_cast<ncclComm_t>(e.nccl), st));
+        OPPO_NCCL_CHECK(ncclGroupEnd());
+        return;
+    }
+    for (const auto& b : bufs) dp_allreduce(e, b.first, b.second, false, st);
+}
+
 }  // namespace oppo
 
 // ==================================================================== C ABI

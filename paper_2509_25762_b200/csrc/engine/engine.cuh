@@ -263,6 +263,7 @@ std::vector<std::pair<void*, size_t>> train_tensors(Engine& e, cudaStream_t st);
 const float* train_master(Engine& e, int model, const std::string& name, int layer);
 // engine.cu
 void dp_allreduce_pub(Engine& e, void* buf, int64_t count, bool f64, cudaStream_t st);
+void dp_allreduce_bucket(Engine& e, const std::vector<std::pair<float*, int64_t>>& bufs, cudaStream_t st);
 
 // gemm_host.cu
 void gemm_run(Engine& e, Work& w, cudaStream_t st, const void* x, int M, int K, int ldx,

@@ -19,12 +19,18 @@
 // dgrad GEMM of the down projection writes d(gate, up) directly), and the
 // RMSNorm backward emits the bf16 copy of the residual gradient the next
 // GEMMs read.
-// After the last micro-batch the gradients are allreduced across the
-// data-parallel ranks (one NCCL call per tensor) and applied by SGD to the
-// fp32 masters, from which the bf16 compute weights are re-rounded.
+// Data-parallel runs allreduce the gradients in per-layer buckets overlapped
+// with the backward: in the last micro-batch, as soon as layer
+// l's gradients are final, a comm stream waits for them, runs one grouped NCCL
+// allreduce of the layer's tensors and applies their SGD step to the fp32
+// masters (re-rounding the bf16 compute weights) while the compute stream
+// goes on with layers l-1 .. 0; the embedding / lm_head / final norm / head
+// form the last bucket.  Without a communicator (or with the host allreduce
+// hook) the tensors are reduced and applied after the last micro-batch.
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -114,12 +120,18 @@ struct TrainState {
          *Gt = nullptr;
     int32_t *tok = nullptr, *pos = nullptr;
     int g_rows = 0;  // lm_head gradient chunk (rows)
+    // gradient buckets of data-parallel updates: comm stream + hand-off events
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
 };
 
 void train_free(Engine& e) {
     auto* ts = static_cast<TrainState*>(e.train_state);
     if (!ts) return;
     ts->scr.release();
+    if (ts->comm) cudaStreamDestroy(ts->comm);
+    if (ts->ev_ready) cudaEventDestroy(ts->ev_ready);
+    if (ts->ev_comm) cudaEventDestroy(ts->ev_comm);
     for (auto& m : ts->m)
         for (PT* p : m.all()) {
             if (p->grad) cudaFree(p->grad);
@@ -399,7 +411,8 @@ void ensure_scratch(Engine& e, TrainState& ts, int rows) {
 // lm_head; critic: squared error of the value head).  Gradients accumulate
 // into the tensors' fp32 grad buffers; the caller applies them.
 template <class T>
-void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
+void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st,
+                 const std::function<void(int)>& layer_final = {}) {
     auto& ts = *static_cast<TrainState*>(e.train_state);
     Model& m = e.models[mid];
     ModelT& mt = ts.m[mid];
@@ -610,6 +623,7 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
             mmt(e, st, dqc, kK, qkvw, Lw.wqkv, kMN, D, Tr, D, qkvw, epi(EPI_STORE_F32, ts.dh, D));
             rms_bwd_into<T>(ts, ts.x_in[l], Lw.ln1, ts.dh, Tr, D, dx, l > 0 ? dxc : static_cast<T*>(nullptr),
                             Lt.ln1.grad, st);
+            if (layer_final && s1 == n) layer_final(l);  // layer l's gradients are final
         }
         train::embed_grad_csr<<<static_cast<int>(uniq.size()), 128, 0, st>>>(dx, d_uniq, d_start, d_order, D,
                                                                               mt.embed.grad);
@@ -621,17 +635,64 @@ void train_model(Engine& e, const TrainBatch& b, int mid, cudaStream_t st) {
 }
 
 template <class T>
-void train_apply(Engine& e, int mid, float scale, bool dp, cudaStream_t st) {
-    auto& ts = *static_cast<TrainState*>(e.train_state);
-    for (PT* p : ts.m[mid].all()) {
-        if (dp) dp_allreduce_pub(e, p->grad, p->n(), false, st);
-        if (p->master)
+void sgd_into(PT* p, float scale, cudaStream_t st) {
+    if (p->master)
             train::sgd_apply<T><<<cdiv(p->n(), 256), 256, 0, st>>>(p->master, p->grad, p->n(), scale, static_cast<T*>(p->w));
         else
             train::sgd_apply<T><<<cdiv(p->n(), 256), 256, 0, st>>>(static_cast<float*>(p->w), p->grad, p->n(), scale,
                                                                     static_cast<T*>(nullptr));
+}
+
+template <class T>
+void train_apply(Engine& e, int mid, float scale, bool dp, cudaStream_t st) {
+    auto& ts = *static_cast<TrainState*>(e.train_state);
+    for (PT* p : ts.m[mid].all()) {
+        if (dp) dp_allreduce_pub(e, p->grad, p->n(), false, st);
+        sgd_into<T>(p, scale, st);
     }
     OPPO_CUDA_CHECK(cudaGetLastError());
+}
+
+// One bucket on the comm stream once the compute stream has produced it:
+// grouped allreduce, then the SGD step of each tensor.
+template <class T>
+void bucket_apply(Engine& e, TrainState& ts, const std::vector<PT*>& ps, float scale, cudaStream_t st) {
+    OPPO_CUDA_CHECK(cudaEventRecord(ts.ev_ready, st));
+    OPPO_CUDA_CHECK(cudaStreamWaitEvent(ts.comm, ts.ev_ready, 0));
+    std::vector<std::pair<float*, int64_t>> bufs;
+    for (PT* p : ps) bufs.emplace_back(p->grad, p->n());
+    dp_allreduce_bucket(e, bufs, ts.comm);
+    for (PT* p : ps) sgd_into<T>(p, scale, ts.comm);
+    OPPO_CUDA_CHECK(cudaGetLastError());
+}
+
+// train_model + train_apply with the data-parallel gradient buckets
+// overlapped with the backward (NCCL communicator only).
+template <class T>
+void train_and_apply(Engine& e, TrainBatch& b, int mid, float scale, bool dp, cudaStream_t st) {
+    auto& ts = *static_cast<TrainState*>(e.train_state);
+    if (!dp || !e.nccl || std::getenv("OPPO_GRAD_BUCKETS_OFF")) {
+        train_model<T>(e, b, mid, st);
+        train_apply<T>(e, mid, scale, dp, st);
+        return;
+    }
+    if (!ts.comm) {
+        OPPO_CUDA_CHECK(cudaStreamCreateWithFlags(&ts.comm, cudaStreamNonBlocking));
+        OPPO_CUDA_CHECK(cudaEventCreateWithFlags(&ts.ev_ready, cudaEventDisableTiming));
+        OPPO_CUDA_CHECK(cudaEventCreateWithFlags(&ts.ev_comm, cudaEventDisableTiming));
+    }
+    ModelT& mt = ts.m[mid];
+    train_model<T>(e, b, mid, st, [&](int l) {
+        auto& L = mt.layers[l];
+        bucket_apply<T>(e, ts, {&L.wqkv, &L.bqkv, &L.wo, &L.wgu, &L.wdown, &L.ln1, &L.ln2}, scale, st);
+    });
+    std::vector<PT*> rest{&mt.embed};
+    if (mt.lm_head.w && mt.lm_head.w != mt.embed.w) rest.push_back(&mt.lm_head);
+    rest.push_back(&mt.final_norm);
+    if (mt.head.w) rest.push_back(&mt.head);
+    bucket_apply<T>(e, ts, rest, scale, st);
+    OPPO_CUDA_CHECK(cudaEventRecord(ts.ev_comm, ts.comm));
+    OPPO_CUDA_CHECK(cudaStreamWaitEvent(st, ts.ev_comm, 0));  // updated weights before anything else
 }
 
 template <class T>
@@ -644,14 +705,10 @@ void train_full(Engine& e, TrainBatch& b, const oppo_ppo_hparams& hp, bool dp, c
     for (size_t i = 0; i < b.slot.size(); ++i) max_seq = std::max(max_seq, b.P[i] + b.L[i] - 1);
     b.rows_max = std::max(b.rows_max, max_seq);
     ensure_scratch<T>(e, ts, b.rows_max);
-    if (hp.learning_rate != 0) {
-        train_model<T>(e, b, ACTOR, st);
-        train_apply<T>(e, ACTOR, static_cast<float>(hp.learning_rate), dp, st);  // ascent (ppo.cpp:288-290)
-    }
-    if (hp.value_learning_rate != 0) {
-        train_model<T>(e, b, CRITIC, st);
-        train_apply<T>(e, CRITIC, -static_cast<float>(hp.value_learning_rate), dp, st);  // descent on (V-R)^2/2
-    }
+    if (hp.learning_rate != 0)  // ascent (ppo.cpp:288-290)
+        train_and_apply<T>(e, b, ACTOR, static_cast<float>(hp.learning_rate), dp, st);
+    if (hp.value_learning_rate != 0)  // descent on (V-R)^2/2
+        train_and_apply<T>(e, b, CRITIC, -static_cast<float>(hp.value_learning_rate), dp, st);
 }
 
 // Every tensor the full update changes, for checkpoints: (device pointer,

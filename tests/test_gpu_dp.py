@@ -128,10 +128,12 @@ def _nccl_world1(q):
 
 
 def test_nccl_call_sites_on_hardware_world1():
-    """The engine's NCCL call sites (whitening / reward statistics, per-tensor
-    gradient allreduce of the full-parameter update) executed on the GPU with
-    a world-1 communicator: the update is bit-identical to the engine without
-    one (the sum over one rank is the identity)."""
+    """The engine's NCCL call sites (whitening / reward statistics, and the
+    full-parameter update's per-layer gradient buckets: grouped allreduce +
+    SGD on a comm stream overlapped with the rest of the backward) executed
+    on the GPU with a world-1 communicator: the update is bit-identical to
+    the engine without one, whose SGD runs after the backward on the compute
+    stream (the sum over one rank is the identity)."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     ctx = mp.get_context("spawn")
