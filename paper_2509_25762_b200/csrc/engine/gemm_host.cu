@@ -106,15 +106,6 @@ static const double g_fold_ns = [] {
     return v ? std::atof(v) : 400.0;  // measured: -8% decode iteration at 16 rows, neutral above
 }();
 
-// CTA-pair 256x256 prefill tiles: correct in isolation (tests) and measured
-// down 91 -> 83 us, gate|up 182 -> 180 us at 8192 rows (the operand stream is
-// the limit, ~6 TB/s L2 -> SM).  Launched on the whole-GPU update/admission
-// stream it runs fine (OPPO_TC2SM=3); inside the scorer's green-context
-// partition it hangs (OPPO_TC2SM=2, either SM-split layout).  Off by default.
-static const int g_tc2sm = [] {  // 0 off, 1 everywhere, 2 scorer stream only, 3 other streams only
-    const char* v = std::getenv("OPPO_TC2SM");
-    return v ? std::atoi(v) : 0;
-}();
 
 static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M, int K, int ldx,
                       const void* wt, int N, int ldw, const EpiParams& ep_in, int dtype,
@@ -190,8 +181,9 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
         return;
     }
     // Token-rich prefill GEMMs: CTA-pair 256x256 tiles (cta_group::2)
+    // (not on the scorer streams: cluster launches inside the scorer's green
+    // context hung in round-1 measurements, so prefill keeps single-CTA tiles)
     const bool scorer_stream = e && (st == e->ss || st == e->ss_m[0] || st == e->ss_m[1]);
-    const bool use2 = g_tc2sm == 1 || (g_tc2sm == 2 && scorer_stream) || (g_tc2sm == 3 && !scorer_stream);
     // Long-K GEMMs that fill the GPU with CTA pairs (the update's weight
     // gradients, K = tokens): the pair tile halves each SM's operand stream
     // per flop, and the 6-stage ring covers the L2 latency (OPPO_TC2SM_LONGK)
@@ -203,7 +195,7 @@ static void gemm_impl(Engine* e, Work* wk, cudaStream_t st, const void* x, int M
     // weights) on CTA pairs, two pairs per SM pair (OPPO_TC2SM_SHORT)
     const bool short2 = ep.update_gemm && tc2sm_short_enabled() && !long2 && m_tiles >= 8 && N >= 512 &&
                         pairs * 2 >= num_sms && ep.mode != EPI_LOGITS && !rope;
-    if ((m_tiles >= 8 && ep.mode != EPI_LOGITS && !rope && !mn && use2) || long2 || short2) {
+    if (long2 || short2) {
         static std::once_flag attr2;
         std::call_once(attr2, [] {
             OPPO_CUDA_CHECK(cudaFuncSetAttribute(tc::gemm_bf16_tc2sm<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -12,7 +12,7 @@ from paper_2509_25762_b200 import abi, scheduler as S
 from paper_2509_25762_b200.engine import Engine, SHAPES
 
 Ms = [int(x) for x in os.environ.get("MS", "16,64,128,256").split(",")]
-L, P = int(os.environ.get("L", "48")), 128
+L, P = int(os.environ.get("L", "48")), int(os.environ.get("P", "128"))  # P: context before the first decode
 SHAPE = os.environ.get("SHAPE", "0.5b")
 shape = dict(SHAPES[SHAPE])
 eng = Engine(shape, shape, shape, shape, dtype=abi.DTYPE_BF16, max_slots=max(Ms) + 8, max_prompt_len=P,
