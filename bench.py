@@ -50,10 +50,15 @@ CFG3 = dict(name="cfg3", actor="1.5b", scorer="0.5b", batch=256, prompt_len=128,
 # LN(5.5, 1.0) cap 2048, 10% overcommit (6 per GPU)
 CFG4 = dict(name="cfg4", actor="7b", scorer="1.5b", batch=64, prompt_len=128, mu=5.5,
             sigma=1.0, cap=2048, chunk=64, delta=6, scorer_sms=CFG4_SMS)
+# BASELINE configs[4] per GPU: 7B actor, 4K max response, heavy long tail LN(6.0, 1.2) cap 4096,
+# 256 prompts over 8 GPUs = 32 per GPU (KV + the 7B update's fp32 masters / gradients fit 180 GB),
+# 10% overcommit (3 per GPU), chunk 128
+CFG5 = dict(name="cfg5", actor="7b", scorer="1.5b", batch=32, prompt_len=128, mu=6.0,
+            sigma=1.2, cap=4096, chunk=128, delta=3, scorer_sms=CFG4_SMS)
 WORKLOADS = {}
 TINY = dict(name="cfg1", actor="tiny", scorer="tiny", batch=8, prompt_len=8, mu=3.5, sigma=0.6,
             cap=64, chunk=16, delta=2)
-WORKLOADS.update(cfg1=TINY, cfg2=CFG2, cfg3=CFG3, cfg4=CFG4)
+WORKLOADS.update(cfg1=TINY, cfg2=CFG2, cfg3=CFG3, cfg4=CFG4, cfg5=CFG5)
 
 
 def workload(args):

@@ -431,8 +431,10 @@ oppo_status oppo_run_seed_ex(oppo_engine* e, const oppo_run_config* cfg, uint64_
 
 /* Data-parallel plumbing: one NCCL communicator over the GPUs of
  * the box; pass it as oppo_engine_cfg.nccl_comm with rank/world.  The engine
- * then allreduces the whitening / reward statistics and the trained heads'
- * gradients inside oppo_ppo_update.  Rank 0 creates the id and ships it to
+ * then allreduces the whitening / reward statistics and the gradients of the
+ * trained tensors inside oppo_ppo_update (full-parameter update: one grouped
+ * allreduce per layer on a comm stream, overlapped with the rest of the
+ * backward).  Rank 0 creates the id and ships it to
  * the other ranks (e.g. torch.distributed broadcast). */
 #define OPPO_NCCL_ID_BYTES 128
 oppo_status oppo_nccl_unique_id(uint8_t* out /* OPPO_NCCL_ID_BYTES */);
