@@ -486,11 +486,17 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     const auto& d = m.dims;
     const KvView kv = m.kv(e.d_page_table, e.max_pages, e.page_size);
     const int base = R * d.n_kv_heads;
-    // split-KV clusters measured slower than one CTA per (row, KV head) with
-    // 4 warps over the context (cluster co-scheduling); OPPO_ATTN_MAX_SPLIT > 1
-    // re-enables them for very long contexts at tiny batches
-    int nsp = std::max(1, std::min(cdiv(2 * w.sms, base), Cf::MAX_SPLIT));
-    nsp = std::min(nsp, e.attn_max_split > 0 ? e.attn_max_split : 1);
+    // split-KV clusters for long-context iterations; each row uses only as
+    // many of the cluster's CTAs as give it >= attn_split_minpos positions.
+    // Measured (profiles/r02_attn_split.txt): 7B actor at ctx 2K, 16 rows,
+    // iteration 7.15 -> 5.86 ms; 0.5B at ctx 768, 32-64 rows, -4..-5.5%; a
+    // cluster launch at short contexts costs +5-16% (hence the host's
+    // per-iteration choice between the two graph variants)
+    // (only in long-context iterations, e.attn_long, and while the clustered
+    // grid stays within 2 CTAs per SM: larger clustered grids measured slower)
+    int nsp = std::max(1, std::min((2 * w.sms) / base, Cf::MAX_SPLIT));
+    nsp = std::min(nsp, e.attn_max_split > 0 ? e.attn_max_split : 8);
+    if (!e.attn_long) nsp = 1;
     const dim3 grid(R, d.n_kv_heads, nsp);
     auto* out = static_cast<__nv_bfloat16*>(w.attn);
     const auto* qkv = static_cast<const __nv_bfloat16*>(w.qkv);
@@ -501,10 +507,11 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     const int smem = early ? Cf::SMEM : Cf::SMEM_ALIAS;
     if (nsp > 1)
         launch_cluster_z(e.pdl, nsp, attn_dec<HD, NW, TPO>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias,
-                         qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
+                         qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early,
+                         e.attn_split_minpos);
     else
         launch(e.pdl, attn_dec<HD, NW, TPO>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias, qkv, out, kv,
-               layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early);
+               layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early, e.attn_split_minpos);
     e.launches += 1;
 }
 
@@ -862,6 +869,8 @@ Engine* engine_new(const oppo_engine_cfg& cfg) {
         e->attn_cluster = env_int("OPPO_ATTN_CLUSTER", 1) != 0;
         e->attn_per_sm = std::max(1, env_int("OPPO_ATTN_PER_SM", 4));
         e->attn_max_split = env_int("OPPO_ATTN_MAX_SPLIT", 0);
+        e->attn_split_minpos = std::max(1, env_int("OPPO_ATTN_SPLIT_MINPOS", 512));
+        e->attn_long_ctx = std::max(1, env_int("OPPO_ATTN_LONG_CTX", 768));
         e->debug_skip = env_int("OPPO_DEBUG_SKIP", 0);
         e->attn_fused = env_int("OPPO_ATTN_FUSED", 1) != 0;
         e->lmhead_dec_max = env_int("OPPO_LMHEAD_DEC_MAX", 32);  // measured crossover ~40 rows
@@ -1348,38 +1357,44 @@ void decode_iteration(Engine& e, int M, cudaStream_t st) {
 // One decode iteration for batch size M: replay the captured graph (capture on
 // first use).  Host cost per iteration is one cudaGraphLaunch.
 template <class T>
-cudaGraphExec_t ensure_decode_graph(Engine& e, int M, cudaStream_t st) {
-    auto it = e.decode_graphs.find(M);
+cudaGraphExec_t ensure_decode_graph(Engine& e, int M, cudaStream_t st, bool long_ctx) {
+    const int key = 2 * M + (long_ctx ? 1 : 0);  // two variants per bucket: split-KV attention or not
+    auto it = e.decode_graphs.find(key);
     if (it == e.decode_graphs.end()) {
         const int64_t before = e.launches;
         cudaGraph_t g;
+        e.attn_long = long_ctx;
         OPPO_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
             decode_iteration<T>(e, M, st);
         } catch (...) {
             cudaStreamEndCapture(st, &g);
+            e.attn_long = false;
             throw;
         }
+        e.attn_long = false;
         OPPO_CUDA_CHECK(cudaStreamEndCapture(st, &g));
         cudaGraphExec_t ge;
         OPPO_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
         OPPO_CUDA_CHECK(cudaGraphDestroy(g));
         OPPO_CUDA_CHECK(cudaGraphUpload(ge, st));  // device-side setup now, not at the first launch
-        it = e.decode_graphs.emplace(M, ge).first;
-        e.decode_graph_launches[M] = e.launches - before;
+        it = e.decode_graphs.emplace(key, ge).first;
+        e.decode_graph_launches[key] = e.launches - before;
         e.launches = before;
     }
     return it->second;
 }
 
 template <class T>
-void decode_iteration_graph(Engine& e, int M, cudaStream_t st) {
+void decode_iteration_graph(Engine& e, int M, cudaStream_t st, bool long_ctx) {
     if (!e.cfg.use_graphs) {
+        e.attn_long = long_ctx;
         decode_iteration<T>(e, M, st);
+        e.attn_long = false;
         return;
     }
-    OPPO_CUDA_CHECK(cudaGraphLaunch(ensure_decode_graph<T>(e, M, st), st));
-    e.launches += e.decode_graph_launches[M];
+    OPPO_CUDA_CHECK(cudaGraphLaunch(ensure_decode_graph<T>(e, M, st, long_ctx), st));
+    e.launches += e.decode_graph_launches[2 * M + (long_ctx ? 1 : 0)];
 }
 
 // ------------------------------------ policy log-probs of the finished sequences
@@ -1632,7 +1647,13 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
         // uploaded) before a scorer kernel starts polling: first-time setup of a
         // graph or kernel must not wait behind a spinning poller
         const int top = std::min(cdiv(static_cast<int64_t>(n_dec), 16) * 16, e.S + 16);
-        for (int bkt = 16; bkt <= top; bkt += 16) ensure_decode_graph<T>(e, bkt, e.sa);
+        bool any_long = false;  // can an iteration of this step reach the long-context variant
+        for (size_t r = 0; r < n_dec; ++r)
+            any_long |= dseq[r].prompt_len + dseq[r].target_len >= e.attn_long_ctx;
+        for (int bkt = 16; bkt <= top; bkt += 16) {
+            ensure_decode_graph<T>(e, bkt, e.sa, false);
+            if (any_long && e.attn_max_split != 1) ensure_decode_graph<T>(e, bkt, e.sa, true);
+        }
     }
     std::vector<uint32_t> wave_seq(waves.size());
     for (size_t k = 0; flags && k < waves.size(); ++k) wave_seq[k] = ++e.ready_seq;
@@ -1701,15 +1722,20 @@ void run_step_impl(Engine& e, const std::vector<oppo_seq_state>& active, int chu
         while (active_n > 0 && rem_sorted[active_n - 1] < it) --active_n;
         if (active_n == 0) break;
         loop_w += w_bytes;
+        int64_t ctx_max = 0;
         for (size_t r = 0; r < active_n; ++r) {
             const DecodeSeq& q = dseq[r];
-            loop_kv += kvb * static_cast<double>(q.prompt_len + q.generated + it);  // ctx + appended row
-            loop_f += 2.0 * p_dec + att_f * static_cast<double>(q.prompt_len + q.generated + it);
+            const int64_t ctx = q.prompt_len + q.generated + it;
+            loop_kv += kvb * static_cast<double>(ctx);  // ctx + appended row
+            loop_f += 2.0 * p_dec + att_f * static_cast<double>(ctx);
+            ctx_max = std::max(ctx_max, ctx);
         }
+        // long-context iteration: split-KV decode attention (graph variant)
+        const bool long_ctx = e.attn_max_split != 1 && ctx_max >= e.attn_long_ctx;
         // bucketed batch: rows [active_n, bucket) decode into the scratch slot
         const int bucket = e.cfg.use_graphs ? std::min(cdiv(active_n, 16) * 16, e.S + 16)
                                             : static_cast<int>(active_n);
-        decode_iteration_graph<T>(e, bucket, e.sa);
+        decode_iteration_graph<T>(e, bucket, e.sa, long_ctx);
         decode_tokens += static_cast<int64_t>(active_n);
         if (it == t_end) OPPO_CUDA_CHECK(cudaEventRecord(e.ev_dec_end, e.sa));
         fire_waves_at(it);

@@ -194,7 +194,10 @@ struct Engine {
     // decode-path tuning (defaults measured on B200; OPPO_* env overrides for sweeps)
     bool attn_cluster = true;  // split-KV merge in DSMEM (else workspace + combine kernel)
     int attn_per_sm = 4;       // target decode attention CTAs per SM
-    int attn_max_split = 0;
+    int attn_max_split = 0;    // decode split-KV cluster size cap (0: default 8, 1: off)
+    int attn_split_minpos = 512;  // fewest context positions per split of a row
+    int attn_long_ctx = 768;      // iterations whose longest context reaches this use split-KV attention
+    bool attn_long = false;       // set while a long-context decode iteration is enqueued / captured
     int debug_skip = 0;
     bool attn_fused = true;
     int attn_warps = 0;        // decode attention warps per CTA (0 auto, 4 or 8)

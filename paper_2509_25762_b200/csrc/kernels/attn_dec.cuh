@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(32 * NW)
     attn_dec(const float* __restrict__ part, int n_part, size_t part_stride,
              const float* __restrict__ bias, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* out,
              KvView kv, int layer, int n_heads, const int32_t* __restrict__ slot_r,
-             const int32_t* __restrict__ pos_r, int rows, float theta, int early_tiles) {
+             const int32_t* __restrict__ pos_r, int rows, float theta, int early_tiles, int minpos) {
     using namespace am;
     using Cf = AttnDecCfg<HD, NW, TPO>;
     constexpr int TP = Cf::TP, LDS = Cf::LDS, NT = TP / 8, DT = HD / 8, NTH = Cf::THREADS;
@@ -71,7 +71,11 @@ __global__ void __launch_bounds__(32 * NW)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int slot = slot_r[r], pos = pos_r[r], ctx = pos + 1;
     const int nsp = gridDim.z, z = blockIdx.z;
-    const int slen = (ctx + nsp - 1) / nsp;
+    // this row's split count: at least minpos positions per split (a short
+    // context stays in one CTA; the cluster's other CTAs get empty ranges and
+    // only take part in the merge with m = -inf, l = 0)
+    const int want = max(1, min(nsp, (ctx + minpos - 1) / minpos));
+    const int slen = (ctx + want - 1) / want;
     const int p_begin = min(ctx, z * slen), p_end = min(ctx, p_begin + slen);
     const bool owner = pos >= p_begin && pos < p_end;  // this CTA appends the new k, v
 

@@ -21,9 +21,15 @@ import torch.multiprocessing as mp  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
-# one attention split for every batch size: identical per-row decode arithmetic
-# on the 4-row shards and the 8-row union (row-independent fp32 path)
-os.environ["OPPO_ATTN_MAX_SPLIT"] = "1"
+
+
+@pytest.fixture(autouse=True)
+def _one_attention_split(monkeypatch):
+    """One attention split for every batch size: identical per-row decode
+    arithmetic on the 4-row shards and the 8-row union (row-independent fp32
+    path).  Set per test (spawned ranks inherit it), not at import, so the
+    other modules of the session keep the default split rule."""
+    monkeypatch.setenv("OPPO_ATTN_MAX_SPLIT", "1")
 LENS = [9, 14, 5, 20, 11, 7, 16, 12]
 P, CHUNK = 8, 8
 

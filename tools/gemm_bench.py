@@ -11,6 +11,9 @@ L = lib()
 # name, N, K, copies, epilogue (0 store, 1 add f32, 2 swiglu, 3 logits)
 SHAPES = [("qkv", 1152, 896, 24, 0), ("o", 896, 896, 24, 1), ("gate|up", 9728, 896, 24, 2),
           ("down", 896, 4864, 24, 1), ("lm_head", 151936, 896, 3, 3)]
+if os.environ.get("SHAPE") == "7b":  # 7B actor (cfg4 / cfg5) decode projections
+    SHAPES = [("qkv", 4608, 3584, 3, 0), ("o", 3584, 3584, 3, 1), ("gate|up", 37888, 3584, 3, 2),
+              ("down", 3584, 18944, 3, 1)]
 if os.environ.get("DEC", "1") == "1":  # decode GEMM (gemm_dec): 16 partials, 17 SwiGLU
     SHAPES = [(n, N, K, c, {0: 16, 1: 16, 2: 17}.get(e, e)) for n, N, K, c, e in SHAPES]
 if os.environ.get("PREFILL") == "1":  # scorer prefill pass shapes (token-tiled kernels)
@@ -28,7 +31,7 @@ for M in Ms:
             continue
         byts = N * K * 2 + M * K * 2
         fl = 2.0 * M * N * K
-        mult = 1 if name == "lm_head" else 24
+        mult = 1 if name == "lm_head" else (28 if os.environ.get("SHAPE") == "7b" else 24)
         tot[M] = tot.get(M, 0.0) + mult * us.value
         print(f"M={M:4d} {name:8s} {us.value:9.2f} us {byts/us.value/1e3:8.1f} GB/s "
               f"{fl/us.value/1e6:8.1f} TFLOP/s", flush=True)
