@@ -494,7 +494,8 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     // per-iteration choice between the two graph variants)
     // (only in long-context iterations, e.attn_long, and while the clustered
     // grid stays within 2 CTAs per SM: larger clustered grids measured slower)
-    int nsp = std::max(1, std::min((2 * w.sms) / base, Cf::MAX_SPLIT));
+    const int resident = std::max(1, std::min(2, (227 * 1024) / Cf::SMEM));  // CTAs per SM (shared memory)
+    int nsp = std::max(1, std::min((resident * w.sms) / base, Cf::MAX_SPLIT));
     nsp = std::min(nsp, e.attn_max_split > 0 ? e.attn_max_split : 8);
     if (!e.attn_long) nsp = 1;
     const dim3 grid(R, d.n_kv_heads, nsp);
@@ -537,7 +538,14 @@ void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
             attn_dec_launch_hd<64, 4, 16>(e, m, w, st, layer, R, part, n_part, bias);
         else attn_dec_launch_hd<64, 4>(e, m, w, st, layer, R, part, n_part, bias);
         break;
-    default: attn_dec_launch_hd<128, 4>(e, m, w, st, layer, R, part, n_part, bias); break;
+    default:
+        // head_dim 128 (the 7B actor): 8 warps (149 KB, one CTA per SM) while
+        // the unsplit grid fits one wave: twice the K/V tiles in flight per row
+        if (e.attn_warps == 8 || (e.attn_warps == 0 && R * m.dims.n_kv_heads <= w.sms))
+            attn_dec_launch_hd<128, 8>(e, m, w, st, layer, R, part, n_part, bias);
+        else
+            attn_dec_launch_hd<128, 4>(e, m, w, st, layer, R, part, n_part, bias);
+        break;
     }
 }
 
