@@ -271,6 +271,40 @@ def test_gqa_05b_width_bf16_vs_oracle(attn_env):
     eng.close()
 
 
+@pytest.mark.parametrize("split", ["", "1"], ids=["split_kv", "one_cta"])
+@pytest.mark.parametrize("hd", [64, 128])
+def test_long_context_split_kv_decode_vs_oracle(hd, split):
+    """Long-context decode iterations (longest context >= OPPO_ATTN_LONG_CTX,
+    768) run the split-KV graph variant: the KV range of a row is split over
+    a cluster of CTAs (>= 512 positions each) merged through DSMEM.  Prompts of
+    800 tokens, head_dim 64 (0.5B width, G=7) and 128 (G=4), against the fp64
+    oracle; OPPO_ATTN_MAX_SPLIT=1 forces one CTA per row for comparison."""
+    import os
+    if hd == 64:
+        shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
+                     vocab=1024, tied=1)
+    else:
+        shape = dict(n_layers=2, d_model=1024, n_heads=8, n_kv_heads=2, head_dim=128, d_ff=2816,
+                     vocab=1024, tied=1)
+    P, C = 800, 16
+    lens = [20, 35, 12, 28]
+    if split:
+        os.environ["OPPO_ATTN_MAX_SPLIT"] = split
+    try:
+        eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=48,
+                     sample_seed=SAMPLE_SEED)
+    finally:
+        os.environ.pop("OPPO_ATTN_MAX_SPLIT", None)
+    st = fresh_states(len(lens), P, lens)
+    eng.admit(st)
+    eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
+    orc = oracles(eng)
+    for s in st:
+        check_rollout(eng, orc, s["id"], P, tol_lp=0.15, tol_val=0.2, margin_tol=0.2,
+                      strict_tokens=False)
+    eng.close()
+
+
 @pytest.mark.parametrize("hd", [64, 128])
 def test_rope_append_epilogue_matches_separate_kernel(hd):
     """Prefill q|k|v projection with RoPE + paged KV append in the GEMM

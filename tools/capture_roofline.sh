@@ -8,6 +8,9 @@
 # ncu numbers are serialised and cache-flushed per kernel: shares and bytes,
 # never bench values.
 set -u
+# ncu serialises kernels: a scorer-stream poller (device chunk-ready flags)
+# would wait forever for a flag set by a later kernel -> per-wave events
+export OPPO_CHUNK_FLAGS=0
 OUT=gpurun_out/roof
 mkdir -p $OUT
 PEAK=$(python -c "import json;print(json.load(open('MEASURED_PEAKS.json'))['hbm_gbs'])" 2>/dev/null || echo 6650)
