@@ -274,11 +274,13 @@ def test_gqa_05b_width_bf16_vs_oracle(attn_env):
 @pytest.mark.parametrize("split", ["", "1"], ids=["split_kv", "one_cta"])
 @pytest.mark.parametrize("hd", [64, 128])
 def test_long_context_split_kv_decode_vs_oracle(hd, split):
-    """Long-context decode iterations (longest context >= OPPO_ATTN_LONG_CTX,
-    768) run the split-KV graph variant: the KV range of a row is split over
-    a cluster of CTAs (>= 512 positions each) merged through DSMEM.  Prompts of
-    800 tokens, head_dim 64 (0.5B width, G=7) and 128 (G=4), against the fp64
-    oracle; OPPO_ATTN_MAX_SPLIT=1 forces one CTA per row for comparison."""
+    """Long-context decode iterations (longest context >= OPPO_ATTN_LONG_CTX)
+    run the split-KV graph variant: the KV range of a row is split over a
+    cluster of CTAs (>= OPPO_ATTN_SPLIT_MINPOS positions each) merged through
+    DSMEM.  The thresholds are scaled down here (64 / 32 instead of 768 / 512)
+    so 96-token prompts take the split path and the fp64 oracle stays fast;
+    head_dim 64 (0.5B width, G=7) and 128 (G=4); OPPO_ATTN_MAX_SPLIT=1 forces
+    one CTA per row for comparison."""
     import os
     if hd == 64:
         shape = dict(n_layers=2, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64, d_ff=4864,
@@ -286,15 +288,18 @@ def test_long_context_split_kv_decode_vs_oracle(hd, split):
     else:
         shape = dict(n_layers=2, d_model=1024, n_heads=8, n_kv_heads=2, head_dim=128, d_ff=2816,
                      vocab=1024, tied=1)
-    P, C = 800, 16
+    P, C = 96, 16
     lens = [20, 35, 12, 28]
+    env = {"OPPO_ATTN_LONG_CTX": "64", "OPPO_ATTN_SPLIT_MINPOS": "32"}
     if split:
-        os.environ["OPPO_ATTN_MAX_SPLIT"] = split
+        env["OPPO_ATTN_MAX_SPLIT"] = split
+    os.environ.update(env)
     try:
         eng = Engine(shape, dtype=abi.DTYPE_BF16, max_slots=8, max_prompt_len=P, max_response_len=48,
                      sample_seed=SAMPLE_SEED)
     finally:
-        os.environ.pop("OPPO_ATTN_MAX_SPLIT", None)
+        for k in env:
+            os.environ.pop(k, None)
     st = fresh_states(len(lens), P, lens)
     eng.admit(st)
     eng.run_step(st, C, abi.MODE_STREAMED, len(lens))
