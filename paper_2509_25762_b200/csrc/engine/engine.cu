@@ -472,15 +472,15 @@ void attn_mma_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
 
 // Decode attention with RoPE + KV append fused (attn_dec.cuh), bf16.  The
 // qkv row comes from the decode GEMM's partials (n_part > 0) or a bf16 row.
-template <int HD, int NW, int TPO = 0, int ST = 2>
+template <int HD, int NW, int TPO = 0>
 void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int layer, int R,
                         const float* part, int n_part, const float* bias) {
-    using Cf = AttnDecCfg<HD, NW, TPO, ST>;
+    using Cf = AttnDecCfg<HD, NW, TPO>;
     static std::once_flag attr;
     std::call_once(attr, [] {
-        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW, TPO, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW, TPO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              Cf::SMEM));
-        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW, TPO, ST>,
+        OPPO_CUDA_CHECK(cudaFuncSetAttribute(attn_dec<HD, NW, TPO>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     });
     const auto& d = m.dims;
@@ -507,11 +507,11 @@ void attn_dec_launch_hd(Engine& e, const Model& m, Work& w, cudaStream_t st, int
     const int early = base * nsp <= 2 * w.sms ? 1 : 0;
     const int smem = early ? Cf::SMEM : Cf::SMEM_ALIAS;
     if (nsp > 1)
-        launch_cluster_z(e.pdl, nsp, attn_dec<HD, NW, TPO, ST>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias,
+        launch_cluster_z(e.pdl, nsp, attn_dec<HD, NW, TPO>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias,
                          qkv, out, kv, layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early,
                          e.attn_split_minpos);
     else
-        launch(e.pdl, attn_dec<HD, NW, TPO, ST>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias, qkv, out, kv,
+        launch(e.pdl, attn_dec<HD, NW, TPO>, grid, dim3(Cf::THREADS), smem, st, part, n_part, pstride, bias, qkv, out, kv,
                layer, d.n_heads, w.meta.slot, w.meta.pos, R, kRopeTheta, early, e.attn_split_minpos);
     e.launches += 1;
 }
@@ -539,11 +539,10 @@ void attn_dec_launch(Engine& e, const Model& m, Work& w, cudaStream_t st, int la
         else attn_dec_launch_hd<64, 4>(e, m, w, st, layer, R, part, n_part, bias);
         break;
     default:
-        // head_dim 128 (the 7B actor): 8 warps with a 3-tile K/V ring per warp
-        // (217 KB, one CTA per SM) while the unsplit grid fits one wave: 4x the
-        // K/V bytes in flight per row of the 4-warp double-buffered variant
+        // head_dim 128 (the 7B actor): 8 warps (149 KB, one CTA per SM) while
+        // the unsplit grid fits one wave: twice the K/V tiles in flight per row
         if (e.attn_warps == 8 || (e.attn_warps == 0 && R * m.dims.n_kv_heads <= w.sms))
-            attn_dec_launch_hd<128, 8, 0, 3>(e, m, w, st, layer, R, part, n_part, bias);  // 3-tile ring, 217 KB
+            attn_dec_launch_hd<128, 8>(e, m, w, st, layer, R, part, n_part, bias);
         else
             attn_dec_launch_hd<128, 4>(e, m, w, st, layer, R, part, n_part, bias);
         break;

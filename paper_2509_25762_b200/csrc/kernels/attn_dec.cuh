@@ -26,16 +26,15 @@
 
 namespace oppo {
 
-template <int HD, int NW = 4, int TPO = 0, int ST = 2>
+template <int HD, int NW = 4, int TPO = 0>
 struct AttnDecCfg {
     static constexpr int WARPS = NW;
-    static constexpr int STAGES = ST;  // cp.async K/V ring depth per warp
     static constexpr int THREADS = 32 * NW;
     // positions per warp tile (8 warps: half-size tiles, same shared memory;
     // TPO = 16 with 4 warps: half the shared memory, more resident CTAs)
     static constexpr int TP = TPO ? TPO : ((HD >= 128 || NW == 8) ? 16 : 32);
     static constexpr int LDS = HD + 8;              // padded smem row (elements)
-    static constexpr int WARP_BYTES = ST * 2 * TP * LDS * 2;  // K,V ring of ST tiles
+    static constexpr int WARP_BYTES = 2 * 2 * TP * LDS * 2;  // K,V double buffer
     static constexpr int SLOT = 16 * HD + 32;                // merge partial (floats)
     static constexpr int QBYTES = 16 * LDS * 2;
     // fp32 q/k/v staging of phase 1 (own region: the first K/V tiles load meanwhile)
@@ -49,14 +48,14 @@ struct AttnDecCfg {
                                                                               : (NW * WARP_BYTES) / (NW * SLOT * 4);
 };
 
-template <int HD, int NW, int TPO = 0, int ST = 2>
+template <int HD, int NW, int TPO = 0>
 __global__ void __launch_bounds__(32 * NW)
     attn_dec(const float* __restrict__ part, int n_part, size_t part_stride,
              const float* __restrict__ bias, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* out,
              KvView kv, int layer, int n_heads, const int32_t* __restrict__ slot_r,
              const int32_t* __restrict__ pos_r, int rows, float theta, int early_tiles, int minpos) {
     using namespace am;
-    using Cf = AttnDecCfg<HD, NW, TPO, ST>;
+    using Cf = AttnDecCfg<HD, NW, TPO>;
     constexpr int TP = Cf::TP, LDS = Cf::LDS, NT = TP / 8, DT = HD / 8, NTH = Cf::THREADS;
     extern __shared__ __align__(128) uint8_t adsm[];
     uint8_t* kvbuf = adsm;                                                     // 4 warps x K/V x 2
@@ -85,7 +84,7 @@ __global__ void __launch_bounds__(32 * NW)
     // qkv fold / RoPE / append below (a tile holding `pos` waits for the append)
     const int lane_ = tid & 31;
     auto sK = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES);
-    auto sV = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES + ST * TP * LDS * 2);
+    auto sV = reinterpret_cast<__nv_bfloat16(*)[TP][LDS]>(kvbuf + warp * Cf::WARP_BYTES + 2 * TP * LDS * 2);
     const __nv_bfloat16* kc = static_cast<const __nv_bfloat16*>(kv.k);
     const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(kv.v);
     auto load_tile = [&](int buf, int t0) {
@@ -178,26 +177,12 @@ __global__ void __launch_bounds__(32 * NW)
     for (int d = 0; d < DT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     int buf = 0;
     if (!early && first < p_end) load_tile(0, first);
-    // ring of ST tiles per warp: tiles i+1 .. i+ST-1 in flight while tile i
-    // is consumed (one commit group per tile; empty groups past the range
-    // keep the group count uniform for cp.async.wait_group)
-    for (int k = 1; k < ST - 1; ++k) {
-        if (first + k * NW * TP < p_end) load_tile(k, first + k * NW * TP);
-        else cp_async_commit();
-    }
     for (int t0 = first; t0 < p_end; t0 += NW * TP) {
-        if constexpr (ST == 2) {
-            if (t0 + NW * TP < p_end) {
-                load_tile(buf ^ 1, t0 + NW * TP);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
+        if (t0 + NW * TP < p_end) {
+            load_tile(buf ^ 1, t0 + NW * TP);
+            cp_async_wait<1>();
         } else {
-            const int nxt = t0 + (ST - 1) * NW * TP;
-            if (nxt < p_end) load_tile((buf + ST - 1) % ST, nxt);
-            else cp_async_commit();
-            cp_async_wait<ST - 1>();
+            cp_async_wait<0>();
         }
         __syncwarp();
         float s[NT][4];
@@ -266,10 +251,9 @@ __global__ void __launch_bounds__(32 * NW)
                 mma16816(o[d + 1], pa[kk], b[2], b[3]);
             }
         }
-        __syncwarp();  // the buffer is refilled ST tiles later
-        buf = ST == 2 ? buf ^ 1 : (buf + 1) % ST;
+        __syncwarp();  // the buffer is refilled two tiles later
+        buf ^= 1;
     }
-    if constexpr (ST > 2) cp_async_wait<0>();  // (only empty groups can remain)
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
