@@ -284,7 +284,7 @@ def decode_roofline(recs, hbm_peak, peak_src, actor):
            "peak_source": peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
            "timing": "CUDA events on the actor stream around each step's decode loop"}
     caps = []
-    for m in (64, 128, 256):
+    for m in (16, 64, 128, 256):
         path = os.path.join(ROOT, "profiles", f"r02_decode_traffic_{actor}_M{m}.json")
         if os.path.exists(path):
             caps.append((abs(m - rows), m, path))
